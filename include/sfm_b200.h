@@ -1,0 +1,267 @@
+/*
+ * sfm_b200.h -- C-ABI of the B200-native LM bundle-adjustment / triangulation
+ * core (libsfm_b200.so).  Plain pointers and sizes only; every array is
+ * host memory owned by the caller (C-contiguous, fp64 / int32 / int64 / u8),
+ * copied to context-owned device memory inside the call.  No pointer is
+ * retained after a call returns.
+ *
+ * Each entry point replaces one function of the reference Python package
+ * (`sfmkit`, /root/reference/pkg/src/sfmkit); the citation above each
+ * declaration names the reference interface it stands in for.  The Python
+ * drop-in layer (paper_2510_15271_b200/mapping.py) flattens the reference's
+ * object model into the arrays below and maps the return codes back onto the
+ * reference's exception classes (errors.py).
+ *
+ * Return codes: 0 = OK, negative = error (see SFM_E_*); a human-readable
+ * message with the payload the reference puts in its exception text is
+ * available from sfm_last_error(ctx).
+ */
+#ifndef SFM_B200_H
+#define SFM_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SFM_ABI_VERSION 1
+
+/* ---- error codes (mapped to sfmkit.errors classes by the Python layer) --- */
+#define SFM_OK 0
+#define SFM_E_INVALID (-1)            /* ValueError: malformed arguments      */
+#define SFM_E_NON_POSITIVE_DEPTH (-2) /* NonPositiveDepth   cameras.py:132-133 */
+#define SFM_E_OUT_OF_MODEL_DOMAIN (-3)/* OutOfModelDomain   cameras.py:68-69   */
+#define SFM_E_SOLVER_DIVERGED (-4)    /* SolverDiverged     solver.py:247-248  */
+#define SFM_E_UNDISTORT_DIVERGED (-5) /* UndistortDiverged  cameras.py:119-125 */
+#define SFM_E_CUDA (-10)              /* CUDA runtime failure                  */
+#define SFM_E_NCCL (-11)              /* NCCL failure                          */
+#define SFM_E_OOM (-12)               /* device allocation failure             */
+
+/* ---- per-track triangulation status codes (sfm_tri_output.status) ------- */
+#define SFM_TRI_OK 0
+#define SFM_TRI_INSUFFICIENT_PARALLAX 1 /* InsufficientParallax mapping.py:205-207, :217-218 */
+#define SFM_TRI_CHEIRALITY 2            /* CheiralityViolation  mapping.py:186-191 */
+#define SFM_TRI_PARALLEL_RAYS 3         /* ParallelRays         mapping.py:236-237 */
+#define SFM_TRI_TOO_FEW_OBS 4           /* ValueError           mapping.py:202-203 */
+#define SFM_TRI_CAMERA_ERROR 5          /* unproject raised (UndistortDiverged / OutOfModelDomain) */
+#define SFM_TRI_FAILED 6                /* ransac: track.status = FAILED mapping.py:286-303 */
+#define SFM_TRI_SKIPPED 7               /* track not active (not PENDING)       */
+
+/* ---- camera models: cameras.py:35-54 -------------------------------------- */
+#define SFM_CAM_PINHOLE 0
+#define SFM_CAM_PINHOLE_RADIAL 1
+#define SFM_CAM_EQUIDISTANT_FISHEYE 2
+
+typedef struct {
+  int32_t kind;     /* SFM_CAM_*                                   */
+  int32_t width;
+  int32_t height;
+  int32_t _pad;
+  double fx, fy, cx, cy;
+  double k1, k2;    /* radial distortion (PINHOLE_RADIAL only)     */
+} sfm_camera_model;
+
+/* ---- robust losses: solver.py:25-51 -------------------------------------- */
+#define SFM_LOSS_TRIVIAL 0
+#define SFM_LOSS_HUBER 1
+#define SFM_LOSS_CAUCHY 2
+
+/* ---- linear solver for the reduced camera system ------------------------ */
+#define SFM_LINSOLVE_AUTO 0   /* dense Cholesky when small, PCG otherwise */
+#define SFM_LINSOLVE_DENSE 1  /* on-device dense Cholesky of S            */
+#define SFM_LINSOLVE_PCG 2    /* block-Jacobi PCG on S                    */
+
+/* ---- termination codes: solver.py:194-257 (SolverReport.termination) ---- */
+#define SFM_TERM_MAX_ITERATIONS 0
+#define SFM_TERM_GRADIENT_TOLERANCE 1
+#define SFM_TERM_NO_DECREASE 2
+#define SFM_TERM_PARAMETER_TOLERANCE 3
+#define SFM_TERM_COST_ZERO 4
+#define SFM_TERM_ALL_FIXED 5
+
+typedef struct sfm_ctx sfm_ctx;
+
+/*
+ * Flattened bundle-adjustment problem: the array layout mapping.py:390-509
+ * builds as closures.  Frames are `sorted(keyframes)`; points are the
+ * TRIANGULATED landmarks in map order; observations are every inlier
+ * observation, landmark-major in track order (the reference residual order,
+ * mapping.py:452-475), so `obs_point` is non-decreasing.
+ * Pose terms: lambda_c sequential edges (frame index pairs, measurement taken
+ * from the entry poses on device, mapping.py:477-498) and lambda_a absolute
+ * priors (frame indices, anchored at the entry poses, mapping.py:500-509).
+ * Under point-sharding each rank passes only its points/observations and
+ * rank 0 alone passes the pose terms.
+ */
+typedef struct {
+  int32_t n_frames;
+  int32_t n_models;
+  const double* cam_q;          /* [n_frames,4] unit quaternion (w,x,y,z)  */
+  const double* cam_t;          /* [n_frames,3] cam_from_world translation */
+  const int32_t* frame_model;   /* [n_frames] index into models            */
+  const uint8_t* frame_fixed;   /* [n_frames] 1 = fixed block              */
+  const sfm_camera_model* models;
+  int64_t n_points;
+  const double* points;         /* [n_points,3]                            */
+  int64_t n_obs;
+  const int32_t* obs_frame;     /* [n_obs]                                 */
+  const int32_t* obs_point;     /* [n_obs] non-decreasing                  */
+  const double* obs_uv;         /* [n_obs,2] measured pixel                */
+  int32_t n_edges;
+  int32_t n_priors;
+  const int32_t* edge_ab;       /* [n_edges,2] frame indices (a, b)        */
+  const int32_t* prior_frame;   /* [n_priors]                              */
+  double edge_weight;           /* lambda_c  (information = lambda_c * I)  */
+  double prior_weight;          /* lambda_a                                */
+  int64_t obs_offset;           /* global index of obs 0 (sharding)        */
+  int64_t n_params_global;      /* 6*free frames + 3*all points (0 = local) */
+} sfm_ba_problem;
+
+/* SolverOptions (solver.py:81-87) + the robust loss + B200 solver knobs. */
+typedef struct {
+  int32_t loss_kind;
+  int32_t max_iters;
+  double loss_param;
+  double grad_tol;
+  double param_tol;
+  double initial_lambda;
+  double max_lambda;
+  int32_t linear_solver;      /* SFM_LINSOLVE_*                           */
+  int32_t pcg_max_iters;
+  double pcg_rtol;            /* relative residual tolerance of PCG       */
+  int32_t dense_max_dim;      /* AUTO: dense Cholesky when 6*free <= this */
+  int32_t _pad;
+} sfm_ba_options;
+
+/* SolverReport (solver.py:90-95) + device-side statistics. */
+typedef struct {
+  double initial_cost;
+  double final_cost;
+  int32_t iterations;
+  int32_t termination;        /* SFM_TERM_*                                */
+  int32_t n_trials;           /* linear solves (accepted + rejected)       */
+  int32_t pcg_iterations;     /* summed over trials                        */
+  double final_lambda;
+  double device_ms;           /* CUDA-event time of the LM loop            */
+  int64_t kernel_launches;    /* kernels launched during the call          */
+  int64_t n_blocks_S;         /* stored 6x6 blocks of S (both triangles)   */
+} sfm_ba_report;
+
+/* ---- context ------------------------------------------------------------ */
+int sfm_abi_version(void);
+/* 128-byte NCCL unique id for rank 0 to broadcast (torch.distributed). */
+int sfm_nccl_unique_id(uint8_t out[128]);
+/* world == 1: nccl_id may be NULL.  device = CUDA ordinal used by this rank. */
+int sfm_ctx_create(int32_t device, int32_t rank, int32_t world,
+                   const uint8_t* nccl_id, sfm_ctx** out);
+void sfm_ctx_destroy(sfm_ctx* ctx);
+const char* sfm_last_error(const sfm_ctx* ctx);
+/* Per-kernel CUDA-event timing (bench / roofline).  Off by default. */
+int sfm_set_profiling(sfm_ctx* ctx, int32_t enabled);
+int sfm_prof_count(const sfm_ctx* ctx);
+int sfm_prof_get(const sfm_ctx* ctx, int32_t i, const char** name,
+                 int64_t* launches, double* total_ms, double* bytes);
+int sfm_prof_reset(sfm_ctx* ctx);
+
+/* ---- bundle adjustment -------------------------------------------------- */
+/*
+ * Replaces solver.solve (solver.py:194-257) as driven by
+ * mapping.bundle_adjust (mapping.py:390-527).  Reads the initial state from
+ * `prob`, runs LM on device, writes the final poses/points into
+ * out_cam_q/out_cam_t/out_points (same shapes as the inputs; fixed frames are
+ * copied bit-identically) and fills `report`.  On SFM_E_NON_POSITIVE_DEPTH the
+ * outputs are left untouched (the reference raises before writing back).
+ */
+int sfm_ba_solve(sfm_ctx* ctx, const sfm_ba_problem* prob,
+                 const sfm_ba_options* opt, double* out_cam_q,
+                 double* out_cam_t, double* out_points, sfm_ba_report* report);
+
+/* Stepwise form of sfm_ba_solve for device-resident benchmarking:
+ * setup uploads + builds structure and evaluates the initial cost;
+ * iterate runs up to n LM iterations continuing the same solve;
+ * download copies the current state out. */
+int sfm_ba_setup(sfm_ctx* ctx, const sfm_ba_problem* prob,
+                 const sfm_ba_options* opt);
+int sfm_ba_iterate(sfm_ctx* ctx, int32_t n_iters, sfm_ba_report* report);
+int sfm_ba_download(sfm_ctx* ctx, double* out_cam_q, double* out_cam_t,
+                    double* out_points);
+
+/*
+ * Parity/debug: Problem.evaluate (solver.py:132-142) + _assemble
+ * (solver.py:164-191) restricted to the reprojection residuals: robust cost
+ * per observation, weighted residual r~ [n_obs,2], weighted pose Jacobian
+ * J~_c [n_obs,2,6] and point Jacobian J~_p [n_obs,2,3] (any output may be
+ * NULL).  Fixed frames still get their J~_c here.
+ */
+int sfm_ba_eval(sfm_ctx* ctx, const sfm_ba_problem* prob, int32_t loss_kind,
+                double loss_param, double* out_cost_per_obs, double* out_res,
+                double* out_jc, double* out_jp);
+
+/* ---- triangulation / gating --------------------------------------------- */
+/*
+ * Tracks as CSR: observations of track i are [track_ptr[i], track_ptr[i+1]),
+ * in track order; obs_frame indexes the frame arrays (cam_q/cam_t/
+ * frame_model).  `active` (may be NULL = all) selects the tracks to process
+ * (PENDING tracks in iterative_map, mapping.py:600-602).
+ */
+typedef struct {
+  int32_t n_frames;
+  int32_t n_models;
+  const double* cam_q;
+  const double* cam_t;
+  const int32_t* frame_model;
+  const sfm_camera_model* models;
+  int64_t n_tracks;
+  int64_t n_obs;
+  const int64_t* track_ptr;     /* [n_tracks+1]                             */
+  const int32_t* obs_frame;     /* [n_obs]                                  */
+  const double* obs_uv;         /* [n_obs,2]                                */
+  const uint8_t* active;        /* [n_tracks] or NULL                       */
+} sfm_tracks;
+
+#define SFM_TRI_DLT 0
+#define SFM_TRI_MIDPOINT 1
+
+/*
+ * Replaces ransac_triangulate (mapping.py:255-305) for every active track:
+ * exhaustive i<j pair hypotheses, strict `<` inlier test, lexicographic
+ * (count, -sum err) score with first-best, refine on inliers, final mask.
+ * Outputs: out_X [n_tracks,3], out_mask [n_obs] (u8), out_status [n_tracks]
+ * (SFM_TRI_OK or SFM_TRI_FAILED; SFM_TRI_SKIPPED for inactive tracks).
+ */
+int sfm_ransac_triangulate(sfm_ctx* ctx, const sfm_tracks* tracks,
+                           double threshold_px, double min_angle,
+                           int32_t method, double* out_X, uint8_t* out_mask,
+                           int8_t* out_status);
+
+/*
+ * Replaces triangulate_dlt (mapping.py:194-221) / triangulate_midpoint
+ * (mapping.py:224-240) over all observations of each track (batched):
+ * out_status carries the exception the reference would raise per track.
+ */
+int sfm_triangulate(sfm_ctx* ctx, const sfm_tracks* tracks, double min_angle,
+                    int32_t method, double* out_X, int8_t* out_status);
+
+/*
+ * Replaces remove_outliers (mapping.py:544-566) for the landmarks given as
+ * tracks (one track per TRIANGULATED landmark, all of its observations):
+ * an inlier observation with reprojection error > threshold (strict) is
+ * cleared in mask_inout; out_inliers[i] = surviving inlier count of landmark
+ * i (< 2 means demote to PENDING); *out_removed = cleared count.
+ */
+int sfm_gate(sfm_ctx* ctx, const sfm_tracks* tracks, const double* points,
+             double threshold_px, uint8_t* mask_inout, int32_t* out_inliers,
+             int64_t* out_removed);
+
+/*
+ * reprojection_error (mapping.py:243-252) for every observation of every
+ * track against points [n_tracks,3] (inf where projection raises).
+ */
+int sfm_reprojection_errors(sfm_ctx* ctx, const sfm_tracks* tracks,
+                            const double* points, double* out_err);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SFM_B200_H */

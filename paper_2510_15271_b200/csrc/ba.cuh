@@ -1,0 +1,133 @@
+// ba.cuh -- device-resident Levenberg-Marquardt bundle adjustment.
+//
+// Replaces solver.solve (solver.py:194-257) as driven by bundle_adjust
+// (mapping.py:390-527): same residual set, robust IRLS weighting, Marquardt
+// damping D = max(diag H, 1e-12), lambda schedule and termination rules, but
+// the normal equations are reduced onto the cameras (Schur complement) and
+// solved on device (dense Cholesky when small, block-Jacobi PCG otherwise).
+// See DESIGN.md for the data layout and the kernel/roofline inventory.
+#pragma once
+#include "comm.cuh"
+#include "common.cuh"
+
+namespace sfm {
+
+inline double __longlong_as_double_host(unsigned long long b) {
+  double d;
+  std::memcpy(&d, &b, sizeof(d));
+  return d;
+}
+
+// Device scalars read back once per LM trial (one small D2H).
+struct BAScalars {
+  double cost;               // robust cost of the evaluated state (local part)
+  double dp2;                // sum |delta_p|^2 (local points)
+  double dc2;                // sum |delta_c|^2 (replicated cameras)
+  double bnorm2;             // |b_S|^2 (PCG)
+  unsigned long long gmax;   // bit pattern of max|g| (non-negative doubles)
+  unsigned long long depth_obs;  // min global obs index whose projection raised
+  int nonfinite;             // delta or Schur factor not finite / not PD
+  int pcg_iters;
+  int pcg_fail;
+  int proj_code;             // PROJ_* code of depth_obs (filled on demand)
+  double proj_depth;         // p_cam.z of depth_obs
+};
+
+class BASolver {
+ public:
+  BASolver(cudaStream_t s, Profiler* p, Comm* c) : stream_(s), prof_(p), comm_(c) {}
+  void setup(const sfm_ba_problem& prob, const sfm_ba_options& opt);
+  // Runs up to n LM iterations continuing the current solve.
+  void iterate(int n, sfm_ba_report* rep);
+  void download(double* q, double* t, double* X);
+  // Parity/debug evaluation of the reprojection residuals.
+  static void eval(cudaStream_t s, Profiler* p, const sfm_ba_problem& prob, int loss_kind,
+                   double loss_param, double* cost, double* res, double* jc, double* jp);
+  bool finished() const { return finished_; }
+
+ private:
+  // --- host-side control (solver.py:194-257) ---
+  double eval_cost_current();
+  void linearize();
+  bool trial(double lam, double* new_cost, double* step_norm);
+  void build_schur(double lam);
+  bool solve_reduced();
+  void raise_projection_error(bool trial_state);
+  void read_scalars();
+
+  cudaStream_t stream_;
+  Profiler* prof_;
+  Comm* comm_;
+  sfm_ba_options opt_{};
+  int rank_ = 0;
+
+  // dims
+  int F_ = 0, nfree_ = 0, nmodels_ = 0;
+  int64_t P_ = 0, N_ = 0;
+  int64_t obs_offset_ = 0;
+  int64_t n_params_ = 0;
+  int n_edges_ = 0, n_priors_ = 0;
+  double edge_w_ = 0.0, prior_w_ = 0.0;
+  bool has_residuals_ = false;
+
+  // LM state
+  bool finished_ = true;
+  double initial_cost_ = 0.0, cost_ = 0.0, lam_ = 0.0;
+  int iters_ = 0, term_ = SFM_TERM_MAX_ITERATIONS, n_trials_ = 0, pcg_total_ = 0;
+  int use_dense_ = 0;
+
+  // frames / models
+  DevBuf<sfm_camera_model> models_;
+  DevBuf<int> frame_model_, free_idx_, free_frame_;
+  DevBuf<double> q_[2], t_[2], Rt_[2];  // [F*4], [F*3], [F*12]; index cur_
+  DevBuf<double> X_[2];                 // [P*3]
+  int cur_ = 0;
+
+  // observations (point-major)
+  DevBuf<int> obs_frame_, obs_point_;
+  DevBuf<double> obs_uv_;   // [N*2]
+  DevBuf<int64_t> pt_ptr_;  // [P+1]
+
+  // pair structure (sorted by S block, then point)
+  int64_t n_pairs_ = 0;
+  int n_pb_ = 0, n_ub_ = 0, n_full_ = 0;
+  int64_t n_chunks_ = 0, n_diag_chunks_ = 0;
+  DevBuf<unsigned long long> pairs_;     // (obs_lo << 32) | obs_hi
+  DevBuf<int64_t> chunk_start_;          // [n_chunks+1] pair index
+  DevBuf<int> chunk_pb_;                 // [n_chunks] pair block
+  DevBuf<int64_t> diag_chunks_;          // [n_diag_chunks] chunk ids of diagonal blocks
+  DevBuf<int64_t> pb_chunk_ptr_;         // [n_pb+1]
+  DevBuf<unsigned long long> ub_key_;    // [n_ub] upper block keys lo*nfree+hi
+  DevBuf<int> ub_pb_;                    // [n_ub] pair block or -1
+  DevBuf<int> ub_edge_;                  // [n_ub] edge or -1
+  DevBuf<int> ub_pos_up_, ub_pos_lo_;    // [n_ub] BSR slots (lo = -1 on diagonal)
+  DevBuf<int> row_ptr_, col_idx_;        // BSR full pattern
+  DevBuf<double> chunk_buf_;             // [n_chunks*42]
+
+  // pose terms
+  DevBuf<int> edge_ab_, prior_frame_;
+  DevBuf<double> edge_meas_inv_;         // [E*7] q(4) t(3) of meas^-1
+  DevBuf<double> prior_init_inv_;        // [A*7]
+  DevBuf<int> term_ptr_, term_list_;     // per free camera incident terms
+  DevBuf<double> edge_H_;                // [E*36] J_a^T J_b (weighted)
+
+  // linearization
+  DevBuf<double> V_, gp_;                // [P*6], [P*3]
+  DevBuf<double> U_, gc_, Dc_;           // [nf*36], [nf*6], [nf*6]
+  // trial
+  DevBuf<double> Vinv_, e_;              // [P*6], [P*3]
+  DevBuf<double> S_, b_;                 // [n_full*36], [nf*6]
+  DevBuf<double> dc_;                    // [nf*6]
+  DevBuf<double> Minv_, r_, z_, p0_, p1_, qv_, pcg_part_;  // PCG
+  DevBuf<double> dense_;                 // dense factor scratch (global fallback)
+
+  // reductions
+  DevBuf<double> part_a_, part_b_, part_c_, part_d_;
+  DevBuf<int> diag_ub_, diag_pos_;      // per free camera: upper index, BSR slot
+  std::vector<int> diag_ub_host_;
+  DevBuf<BAScalars> sc_;
+  BAScalars h_sc_{};
+  int pcg_grid_ = 0;
+};
+
+}  // namespace sfm

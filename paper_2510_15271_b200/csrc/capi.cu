@@ -1,0 +1,186 @@
+// capi.cu -- the extern "C" boundary (include/sfm_b200.h).
+//
+// Every entry point catches the driver's SfmError and returns its code; the
+// message (with the payload the reference puts in its exception text) is kept
+// on the context for sfm_last_error().
+#include <memory>
+#include <string>
+
+#include "ba.cuh"
+#include "comm.cuh"
+#include "tri.cuh"
+
+struct sfm_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  sfm::Profiler prof;
+  sfm::Comm comm;
+  std::string err;
+  std::unique_ptr<sfm::BASolver> ba;
+};
+
+namespace {
+
+template <typename F>
+int guarded(sfm_ctx* ctx, F&& body) {
+  if (!ctx) return SFM_E_INVALID;
+  try {
+    cudaError_t e = cudaSetDevice(ctx->device);
+    if (e != cudaSuccess) throw sfm::SfmError(SFM_E_CUDA, std::string("cudaSetDevice: ") + cudaGetErrorString(e));
+    ctx->err.clear();
+    body();
+    return SFM_OK;
+  } catch (const sfm::SfmError& e) {
+    ctx->err = e.what();
+    return e.code;
+  } catch (const std::exception& e) {
+    ctx->err = e.what();
+    return SFM_E_CUDA;
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+int sfm_abi_version(void) { return SFM_ABI_VERSION; }
+
+int sfm_nccl_unique_id(uint8_t out[128]) {
+  if (!out) return SFM_E_INVALID;
+  ncclUniqueId id;
+  if (ncclGetUniqueId(&id) != ncclSuccess) return SFM_E_NCCL;
+  static_assert(sizeof(id) == 128, "NCCL unique id must be 128 bytes");
+  std::memcpy(out, &id, sizeof(id));
+  return SFM_OK;
+}
+
+int sfm_ctx_create(int32_t device, int32_t rank, int32_t world, const uint8_t* nccl_id, sfm_ctx** out) {
+  if (!out || world < 1 || rank < 0 || rank >= world) return SFM_E_INVALID;
+  *out = nullptr;
+  auto* ctx = new sfm_ctx();
+  ctx->device = device;
+  int rc = guarded(ctx, [&] {
+    SFM_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+    ctx->comm.init(rank, world, nccl_id);
+  });
+  if (rc != SFM_OK) {
+    std::fprintf(stderr, "sfm_ctx_create: %s\n", ctx->err.c_str());
+    delete ctx;
+    return rc;
+  }
+  *out = ctx;
+  return SFM_OK;
+}
+
+void sfm_ctx_destroy(sfm_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  ctx->ba.reset();
+  if (ctx->stream) cudaStreamDestroy(ctx->stream);
+  delete ctx;
+}
+
+const char* sfm_last_error(const sfm_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+int sfm_set_profiling(sfm_ctx* ctx, int32_t enabled) {
+  return guarded(ctx, [&] { ctx->prof.enabled = enabled != 0; });
+}
+
+int sfm_prof_count(const sfm_ctx* ctx) { return ctx ? (int)ctx->prof.entries.size() : 0; }
+
+int sfm_prof_get(const sfm_ctx* ctx, int32_t i, const char** name, int64_t* launches, double* total_ms,
+                 double* bytes) {
+  if (!ctx || i < 0 || i >= (int)ctx->prof.entries.size()) return SFM_E_INVALID;
+  const auto& e = ctx->prof.entries[i];
+  if (name) *name = e.name.c_str();
+  if (launches) *launches = e.launches;
+  if (total_ms) *total_ms = e.ms;
+  if (bytes) *bytes = e.bytes;
+  return SFM_OK;
+}
+
+int sfm_prof_reset(sfm_ctx* ctx) {
+  return guarded(ctx, [&] { ctx->prof.reset(); });
+}
+
+int sfm_ba_setup(sfm_ctx* ctx, const sfm_ba_problem* prob, const sfm_ba_options* opt) {
+  return guarded(ctx, [&] {
+    SFM_REQUIRE(prob && opt, "null problem/options");
+    ctx->ba.reset(new sfm::BASolver(ctx->stream, &ctx->prof, &ctx->comm));
+    try {
+      ctx->ba->setup(*prob, *opt);
+    } catch (...) {
+      ctx->ba.reset();
+      throw;
+    }
+  });
+}
+
+int sfm_ba_iterate(sfm_ctx* ctx, int32_t n_iters, sfm_ba_report* report) {
+  return guarded(ctx, [&] {
+    SFM_REQUIRE(ctx->ba != nullptr, "sfm_ba_iterate before sfm_ba_setup");
+    ctx->ba->iterate(n_iters, report);
+  });
+}
+
+int sfm_ba_download(sfm_ctx* ctx, double* out_cam_q, double* out_cam_t, double* out_points) {
+  return guarded(ctx, [&] {
+    SFM_REQUIRE(ctx->ba != nullptr, "sfm_ba_download before sfm_ba_setup");
+    ctx->ba->download(out_cam_q, out_cam_t, out_points);
+  });
+}
+
+int sfm_ba_solve(sfm_ctx* ctx, const sfm_ba_problem* prob, const sfm_ba_options* opt, double* out_cam_q,
+                 double* out_cam_t, double* out_points, sfm_ba_report* report) {
+  return guarded(ctx, [&] {
+    SFM_REQUIRE(prob && opt, "null problem/options");
+    sfm::BASolver solver(ctx->stream, &ctx->prof, &ctx->comm);
+    solver.setup(*prob, *opt);
+    solver.iterate(opt->max_iters > 0 ? opt->max_iters : 0, report);
+    solver.download(out_cam_q, out_cam_t, out_points);
+  });
+}
+
+int sfm_ba_eval(sfm_ctx* ctx, const sfm_ba_problem* prob, int32_t loss_kind, double loss_param,
+                double* out_cost_per_obs, double* out_res, double* out_jc, double* out_jp) {
+  return guarded(ctx, [&] {
+    SFM_REQUIRE(prob != nullptr, "null problem");
+    sfm::BASolver::eval(ctx->stream, &ctx->prof, *prob, loss_kind, loss_param, out_cost_per_obs, out_res,
+                        out_jc, out_jp);
+  });
+}
+
+int sfm_ransac_triangulate(sfm_ctx* ctx, const sfm_tracks* tracks, double threshold_px, double min_angle,
+                           int32_t method, double* out_X, uint8_t* out_mask, int8_t* out_status) {
+  return guarded(ctx, [&] {
+    SFM_REQUIRE(tracks != nullptr, "null tracks");
+    sfm::tri_ransac(ctx->stream, &ctx->prof, *tracks, threshold_px, min_angle, method, out_X, out_mask,
+                    out_status);
+  });
+}
+
+int sfm_triangulate(sfm_ctx* ctx, const sfm_tracks* tracks, double min_angle, int32_t method, double* out_X,
+                    int8_t* out_status) {
+  return guarded(ctx, [&] {
+    SFM_REQUIRE(tracks != nullptr, "null tracks");
+    sfm::tri_direct(ctx->stream, &ctx->prof, *tracks, min_angle, method, out_X, out_status);
+  });
+}
+
+int sfm_gate(sfm_ctx* ctx, const sfm_tracks* tracks, const double* points, double threshold_px,
+             uint8_t* mask_inout, int32_t* out_inliers, int64_t* out_removed) {
+  return guarded(ctx, [&] {
+    SFM_REQUIRE(tracks && points && mask_inout, "null arguments");
+    sfm::tri_gate(ctx->stream, &ctx->prof, *tracks, points, threshold_px, mask_inout, out_inliers,
+                  out_removed);
+  });
+}
+
+int sfm_reprojection_errors(sfm_ctx* ctx, const sfm_tracks* tracks, const double* points, double* out_err) {
+  return guarded(ctx, [&] {
+    SFM_REQUIRE(tracks && points && out_err, "null arguments");
+    sfm::tri_reproj_errors(ctx->stream, &ctx->prof, *tracks, points, out_err);
+  });
+}
+
+}  // extern "C"

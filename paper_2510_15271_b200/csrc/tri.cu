@@ -1,0 +1,626 @@
+// tri.cu -- batched multi-view triangulation, RANSAC over observation pairs
+// and reprojection gating (sm_100a, fp64).
+//
+// Reference path being replaced:
+//   mapping.py:166-191  _world_rays, _max_ray_angle, _check_cheirality
+//   mapping.py:194-221  triangulate_dlt (SVD of the stacked hat(d)[R|t] rows)
+//   mapping.py:224-240  triangulate_midpoint (cond > 1e10 -> ParallelRays)
+//   mapping.py:243-252  reprojection_error (inf when projection raises)
+//   mapping.py:255-305  ransac_triangulate (exhaustive i<j pairs, strict <,
+//                       lexicographic (count, -sum err), first best wins)
+//   mapping.py:544-566  remove_outliers (strict >)
+//
+// DLT: the 3k x 4 system is reduced by streaming Givens rotations to a 4x4
+// upper-triangular R (same right singular vectors as A, no squaring of the
+// condition number), whose smallest right singular vector comes from a
+// one-sided (Hestenes) Jacobi SVD.  RANSAC is warp-per-track: lanes split
+// the pair hypotheses, a warp arg-max with a lowest-index tie-break
+// reproduces the reference's sequential "first best" rule.
+#include <cmath>
+
+#include "sfm_math.cuh"
+#include "tri.cuh"
+
+namespace sfm {
+
+namespace {
+
+struct TriData {
+  const int* of;              // [N] frame per observation
+  const double* uv;           // [N*2]
+  const double* ray;          // [N*3] unit camera-frame ray (unproject)
+  const int* ray_st;          // [N] PROJ_* of unproject
+  const double* Rt;           // [F*12]
+  const int* fm;
+  const sfm_camera_model* models;
+};
+
+__device__ __forceinline__ void cam_of(const TriData& d, int f, Mat3& R, Vec3& t) {
+  const double* p = d.Rt + (int64_t)f * 12;
+#pragma unroll
+  for (int i = 0; i < 9; ++i) R.m[i] = p[i];
+  t = v3(p[9], p[10], p[11]);
+}
+
+__global__ void k_rt(int F, const double* q, const double* t, double* Rt) {
+  int f = blockIdx.x * blockDim.x + threadIdx.x;
+  if (f >= F) return;
+  Mat3 R = quat_to_matrix(Quat{q[f * 4], q[f * 4 + 1], q[f * 4 + 2], q[f * 4 + 3]});
+  for (int i = 0; i < 9; ++i) Rt[f * 12 + i] = R.m[i];
+  for (int i = 0; i < 3; ++i) Rt[f * 12 + 9 + i] = t[f * 3 + i];
+}
+
+// unproject every observation once (cameras.py:162-166)
+__global__ void k_rays(int64_t N, TriData d, double* ray, int* st) {
+  int64_t o = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (o >= N) return;
+  const sfm_camera_model cm = d.models[d.fm[d.of[o]]];
+  Vec3 r = v3(0, 0, 0);
+  int s = unproject(cm, d.uv[o * 2], d.uv[o * 2 + 1], r);
+  ray[o * 3] = r.x; ray[o * 3 + 1] = r.y; ray[o * 3 + 2] = r.z;
+  st[o] = s;
+}
+
+// Observation selection inside a track.
+struct Sel {
+  int64_t b0, b1;
+  int i, j;               // pair mode when i >= 0 (local indices)
+  const uint8_t* mask;    // mask mode when non-null (indexed by global obs)
+  __device__ __forceinline__ bool operator()(int64_t o) const {
+    if (i >= 0) return o == b0 + i || o == b0 + j;
+    if (mask) return mask[o] != 0;
+    return true;
+  }
+};
+
+__device__ __forceinline__ Vec3 world_dir(const TriData& d, int64_t o, Mat3& R, Vec3& t) {
+  cam_of(d, d.of[o], R, t);
+  Vec3 r = v3(d.ray[o * 3], d.ray[o * 3 + 1], d.ray[o * 3 + 2]);
+  return mulT(R, r);
+}
+
+// mapping.py:177-183: max pairwise arccos(clip(|di.dj|)) == arccos(min |.|)
+__device__ double max_ray_angle(const TriData& d, const Sel& s) {
+  double mind = 2.0;
+  for (int64_t a = s.b0; a < s.b1; ++a) {
+    if (!s(a)) continue;
+    Mat3 R; Vec3 t;
+    Vec3 da = world_dir(d, a, R, t);
+    for (int64_t b = a + 1; b < s.b1; ++b) {
+      if (!s(b)) continue;
+      Vec3 db = world_dir(d, b, R, t);
+      double c = fabs(dot(da, db));
+      mind = fmin(mind, c);
+    }
+  }
+  if (mind > 1.0) mind = 1.0;
+  return acos(mind);
+}
+
+__device__ __forceinline__ void givens_add(double Rm[10], double v[4]) {
+  // Rm packed upper triangle row-major: (0,0)(0,1)(0,2)(0,3)(1,1)(1,2)(1,3)(2,2)(2,3)(3,3)
+  int base = 0;
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const int len = 4 - c;
+    double rc = Rm[base];
+    double vc = v[c];
+    if (vc != 0.0) {
+      double r = hypot(rc, vc);
+      double cs = rc / r, sn = vc / r;
+      Rm[base] = r;
+      for (int j = 1; j < len; ++j) {
+        double a = Rm[base + j], b = v[c + j];
+        Rm[base + j] = cs * a + sn * b;
+        v[c + j] = -sn * a + cs * b;
+      }
+    }
+    base += len;
+  }
+}
+
+// Smallest right singular vector of the 4x4 upper-triangular R
+// (one-sided Jacobi on the columns).
+__device__ void smallest_right_sv(const double Rm[10], double out[4]) {
+  double A[4][4];
+  int base = 0;
+  for (int r = 0; r < 4; ++r)
+    for (int c = 0; c < 4; ++c) A[r][c] = 0.0;
+  for (int r = 0; r < 4; ++r) {
+    for (int c = r; c < 4; ++c) A[r][c] = Rm[base + (c - r)];
+    base += 4 - r;
+  }
+  double V[4][4];
+  for (int r = 0; r < 4; ++r)
+    for (int c = 0; c < 4; ++c) V[r][c] = (r == c) ? 1.0 : 0.0;
+  for (int sweep = 0; sweep < 40; ++sweep) {
+    bool rotated = false;
+    for (int p = 0; p < 3; ++p)
+      for (int q = p + 1; q < 4; ++q) {
+        double al = 0.0, be = 0.0, ga = 0.0;
+        for (int r = 0; r < 4; ++r) {
+          al += A[r][p] * A[r][p];
+          be += A[r][q] * A[r][q];
+          ga += A[r][p] * A[r][q];
+        }
+        if (ga == 0.0 || fabs(ga) <= 1e-17 * sqrt(al * be)) continue;
+        rotated = true;
+        double zeta = (be - al) / (2.0 * ga);
+        double tt = copysign(1.0, zeta) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+        double cs = 1.0 / sqrt(1.0 + tt * tt), sn = cs * tt;
+        for (int r = 0; r < 4; ++r) {
+          double a = A[r][p], b = A[r][q];
+          A[r][p] = cs * a - sn * b;
+          A[r][q] = sn * a + cs * b;
+          double va = V[r][p], vb = V[r][q];
+          V[r][p] = cs * va - sn * vb;
+          V[r][q] = sn * va + cs * vb;
+        }
+      }
+    if (!rotated) break;
+  }
+  int best = 0;
+  double bn = 1e308;
+  for (int c = 0; c < 4; ++c) {
+    double n = 0.0;
+    for (int r = 0; r < 4; ++r) n += A[r][c] * A[r][c];
+    if (n < bn) { bn = n; best = c; }
+  }
+  double nv = 0.0;
+  for (int r = 0; r < 4; ++r) nv += V[r][best] * V[r][best];
+  nv = sqrt(nv);
+  for (int r = 0; r < 4; ++r) out[r] = V[r][best] / nv;
+}
+
+// Eigenvalues of a symmetric 3x3 (cyclic Jacobi) -> condition estimate.
+__device__ double sym3_cond(const double S[9]) {
+  double A[3][3];
+  for (int r = 0; r < 3; ++r)
+    for (int c = 0; c < 3; ++c) A[r][c] = S[r * 3 + c];
+  for (int sweep = 0; sweep < 50; ++sweep) {
+    double off = fabs(A[0][1]) + fabs(A[0][2]) + fabs(A[1][2]);
+    if (off == 0.0) break;
+    for (int p = 0; p < 2; ++p)
+      for (int q = p + 1; q < 3; ++q) {
+        if (A[p][q] == 0.0) continue;
+        double theta = (A[q][q] - A[p][p]) / (2.0 * A[p][q]);
+        double t = copysign(1.0, theta) / (fabs(theta) + sqrt(theta * theta + 1.0));
+        double c = 1.0 / sqrt(t * t + 1.0), s = t * c;
+        for (int k = 0; k < 3; ++k) {
+          double akp = A[k][p], akq = A[k][q];
+          A[k][p] = c * akp - s * akq;
+          A[k][q] = s * akp + c * akq;
+        }
+        for (int k = 0; k < 3; ++k) {
+          double apk = A[p][k], aqk = A[q][k];
+          A[p][k] = c * apk - s * aqk;
+          A[q][k] = s * apk + c * aqk;
+        }
+      }
+  }
+  double e0 = fabs(A[0][0]), e1 = fabs(A[1][1]), e2 = fabs(A[2][2]);
+  double mx = fmax(e0, fmax(e1, e2)), mn = fmin(e0, fmin(e1, e2));
+  return mx / fmax(mn, 1e-300);
+}
+
+// LU with partial pivoting (numpy.linalg.solve / LAPACK gesv).
+__device__ bool solve3(double A[9], double b[3], double x[3]) {
+  int piv[3] = {0, 1, 2};
+  for (int k = 0; k < 3; ++k) {
+    int p = k;
+    double mx = fabs(A[piv[k] * 3 + k]);
+    for (int i = k + 1; i < 3; ++i)
+      if (fabs(A[piv[i] * 3 + k]) > mx) { mx = fabs(A[piv[i] * 3 + k]); p = i; }
+    if (mx == 0.0) return false;
+    int tmp = piv[k]; piv[k] = piv[p]; piv[p] = tmp;
+    for (int i = k + 1; i < 3; ++i) {
+      double f = A[piv[i] * 3 + k] / A[piv[k] * 3 + k];
+      A[piv[i] * 3 + k] = f;
+      for (int j = k + 1; j < 3; ++j) A[piv[i] * 3 + j] -= f * A[piv[k] * 3 + j];
+    }
+  }
+  double y[3];
+  for (int i = 0; i < 3; ++i) {
+    double s = b[piv[i]];
+    for (int j = 0; j < i; ++j) s -= A[piv[i] * 3 + j] * y[j];
+    y[i] = s;
+  }
+  for (int i = 2; i >= 0; --i) {
+    double s = y[i];
+    for (int j = i + 1; j < 3; ++j) s -= A[piv[i] * 3 + j] * x[j];
+    x[i] = s / A[piv[i] * 3 + i];
+  }
+  return true;
+}
+
+// Triangulates the selected observations (mapping.py:194-240).  Returns a
+// SFM_TRI_* status.  check_angle applies the min_angle parallax gate.
+__device__ int tri_solve(const TriData& d, const Sel& s, int method, double min_angle, bool check_angle,
+                         Vec3& X) {
+  int n = 0;
+  for (int64_t o = s.b0; o < s.b1; ++o) {
+    if (!s(o)) continue;
+    ++n;
+    if (d.ray_st[o] != PROJ_OK) return SFM_TRI_CAMERA_ERROR;
+  }
+  if (n < 2) return SFM_TRI_TOO_FEW_OBS;
+  if (check_angle && max_ray_angle(d, s) < min_angle) return SFM_TRI_INSUFFICIENT_PARALLAX;
+  if (method == SFM_TRI_DLT) {
+    double Rm[10];
+    for (int i = 0; i < 10; ++i) Rm[i] = 0.0;
+    for (int64_t o = s.b0; o < s.b1; ++o) {
+      if (!s(o)) continue;
+      Mat3 R; Vec3 t;
+      cam_of(d, d.of[o], R, t);
+      const double dx = d.ray[o * 3], dy = d.ray[o * 3 + 1], dz = d.ray[o * 3 + 2];
+      double P[3][4];
+      for (int i = 0; i < 3; ++i) {
+        P[i][0] = R.m[i * 3]; P[i][1] = R.m[i * 3 + 1]; P[i][2] = R.m[i * 3 + 2];
+      }
+      P[0][3] = t.x; P[1][3] = t.y; P[2][3] = t.z;
+      double row[4];
+      for (int c = 0; c < 4; ++c) row[c] = -dz * P[1][c] + dy * P[2][c];
+      givens_add(Rm, row);
+      for (int c = 0; c < 4; ++c) row[c] = dz * P[0][c] - dx * P[2][c];
+      givens_add(Rm, row);
+      for (int c = 0; c < 4; ++c) row[c] = -dy * P[0][c] + dx * P[1][c];
+      givens_add(Rm, row);
+    }
+    double Xh[4];
+    smallest_right_sv(Rm, Xh);
+    if (fabs(Xh[3]) < 1e-12) return SFM_TRI_INSUFFICIENT_PARALLAX;
+    X = v3(Xh[0] / Xh[3], Xh[1] / Xh[3], Xh[2] / Xh[3]);
+  } else {
+    double A[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0}, b[3] = {0, 0, 0};
+    for (int64_t o = s.b0; o < s.b1; ++o) {
+      if (!s(o)) continue;
+      Mat3 R; Vec3 t;
+      Vec3 w = world_dir(d, o, R, t);
+      Vec3 c = mulT(R, t);
+      c = v3(-c.x, -c.y, -c.z);
+      const double wv[3] = {w.x, w.y, w.z}, cv[3] = {c.x, c.y, c.z};
+      for (int i = 0; i < 3; ++i) {
+        double bi = 0.0;
+        for (int j = 0; j < 3; ++j) {
+          double m = (i == j ? 1.0 : 0.0) - wv[i] * wv[j];
+          A[i * 3 + j] += m;
+          bi += m * cv[j];
+        }
+        b[i] += bi;
+      }
+    }
+    if (sym3_cond(A) > 1e10) return SFM_TRI_PARALLEL_RAYS;
+    double x[3];
+    if (!solve3(A, b, x)) return SFM_TRI_PARALLEL_RAYS;
+    X = v3(x[0], x[1], x[2]);
+  }
+  // cheirality (mapping.py:186-191)
+  for (int64_t o = s.b0; o < s.b1; ++o) {
+    if (!s(o)) continue;
+    Mat3 R; Vec3 t;
+    cam_of(d, d.of[o], R, t);
+    Vec3 pc = add(mul(R, X), t);
+    Vec3 r = v3(d.ray[o * 3], d.ray[o * 3 + 1], d.ray[o * 3 + 2]);
+    if (dot(pc, r) <= 0.0) return SFM_TRI_CHEIRALITY;
+  }
+  if (!(isfinite(X.x) && isfinite(X.y) && isfinite(X.z))) return SFM_TRI_INSUFFICIENT_PARALLAX;
+  return SFM_TRI_OK;
+}
+
+// mapping.py:243-252
+__device__ __forceinline__ double reproj_err(const TriData& d, int64_t o, Vec3 X) {
+  Mat3 R; Vec3 t;
+  const int f = d.of[o];
+  cam_of(d, f, R, t);
+  Vec3 pc = add(mul(R, X), t);
+  double u, v;
+  if (project_point(d.models[d.fm[f]], pc, u, v) != PROJ_OK) return INFINITY;
+  double du = u - d.uv[o * 2], dv = v - d.uv[o * 2 + 1];
+  return sqrt(du * du + dv * dv);
+}
+
+// numpy's pairwise summation order (numpy/_core/src/umath/loops_utils.h
+// pairwise_sum) for n <= 128 elements streamed in order; longer arrays fall
+// back to a sequential sum.
+struct NpSum {
+  int n, m = 0;
+  double r[8];
+  double res = 0.0;
+  __device__ explicit NpSum(int n_) : n(n_) {}
+  __device__ void add(double v) {
+    if (n < 8 || n > 128) { res += v; ++m; return; }
+    const int blocks = n - (n % 8);
+    if (m < 8) r[m] = v;
+    else if (m < blocks) r[m % 8] += v;
+    else res += v;
+    ++m;
+    if (m == blocks) res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7])) + res;
+  }
+  __device__ double value() const { return res; }
+};
+
+// Score of one hypothesis: inlier count and -sum(err[inliers]).
+__device__ void score_hyp(const TriData& d, int64_t b0, int64_t b1, Vec3 X, double thr, int& cnt,
+                          double& negsum) {
+  cnt = 0;
+  for (int64_t o = b0; o < b1; ++o) cnt += reproj_err(d, o, X) < thr;
+  NpSum s(cnt);
+  for (int64_t o = b0; o < b1; ++o) {
+    double e = reproj_err(d, o, X);
+    if (e < thr) s.add(e);
+  }
+  negsum = -s.value();
+}
+
+struct TrackArgs {
+  int64_t T;
+  const int64_t* ptr;
+  const uint8_t* active;
+  TriData d;
+  double thr, min_angle;
+  int method;
+  double* X;
+  uint8_t* mask;
+  int8_t* status;
+};
+
+__device__ __forceinline__ void pair_of(int k, int pi, int& i, int& j) {
+  i = 0;
+  int rem = pi;
+  while (rem >= k - 1 - i) { rem -= k - 1 - i; ++i; }
+  j = i + 1 + rem;
+}
+
+// Warp per track: ransac_triangulate (mapping.py:255-305).
+__global__ void __launch_bounds__(128) k_ransac(TrackArgs a) {
+  const int64_t t = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (t >= a.T) return;
+  const int64_t b0 = a.ptr[t], b1 = a.ptr[t + 1];
+  const int k = (int)(b1 - b0);
+  if (a.active && !a.active[t]) {
+    for (int64_t o = b0 + lane; o < b1; o += 32) a.mask[o] = 0;
+    if (lane == 0) {
+      a.status[t] = SFM_TRI_SKIPPED;
+      a.X[t * 3] = a.X[t * 3 + 1] = a.X[t * 3 + 2] = NAN;
+    }
+    return;
+  }
+  const int npairs = k * (k - 1) / 2;
+  int bcnt = -1, bidx = 0x7fffffff;
+  double bneg = -INFINITY;
+  for (int pi = lane; pi < npairs; pi += 32) {
+    int i, j;
+    pair_of(k, pi, i, j);
+    Sel s{b0, b1, i, j, nullptr};
+    Vec3 X;
+    int st;
+    if (a.method == SFM_TRI_DLT) {
+      st = tri_solve(a.d, s, SFM_TRI_DLT, a.min_angle, true, X);
+    } else {
+      st = tri_solve(a.d, s, SFM_TRI_MIDPOINT, a.min_angle, true, X);
+    }
+    if (st != SFM_TRI_OK) continue;
+    int cnt;
+    double neg;
+    score_hyp(a.d, b0, b1, X, a.thr, cnt, neg);
+    if (cnt >= 2 && (cnt > bcnt || (cnt == bcnt && neg > bneg))) {
+      bcnt = cnt; bneg = neg; bidx = pi;
+    }
+  }
+  // warp arg-max: (count, -sum) lexicographic, lowest pair index on ties
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    int oc = __shfl_down_sync(0xffffffffu, bcnt, off);
+    double on = __shfl_down_sync(0xffffffffu, bneg, off);
+    int oi = __shfl_down_sync(0xffffffffu, bidx, off);
+    bool take = oc > bcnt || (oc == bcnt && (on > bneg || (on == bneg && oi < bidx)));
+    if (take) { bcnt = oc; bneg = on; bidx = oi; }
+  }
+  if (lane != 0) return;
+  int status = SFM_TRI_FAILED;
+  Vec3 X = v3(NAN, NAN, NAN);
+  if (bcnt >= 2) {
+    int i, j;
+    pair_of(k, bidx, i, j);
+    Sel s{b0, b1, i, j, nullptr};
+    Vec3 Xb;
+    tri_solve(a.d, s, a.method, a.min_angle, true, Xb);
+    for (int64_t o = b0; o < b1; ++o) a.mask[o] = reproj_err(a.d, o, Xb) < a.thr;
+    Sel si{b0, b1, -1, -1, a.mask};
+    // refinement on the inliers (midpoint has no parallax gate, :295)
+    int st = tri_solve(a.d, si, a.method, a.min_angle, a.method == SFM_TRI_DLT, X);
+    if (st == SFM_TRI_OK) {
+      int cnt = 0;
+      for (int64_t o = b0; o < b1; ++o) {
+        uint8_t m = reproj_err(a.d, o, X) < a.thr;
+        a.mask[o] = m;
+        cnt += m;
+      }
+      if (cnt >= 2) status = SFM_TRI_OK;
+    }
+  }
+  if (status != SFM_TRI_OK) {
+    for (int64_t o = b0; o < b1; ++o) a.mask[o] = 0;
+    X = v3(NAN, NAN, NAN);
+  }
+  a.status[t] = (int8_t)status;
+  a.X[t * 3] = X.x; a.X[t * 3 + 1] = X.y; a.X[t * 3 + 2] = X.z;
+}
+
+__global__ void k_direct(TrackArgs a) {
+  int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= a.T) return;
+  if (a.active && !a.active[t]) { a.status[t] = SFM_TRI_SKIPPED; return; }
+  Sel s{a.ptr[t], a.ptr[t + 1], -1, -1, nullptr};
+  Vec3 X = v3(NAN, NAN, NAN);
+  int st = tri_solve(a.d, s, a.method, a.min_angle, a.method == SFM_TRI_DLT, X);
+  if (st != SFM_TRI_OK) X = v3(NAN, NAN, NAN);
+  a.status[t] = (int8_t)st;
+  a.X[t * 3] = X.x; a.X[t * 3 + 1] = X.y; a.X[t * 3 + 2] = X.z;
+}
+
+__global__ void k_gate(int64_t T, const int64_t* ptr, TriData d, const double* P, double thr, uint8_t* mask,
+                       int* inliers, unsigned long long* removed) {
+  int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  unsigned long long rm = 0;
+  if (t < T) {
+    Vec3 X = v3(P[t * 3], P[t * 3 + 1], P[t * 3 + 2]);
+    int cnt = 0;
+    for (int64_t o = ptr[t]; o < ptr[t + 1]; ++o) {
+      if (!mask[o]) continue;
+      if (reproj_err(d, o, X) > thr) { mask[o] = 0; ++rm; }
+      else ++cnt;
+    }
+    inliers[t] = cnt;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) rm += __shfl_down_sync(0xffffffffu, rm, o);
+  if ((threadIdx.x & 31) == 0 && rm) atomicAdd(removed, rm);  // integer: order-free
+}
+
+__global__ void k_errs(int64_t T, const int64_t* ptr, TriData d, const double* P, double* err) {
+  int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= T) return;
+  Vec3 X = v3(P[t * 3], P[t * 3 + 1], P[t * 3 + 2]);
+  for (int64_t o = ptr[t]; o < ptr[t + 1]; ++o) err[o] = reproj_err(d, o, X);
+}
+
+// Device copies of a track set.
+struct TrackDev {
+  DevBuf<sfm_camera_model> models;
+  DevBuf<int> fm, of, st;
+  DevBuf<double> q, t, Rt, uv, ray;
+  DevBuf<int64_t> ptr;
+  DevBuf<uint8_t> active;
+  TriData d{};
+  void load(const sfm_tracks& tr, cudaStream_t s, Profiler* prof, bool rays) {
+    SFM_REQUIRE(tr.n_tracks >= 0 && tr.n_obs >= 0 && tr.n_frames >= 0, "negative sizes");
+    models.upload(tr.models, tr.n_models, s);
+    fm.upload(tr.frame_model, tr.n_frames, s);
+    q.upload(tr.cam_q, (size_t)tr.n_frames * 4, s);
+    t.upload(tr.cam_t, (size_t)tr.n_frames * 3, s);
+    Rt.resize((size_t)tr.n_frames * 12);
+    if (tr.n_frames) {
+      ProfScope ps(*prof, "tri_rt", 0.0, s);
+      k_rt<<<grid_for(tr.n_frames, 128), 128, 0, s>>>(tr.n_frames, q.get(), t.get(), Rt.get());
+    }
+    ptr.upload(tr.track_ptr, tr.n_tracks + 1, s);
+    of.upload(tr.obs_frame, tr.n_obs, s);
+    uv.upload(tr.obs_uv, (size_t)tr.n_obs * 2, s);
+    if (tr.active) active.upload(tr.active, tr.n_tracks, s);
+    d.of = of.get(); d.uv = uv.get(); d.Rt = Rt.get(); d.fm = fm.get(); d.models = models.get();
+    if (rays) {
+      ray.resize((size_t)tr.n_obs * 3);
+      st.resize(tr.n_obs);
+      d.ray = ray.get();
+      d.ray_st = st.get();
+      if (tr.n_obs) {
+        ProfScope ps(*prof, "tri_rays", 48.0 * tr.n_obs, s);
+        k_rays<<<grid_for(tr.n_obs, 128), 128, 0, s>>>(tr.n_obs, d, ray.get(), st.get());
+      }
+    }
+  }
+};
+
+void validate(const sfm_tracks& tr) {
+  for (int f = 0; f < tr.n_frames; ++f)
+    SFM_REQUIRE(tr.frame_model[f] >= 0 && tr.frame_model[f] < tr.n_models, "frame_model out of range");
+  SFM_REQUIRE(tr.track_ptr[0] == 0 && tr.track_ptr[tr.n_tracks] == tr.n_obs, "track_ptr must span obs");
+  for (int64_t i = 0; i < tr.n_tracks; ++i)
+    SFM_REQUIRE(tr.track_ptr[i + 1] >= tr.track_ptr[i], "track_ptr must be non-decreasing");
+  for (int64_t o = 0; o < tr.n_obs; ++o)
+    SFM_REQUIRE(tr.obs_frame[o] >= 0 && tr.obs_frame[o] < tr.n_frames, "obs_frame out of range");
+}
+
+}  // namespace
+
+void tri_ransac(cudaStream_t s, Profiler* prof, const sfm_tracks& tr, double thr, double min_angle, int method,
+                double* out_X, uint8_t* out_mask, int8_t* out_status) {
+  validate(tr);
+  TrackDev dev;
+  dev.load(tr, s, prof, true);
+  DevBuf<double> X;
+  DevBuf<uint8_t> mask;
+  DevBuf<int8_t> st;
+  X.resize((size_t)tr.n_tracks * 3);
+  mask.resize(tr.n_obs);
+  st.resize(tr.n_tracks);
+  TrackArgs a{};
+  a.T = tr.n_tracks; a.ptr = dev.ptr.get(); a.active = tr.active ? dev.active.get() : nullptr; a.d = dev.d;
+  a.thr = thr; a.min_angle = min_angle; a.method = method; a.X = X.get(); a.mask = mask.get(); a.status = st.get();
+  if (tr.n_tracks) {
+    ProfScope ps(*prof, "tri_ransac", 24.0 * tr.n_obs + 24.0 * tr.n_tracks + tr.n_obs, s);
+    k_ransac<<<grid_for(tr.n_tracks * 32, 128), 128, 0, s>>>(a);
+  }
+  X.download(out_X, (size_t)tr.n_tracks * 3, s);
+  mask.download(out_mask, tr.n_obs, s);
+  st.download(out_status, tr.n_tracks, s);
+  SFM_CUDA(cudaStreamSynchronize(s));
+}
+
+void tri_direct(cudaStream_t s, Profiler* prof, const sfm_tracks& tr, double min_angle, int method, double* out_X,
+                int8_t* out_status) {
+  validate(tr);
+  TrackDev dev;
+  dev.load(tr, s, prof, true);
+  DevBuf<double> X;
+  DevBuf<int8_t> st;
+  X.resize((size_t)tr.n_tracks * 3);
+  st.resize(tr.n_tracks);
+  TrackArgs a{};
+  a.T = tr.n_tracks; a.ptr = dev.ptr.get(); a.active = tr.active ? dev.active.get() : nullptr; a.d = dev.d;
+  a.min_angle = min_angle; a.method = method; a.X = X.get(); a.status = st.get();
+  if (tr.n_tracks) {
+    ProfScope ps(*prof, "tri_direct", 0.0, s);
+    k_direct<<<grid_for(tr.n_tracks, 128), 128, 0, s>>>(a);
+  }
+  X.download(out_X, (size_t)tr.n_tracks * 3, s);
+  st.download(out_status, tr.n_tracks, s);
+  SFM_CUDA(cudaStreamSynchronize(s));
+}
+
+void tri_gate(cudaStream_t s, Profiler* prof, const sfm_tracks& tr, const double* points, double thr,
+              uint8_t* mask_inout, int32_t* out_inliers, int64_t* out_removed) {
+  validate(tr);
+  TrackDev dev;
+  dev.load(tr, s, prof, false);
+  DevBuf<double> P;
+  DevBuf<uint8_t> mask;
+  DevBuf<int> inl;
+  DevBuf<unsigned long long> rm;
+  P.upload(points, (size_t)tr.n_tracks * 3, s);
+  mask.upload(mask_inout, tr.n_obs, s);
+  inl.resize(tr.n_tracks);
+  rm.resize(1);
+  rm.zero(s);
+  if (tr.n_tracks) {
+    ProfScope ps(*prof, "gate", 24.0 * tr.n_obs + 24.0 * tr.n_tracks + 2.0 * tr.n_obs, s);
+    k_gate<<<grid_for(tr.n_tracks, 128), 128, 0, s>>>(tr.n_tracks, dev.ptr.get(), dev.d, P.get(), thr, mask.get(),
+                                                       inl.get(), rm.get());
+  }
+  unsigned long long h = 0;
+  mask.download(mask_inout, tr.n_obs, s);
+  if (out_inliers) inl.download(out_inliers, tr.n_tracks, s);
+  rm.download(&h, 1, s);
+  SFM_CUDA(cudaStreamSynchronize(s));
+  if (out_removed) *out_removed = (int64_t)h;
+}
+
+void tri_reproj_errors(cudaStream_t s, Profiler* prof, const sfm_tracks& tr, const double* points,
+                       double* out_err) {
+  validate(tr);
+  TrackDev dev;
+  dev.load(tr, s, prof, false);
+  DevBuf<double> P, err;
+  P.upload(points, (size_t)tr.n_tracks * 3, s);
+  err.resize(tr.n_obs);
+  if (tr.n_tracks) {
+    ProfScope ps(*prof, "reproj_errors", 0.0, s);
+    k_errs<<<grid_for(tr.n_tracks, 128), 128, 0, s>>>(tr.n_tracks, dev.ptr.get(), dev.d, P.get(), err.get());
+  }
+  err.download(out_err, tr.n_obs, s);
+  SFM_CUDA(cudaStreamSynchronize(s));
+}
+
+}  // namespace sfm

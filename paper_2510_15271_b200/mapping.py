@@ -1,0 +1,559 @@
+"""Drop-in for sfmkit.mapping's hot path, executed on the B200.
+
+Same names, signatures, defaults, in-place mutations, reports and exception
+classes as the reference module (/root/reference/pkg/src/sfmkit/mapping.py):
+
+    bundle_adjust          mapping.py:390-527   -> sfm_ba_solve
+    ransac_triangulate     mapping.py:255-305   -> sfm_ransac_triangulate
+    triangulate_dlt        mapping.py:194-221   -> sfm_triangulate (DLT)
+    triangulate_midpoint   mapping.py:224-240   -> sfm_triangulate (midpoint)
+    reprojection_error     mapping.py:243-252   -> sfm_reprojection_errors
+    remove_outliers        mapping.py:544-566   -> sfm_gate
+    iterative_map          mapping.py:569-624   (host loop, batched device calls)
+    mean_reprojection_error mapping.py:627-636  -> sfm_reprojection_errors
+
+This module only flattens the object model into the C-ABI's arrays and maps
+results and error codes back; every floating-point operation of the path
+runs in libsfm_b200.so.  Objects from the reference package are accepted
+(duck typing) and written back with their own types.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _native as nat
+from .cameras import CameraModel
+from .errors import NoGauge, raise_for_tri_status
+from .keyframes import ROLLING_SHUTTER, Keyframe
+from .se3 import Pose
+from .solver import (DEFAULT_DEVICE_OPTIONS, RobustLoss, SolverOptions, SolverReport,
+                     TRIVIAL_LOSS, DeviceOptions)
+
+PENDING = "pending"
+TRIANGULATED = "triangulated"
+FAILED = "failed"
+
+PURE = "pure"
+LOCALIZATION_FIXED = "localization_fixed"
+LOCALIZATION_ADJUST = "localization_adjust"
+RIG_EXTRINSIC = "rig_extrinsic"
+
+
+# --- object model (mapping.py:30-108) ---------------------------------------
+
+@dataclass
+class Observation:
+    frame_id: int
+    feature_index: int
+    pixel: np.ndarray
+
+    def __post_init__(self):
+        self.pixel = np.asarray(self.pixel, dtype=float).reshape(2)
+
+
+@dataclass
+class Track:
+    observations: list
+    status: str = PENDING
+
+    def __post_init__(self):
+        if len(self.observations) < 2:
+            raise ValueError("tracks need at least two observations")
+        frames = [o.frame_id for o in self.observations]
+        if len(set(frames)) != len(frames):
+            raise ValueError("duplicate frame in track")
+
+
+@dataclass
+class Landmark:
+    position: np.ndarray
+    track: Track
+    inlier_mask: np.ndarray
+
+    def __post_init__(self):
+        self.position = np.asarray(self.position, dtype=float).reshape(3)
+        self.inlier_mask = np.asarray(self.inlier_mask, dtype=bool)
+
+    def inlier_observations(self):
+        return [o for o, ok in zip(self.track.observations, self.inlier_mask) if ok]
+
+
+@dataclass
+class SparseMap:
+    keyframes: dict
+    cameras: dict
+    landmarks: list = field(default_factory=list)
+    rig: object = None
+    provenance: dict = field(default_factory=dict)
+    fixed_frames: set = field(default_factory=set)
+
+    def camera_of(self, frame_id):
+        return self.cameras[self.keyframes[frame_id].camera_id]
+
+    def pose_of(self, frame_id) -> Pose:
+        return self.keyframes[frame_id].cam_from_world
+
+
+@dataclass
+class StageConfig:
+    outlier_px: float
+    loss: RobustLoss = TRIVIAL_LOSS
+
+
+@dataclass
+class MappingConfig:
+    stage1: StageConfig = field(
+        default_factory=lambda: StageConfig(4.0, RobustLoss("huber", 2.0)))
+    stage2: StageConfig = field(default_factory=lambda: StageConfig(2.0))
+    lambda_c: float = 1.0
+    lambda_a: float = 1.0
+    extrinsic_prior_weight: float = 1.0
+    max_outer_iters: int = 10
+    min_triangulation_angle: float = float(np.radians(0.5))
+    triangulation: str = "dlt"
+    seed: int = 42
+    max_solver_iters: int = 50
+
+    def __post_init__(self):
+        if self.stage2.outlier_px > self.stage1.outlier_px:
+            raise ValueError("stage 2 threshold must not exceed stage 1")
+        if min(self.lambda_c, self.lambda_a) < 0:
+            raise ValueError("weights must be non-negative")
+
+
+# --- flattened arrays --------------------------------------------------------
+
+def camera_struct(cam) -> nat.CameraModelC:
+    k1, k2 = (tuple(cam.distortion) + (0.0, 0.0))[:2]
+    return nat.CameraModelC(nat.CAM_KINDS[cam.kind], int(cam.width), int(cam.height), 0,
+                            float(cam.fx), float(cam.fy), float(cam.cx), float(cam.cy),
+                            float(k1), float(k2))
+
+
+def model_table(cams_per_frame):
+    """Unique camera models -> (ctypes array, per-frame model index)."""
+    models, index, fm = [], {}, []
+    for cam in cams_per_frame:
+        key = id(cam)
+        if key not in index:
+            index[key] = len(models)
+            models.append(cam)
+        fm.append(index[key])
+    arr = (nat.CameraModelC * max(len(models), 1))(*[camera_struct(c) for c in models])
+    return arr, len(models), np.asarray(fm, dtype=np.int32)
+
+
+@dataclass
+class BAArrays:
+    """The C-ABI's sfm_ba_problem as numpy arrays (include/sfm_b200.h)."""
+
+    cam_q: np.ndarray          # [F,4]
+    cam_t: np.ndarray          # [F,3]
+    frame_model: np.ndarray    # [F] i32
+    frame_fixed: np.ndarray    # [F] u8
+    models: object             # ctypes array of CameraModelC
+    n_models: int
+    points: np.ndarray         # [P,3]
+    obs_frame: np.ndarray      # [N] i32
+    obs_point: np.ndarray      # [N] i32, non-decreasing
+    obs_uv: np.ndarray         # [N,2]
+    edge_ab: np.ndarray        # [E,2] i32
+    prior_frame: np.ndarray    # [A] i32
+    edge_weight: float = 0.0
+    prior_weight: float = 0.0
+    obs_offset: int = 0
+    n_params_global: int = 0
+
+    def struct(self) -> nat.BAProblemC:
+        self._keep = [self.cam_q, self.cam_t, self.frame_model, self.frame_fixed, self.points,
+                      self.obs_frame, self.obs_point, self.obs_uv, self.edge_ab, self.prior_frame]
+        return nat.BAProblemC(
+            len(self.frame_model), self.n_models, nat.ptr(self.cam_q), nat.ptr(self.cam_t),
+            nat.ptr(self.frame_model), nat.ptr(self.frame_fixed), ctypes.addressof(self.models),
+            len(self.points), nat.ptr(self.points), len(self.obs_frame), nat.ptr(self.obs_frame),
+            nat.ptr(self.obs_point), nat.ptr(self.obs_uv), len(self.edge_ab), len(self.prior_frame),
+            nat.ptr(self.edge_ab), nat.ptr(self.prior_frame), float(self.edge_weight),
+            float(self.prior_weight), int(self.obs_offset), int(self.n_params_global))
+
+    def shard(self, rank: int, world: int) -> "BAArrays":
+        """Point-sharded slice for `rank` (contiguous points balanced by
+        observation count); pose terms stay on rank 0 only."""
+        p0, p1 = shard_ranges(self.obs_point, len(self.points), world)[rank]
+        o0, o1 = np.searchsorted(self.obs_point, [p0, p1])
+        n_free = int((self.frame_fixed == 0).sum())
+        return BAArrays(
+            self.cam_q, self.cam_t, self.frame_model, self.frame_fixed, self.models, self.n_models,
+            np.ascontiguousarray(self.points[p0:p1]), np.ascontiguousarray(self.obs_frame[o0:o1]),
+            np.ascontiguousarray(self.obs_point[o0:o1] - p0, dtype=np.int32),
+            np.ascontiguousarray(self.obs_uv[o0:o1]),
+            self.edge_ab if rank == 0 else np.zeros((0, 2), np.int32),
+            self.prior_frame if rank == 0 else np.zeros(0, np.int32),
+            self.edge_weight, self.prior_weight, int(o0),
+            6 * n_free + 3 * len(self.points))
+
+
+def shard_ranges(obs_point, n_points: int, world: int):
+    """Contiguous point ranges with (near) equal observation counts
+    (SURVEY.md §8e): boundaries at the points where the running observation
+    count crosses r*N/world."""
+    obs_point = np.asarray(obs_point)
+    n = len(obs_point)
+    ptr = np.searchsorted(obs_point, np.arange(n_points + 1))
+    bounds = [0]
+    for r in range(1, world):
+        target = (r * n) // world
+        p = int(np.searchsorted(ptr, target, side="left"))
+        bounds.append(min(max(p, bounds[-1]), n_points))
+    bounds.append(n_points)
+    return [(bounds[r], bounds[r + 1]) for r in range(world)]
+
+
+def _options(loss: RobustLoss, sopt: SolverOptions, dopt: DeviceOptions) -> nat.BAOptionsC:
+    return nat.BAOptionsC(nat.LOSS_KINDS[loss.kind], int(sopt.max_iters), float(loss.param),
+                          float(sopt.grad_tol), float(sopt.param_tol), float(sopt.initial_lambda),
+                          float(sopt.max_lambda), nat.LINSOLVE[dopt.linear_solver],
+                          int(dopt.pcg_max_iters), float(dopt.pcg_rtol), int(dopt.dense_max_dim), 0)
+
+
+def solve_arrays(arrays: BAArrays, loss: RobustLoss = TRIVIAL_LOSS,
+                 options: SolverOptions = None, device: DeviceOptions = None, ctx=None):
+    """sfm_ba_solve on flattened arrays -> (cam_q, cam_t, points, report, raw)."""
+    ctx = ctx or nat.default_context()
+    options = options or SolverOptions()
+    device = device or DEFAULT_DEVICE_OPTIONS
+    prob = arrays.struct()
+    opt = _options(loss, options, device)
+    q = np.array(arrays.cam_q, dtype=np.float64, copy=True)
+    t = np.array(arrays.cam_t, dtype=np.float64, copy=True)
+    X = np.array(arrays.points, dtype=np.float64, copy=True)
+    rep = nat.BAReportC()
+    ctx.check(ctx.lib.sfm_ba_solve(ctx.handle, ctypes.byref(prob), ctypes.byref(opt),
+                                   nat.ptr(q), nat.ptr(t), nat.ptr(X), ctypes.byref(rep)))
+    report = SolverReport(rep.initial_cost, rep.final_cost, rep.iterations,
+                          nat.TERMINATIONS[rep.termination])
+    return q, t, X, report, rep
+
+
+def _check_supported(sparse_map, frames, mode):
+    if mode == RIG_EXTRINSIC:
+        raise NotImplementedError("rig_extrinsic residuals are a SURVEY §8(f) 'next' row")
+    by_cam = {}
+    for f in frames:
+        by_cam.setdefault(sparse_map.keyframes[f].camera_id, []).append(sparse_map.keyframes[f])
+    for seq in by_cam.values():
+        seq = sorted(seq, key=lambda k: k.timestamp)
+        for a, b in zip(seq, seq[1:]):
+            if a.shutter == ROLLING_SHUTTER and b.timestamp - a.timestamp > 0:
+                raise NotImplementedError(
+                    "rolling-shutter residuals are a SURVEY §8(f) 'next' row")
+
+
+def flatten_ba(sparse_map, config, stage=1, mode=PURE):
+    """SparseMap -> (BAArrays, frames, landmark indices, loss).
+
+    Follows the problem construction of mapping.py:399-509: frames sorted,
+    fixed set (+ prior frames in localization_fixed), NoGauge check, points
+    = TRIANGULATED landmarks in map order, observations = inlier obs,
+    landmark-major in track order, lambda_c edges between consecutive frames
+    of each camera, lambda_a priors on non-fixed frames (PURE skips prior
+    provenance)."""
+    loss = config.stage1.loss if stage == 1 else config.stage2.loss
+    frames = sorted(sparse_map.keyframes)
+    fixed = set(sparse_map.fixed_frames)
+    if mode == LOCALIZATION_FIXED:
+        fixed |= {f for f in frames if sparse_map.provenance.get(f) == "prior"}
+    if mode != RIG_EXTRINSIC and not fixed and config.lambda_a <= 0:
+        raise NoGauge("no fixed pose and no absolute prior")
+    _check_supported(sparse_map, frames, mode)
+    fidx = {f: i for i, f in enumerate(frames)}
+    F = len(frames)
+    cam_q = np.empty((F, 4))
+    cam_t = np.empty((F, 3))
+    for i, f in enumerate(frames):
+        pose = sparse_map.keyframes[f].cam_from_world
+        cam_q[i] = pose.quat
+        cam_t[i] = pose.t
+    models, n_models, fm = model_table([sparse_map.cameras[sparse_map.keyframes[f].camera_id]
+                                        for f in frames])
+    fixed_arr = np.array([1 if f in fixed else 0 for f in frames], dtype=np.uint8)
+    lms = [li for li, lm in enumerate(sparse_map.landmarks) if lm.track.status == TRIANGULATED]
+    points = np.array([sparse_map.landmarks[li].position for li in lms],
+                      dtype=np.float64).reshape(-1, 3)
+    of, op, uv = [], [], []
+    for pi, li in enumerate(lms):
+        lm = sparse_map.landmarks[li]
+        for o, ok in zip(lm.track.observations, lm.inlier_mask):
+            if ok:
+                of.append(fidx[o.frame_id])
+                op.append(pi)
+                uv.append(o.pixel)
+    edges = []
+    if config.lambda_c > 0:
+        by_cam = {}
+        for f in frames:
+            by_cam.setdefault(sparse_map.keyframes[f].camera_id, []).append(f)
+        for seq in by_cam.values():
+            edges.extend((fidx[a], fidx[b]) for a, b in zip(seq, seq[1:]))
+    priors = []
+    if config.lambda_a > 0:
+        for f in frames:
+            if f in fixed:
+                continue
+            if mode == PURE and sparse_map.provenance.get(f) == "prior":
+                continue
+            priors.append(fidx[f])
+    arrays = BAArrays(
+        cam_q, cam_t, fm, fixed_arr, models, n_models, np.ascontiguousarray(points),
+        np.asarray(of, dtype=np.int32), np.asarray(op, dtype=np.int32),
+        np.asarray(uv, dtype=np.float64).reshape(-1, 2),
+        np.asarray(edges, dtype=np.int32).reshape(-1, 2), np.asarray(priors, dtype=np.int32),
+        float(config.lambda_c), float(config.lambda_a))
+    return arrays, frames, lms, loss
+
+
+def bundle_adjust(sparse_map, config: MappingConfig = None, stage: int = 1, mode: str = PURE,
+                  device: DeviceOptions = None, ctx=None):
+    """mapping.py:390-527 on the B200.  Returns the SolverReport; poses and
+    TRIANGULATED landmark positions are written back in place.  With a
+    multi-rank context (ctx.world > 1, one process per GPU) the points are
+    sharded across ranks and the camera system is all-reduced over NCCL."""
+    if config is None:
+        config = MappingConfig()
+    arrays, frames, lms, loss = flatten_ba(sparse_map, config, stage, mode)
+    ctx = ctx or nat.default_context()
+    sopt = SolverOptions(max_iters=config.max_solver_iters)
+    if ctx.world > 1:
+        q, t, X, report, _ = _solve_sharded(arrays, loss, sopt, device, ctx)
+    else:
+        q, t, X, report, _ = solve_arrays(arrays, loss, sopt, device, ctx)
+    for i, f in enumerate(frames):
+        if arrays.frame_fixed[i]:
+            continue  # fixed blocks keep their (byte-identical) value
+        if np.array_equal(q[i], arrays.cam_q[i]) and np.array_equal(t[i], arrays.cam_t[i]):
+            continue  # never retracted: keep the entry object
+        kf = sparse_map.keyframes[f]
+        kf.cam_from_world = type(kf.cam_from_world)(q[i], t[i])
+    for pi, li in enumerate(lms):
+        sparse_map.landmarks[li].position = X[pi].copy()
+    return report
+
+
+def _solve_sharded(arrays, loss, sopt, device, ctx):
+    import torch.distributed as dist
+    part = arrays.shard(ctx.rank, ctx.world)
+    q, t, Xs, report, rep = solve_arrays(part, loss, sopt, device, ctx)
+    gathered = [None] * ctx.world
+    dist.all_gather_object(gathered, Xs)
+    return q, t, np.concatenate(gathered, axis=0), report, rep
+
+
+# --- tracks ------------------------------------------------------------------
+
+class TrackArrays:
+    """Tracks as CSR over a frame table (sfm_tracks)."""
+
+    def __init__(self, obs_lists, poses, cameras, active=None):
+        frames = sorted(poses)
+        self.fidx = {f: i for i, f in enumerate(frames)}
+        F = len(frames)
+        self.cam_q = np.empty((F, 4))
+        self.cam_t = np.empty((F, 3))
+        for i, f in enumerate(frames):
+            self.cam_q[i] = poses[f].quat
+            self.cam_t[i] = poses[f].t
+        self.models, self.n_models, self.fm = model_table([cameras[f] for f in frames])
+        counts = np.fromiter((len(o) for o in obs_lists), dtype=np.int64, count=len(obs_lists))
+        self.ptr = np.zeros(len(obs_lists) + 1, dtype=np.int64)
+        np.cumsum(counts, out=self.ptr[1:])
+        n = int(self.ptr[-1])
+        self.obs_frame = np.fromiter((self.fidx[o.frame_id] for obs in obs_lists for o in obs),
+                                     dtype=np.int32, count=n)
+        self.obs_uv = np.array([o.pixel for obs in obs_lists for o in obs],
+                               dtype=np.float64).reshape(-1, 2)
+        self.active = None if active is None else np.asarray(active, dtype=np.uint8)
+
+    def struct(self) -> nat.TracksC:
+        return nat.TracksC(len(self.fm), self.n_models, nat.ptr(self.cam_q), nat.ptr(self.cam_t),
+                           nat.ptr(self.fm), ctypes.addressof(self.models), len(self.ptr) - 1,
+                           len(self.obs_frame), nat.ptr(self.ptr), nat.ptr(self.obs_frame),
+                           nat.ptr(self.obs_uv), nat.ptr(self.active))
+
+
+def _tri_call(observations, poses, cameras, method, min_angle, ctx):
+    if len(observations) < 2:
+        raise ValueError("need at least two observations")
+    ctx = ctx or nat.default_context()
+    ta = TrackArrays([list(observations)], poses, cameras)
+    X = np.empty((1, 3))
+    st = np.empty(1, dtype=np.int8)
+    s = ta.struct()
+    ctx.check(ctx.lib.sfm_triangulate(ctx.handle, ctypes.byref(s), float(min_angle),
+                                      nat.TRI_METHODS[method], nat.ptr(X), nat.ptr(st)))
+    raise_for_tri_status(int(st[0]))
+    return X[0].copy()
+
+
+def triangulate_dlt(observations, poses, cameras, min_angle=np.radians(0.5), ctx=None):
+    """mapping.py:194-221 on device."""
+    return _tri_call(observations, poses, cameras, "dlt", min_angle, ctx)
+
+
+def triangulate_midpoint(observations, poses, cameras, ctx=None):
+    """mapping.py:224-240 on device (no parallax gate, as in the reference)."""
+    return _tri_call(observations, poses, cameras, "midpoint", 0.0, ctx)
+
+
+def ransac_triangulate_batch(tracks, poses, cameras, threshold_px=4.0,
+                             min_angle=np.radians(0.5), method="dlt", ctx=None):
+    """Batched ransac_triangulate over `tracks` in one device call.  Sets each
+    track's status and returns the list of Landmark-or-None in track order."""
+    ctx = ctx or nat.default_context()
+    if not tracks:
+        return []
+    ta = TrackArrays([t.observations for t in tracks], poses, cameras)
+    T = len(tracks)
+    X = np.empty((T, 3))
+    mask = np.empty(len(ta.obs_frame), dtype=np.uint8)
+    st = np.empty(T, dtype=np.int8)
+    s = ta.struct()
+    ctx.check(ctx.lib.sfm_ransac_triangulate(ctx.handle, ctypes.byref(s), float(threshold_px),
+                                             float(min_angle), nat.TRI_METHODS[method], nat.ptr(X),
+                                             nat.ptr(mask), nat.ptr(st)))
+    out = []
+    for i, tr in enumerate(tracks):
+        if st[i] == nat.TRI_OK:
+            tr.status = TRIANGULATED
+            m = mask[ta.ptr[i]:ta.ptr[i + 1]].astype(bool)
+            out.append(Landmark(X[i].copy(), tr, m))
+        else:
+            tr.status = FAILED
+            out.append(None)
+    return out
+
+
+def ransac_triangulate(track, poses, cameras, threshold_px=4.0, min_angle=np.radians(0.5),
+                       method="dlt", seed=42, ctx=None):
+    """mapping.py:255-305 on device (`seed` is unused, as in the reference)."""
+    return ransac_triangulate_batch([track], poses, cameras, threshold_px, min_angle, method,
+                                    ctx)[0]
+
+
+def _reproj_errors(obs_lists, positions, poses, cameras, ctx):
+    ctx = ctx or nat.default_context()
+    ta = TrackArrays(obs_lists, poses, cameras)
+    P = np.ascontiguousarray(np.asarray(positions, dtype=np.float64).reshape(-1, 3))
+    err = np.empty(len(ta.obs_frame))
+    s = ta.struct()
+    ctx.check(ctx.lib.sfm_reprojection_errors(ctx.handle, ctypes.byref(s), nat.ptr(P),
+                                              nat.ptr(err)))
+    return err, ta
+
+
+def reprojection_error(map_or_poses, cameras, observation, point, ctx=None):
+    """mapping.py:243-252 (inf when the projection raises)."""
+    poses = {observation.frame_id: map_or_poses[observation.frame_id]}
+    cams = {observation.frame_id: cameras[observation.frame_id]}
+    err, _ = _reproj_errors([[observation]], [point], poses, cams, ctx)
+    return float(err[0])
+
+
+def remove_outliers(sparse_map, threshold_px: float, ctx=None):
+    """mapping.py:544-566 on device: strict `>` gate on inlier observations,
+    landmarks left with < 2 inliers revert to PENDING and are dropped."""
+    ctx = ctx or nat.default_context()
+    poses = {f: kf.cam_from_world for f, kf in sparse_map.keyframes.items()}
+    cams = {f: sparse_map.camera_of(f) for f in sparse_map.keyframes}
+    tri = [lm for lm in sparse_map.landmarks if lm.track.status == TRIANGULATED]
+    removed = 0
+    if tri:
+        ta = TrackArrays([lm.track.observations for lm in tri], poses, cams)
+        mask = np.ascontiguousarray(np.concatenate([np.asarray(lm.inlier_mask, dtype=np.uint8)
+                                                    for lm in tri]))
+        P = np.ascontiguousarray(np.array([lm.position for lm in tri], dtype=np.float64))
+        inl = np.empty(len(tri), dtype=np.int32)
+        rm = ctypes.c_int64()
+        s = ta.struct()
+        ctx.check(ctx.lib.sfm_gate(ctx.handle, ctypes.byref(s), nat.ptr(P), float(threshold_px),
+                                   nat.ptr(mask), nat.ptr(inl), ctypes.byref(rm)))
+        removed = int(rm.value)
+        for i, lm in enumerate(tri):
+            m = mask[ta.ptr[i]:ta.ptr[i + 1]].astype(bool)
+            if not np.array_equal(m, lm.inlier_mask):
+                lm.inlier_mask[:] = m
+            if inl[i] < 2:
+                lm.track.status = PENDING
+    tri_ids = {id(lm) for lm in tri}
+    sparse_map.landmarks = [lm for lm in sparse_map.landmarks
+                            if not (id(lm) in tri_ids and lm.track.status == PENDING)]
+    return sparse_map, removed
+
+
+def iterative_map(keyframes, tracks, cameras, config: MappingConfig = None, rig=None,
+                  mode: str = PURE, provenance=None, fixed_frames=None, device=None,
+                  ctx=None) -> SparseMap:
+    """mapping.py:569-624: rounds of {batched RANSAC triangulation of pending
+    tracks -> stage-1 BA -> 4 px gate} until a round neither adds nor
+    removes, then stage-2 BA and the 2 px gate."""
+    if config is None:
+        config = MappingConfig()
+    kf_map = {kf.frame_id: kf for kf in keyframes}
+    sparse_map = SparseMap(kf_map, dict(cameras), [], rig, dict(provenance or {}),
+                           set(fixed_frames or ()))
+    has_prior = any(sparse_map.provenance.get(f) == "prior" for f in kf_map)
+    needs_anchor = not (mode == LOCALIZATION_FIXED and has_prior)
+    if not sparse_map.fixed_frames and kf_map and needs_anchor:
+        new = [f for f in kf_map if sparse_map.provenance.get(f) != "prior"]
+        sparse_map.fixed_frames = {min(new) if new else min(kf_map)}
+    stats = []
+    for round_idx in range(config.max_outer_iters):
+        poses = {f: kf.cam_from_world for f, kf in kf_map.items()}
+        cams = {f: sparse_map.camera_of(f) for f in kf_map}
+        pending = [t for t in tracks if t.status == PENDING]
+        results = ransac_triangulate_batch(
+            pending, poses, cams, threshold_px=config.stage1.outlier_px,
+            min_angle=config.min_triangulation_angle, method=config.triangulation, ctx=ctx)
+        added = 0
+        for lm in results:
+            if lm is not None:
+                sparse_map.landmarks.append(lm)
+                added += 1
+        if sparse_map.landmarks:
+            bundle_adjust(sparse_map, config, stage=1, mode=mode, device=device, ctx=ctx)
+        _, removed = remove_outliers(sparse_map, config.stage1.outlier_px, ctx=ctx)
+        stats.append({"round": round_idx, "added": added, "removed": removed,
+                      "landmarks": len(sparse_map.landmarks)})
+        if added == 0 and removed == 0:
+            break
+    if sparse_map.landmarks:
+        bundle_adjust(sparse_map, config, stage=2, mode=mode, device=device, ctx=ctx)
+        _, removed = remove_outliers(sparse_map, config.stage2.outlier_px, ctx=ctx)
+        stats.append({"round": "final", "added": 0, "removed": removed,
+                      "landmarks": len(sparse_map.landmarks)})
+    sparse_map.round_stats = stats
+    return sparse_map
+
+
+def mean_reprojection_error(sparse_map, ctx=None) -> float:
+    """mapping.py:627-636."""
+    poses = {f: kf.cam_from_world for f, kf in sparse_map.keyframes.items()}
+    cams = {f: sparse_map.camera_of(f) for f in sparse_map.keyframes}
+    lms = [lm for lm in sparse_map.landmarks if lm.track.status == TRIANGULATED]
+    obs = [lm.inlier_observations() for lm in lms]
+    if not any(obs):
+        return 0.0
+    err, _ = _reproj_errors(obs, [lm.position for lm in lms], poses, cams, ctx)
+    return float(np.mean(err)) if len(err) else 0.0
+
+
+__all__ = [
+    "PENDING", "TRIANGULATED", "FAILED", "PURE", "LOCALIZATION_FIXED", "LOCALIZATION_ADJUST",
+    "RIG_EXTRINSIC", "Observation", "Track", "Landmark", "SparseMap", "StageConfig",
+    "MappingConfig", "BAArrays", "flatten_ba", "solve_arrays", "shard_ranges", "bundle_adjust",
+    "triangulate_dlt", "triangulate_midpoint", "reprojection_error", "ransac_triangulate",
+    "ransac_triangulate_batch", "remove_outliers", "iterative_map", "mean_reprojection_error",
+    "CameraModel", "Keyframe",
+]

@@ -1,0 +1,303 @@
+"""Vectorised synthetic scenes of the benchmark shapes.
+
+The reference generator (synth.py:119-186) loops over frames x landmarks in
+Python and cannot reach config scale, so scenes are generated here directly
+in the flattened layout:
+
+  * pinhole fx=fy=500, cx=320, cy=240, 640x480 (synth.py:20-21);
+  * "line"/"curve": a driving sequence, each point observed by k consecutive
+    frames; "venice": cameras on a ring looking at a central plaza, each
+    point observed by a random co-visible subset of ring neighbours
+    (BAL-Venice-shaped counts);
+  * pixel noise N(0, noise_px), optional outliers shifted 20-50 px,
+  * initial poses exp(N(0, pose_sigma) I6) T_gt except fixed frames, points
+    + N(0, point_sigma) (test_mapping.py:287-294);
+  * points ordered by their first observing frame and observations sorted
+    by frame inside a track, like build_tracks (mapping.py:148-160).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+CAMERA = dict(kind="pinhole", fx=500.0, fy=500.0, cx=320.0, cy=240.0, width=640, height=480)
+
+
+def _rodrigues_batch(xi):
+    """exp_map for a batch of 6-vectors -> (q [n,4], t [n,3]) (se3.py:143-194)."""
+    phi, rho = xi[:, :3], xi[:, 3:]
+    theta = np.linalg.norm(phi, axis=1)
+    half = 0.5 * theta
+    small = theta < 1e-8
+    ts = np.where(small, 1.0, theta)
+    w = np.where(small, 1.0 - half * half / 2.0, np.cos(half))
+    s = np.where(small, 0.5 - half * half / 12.0, np.sin(half) / ts)
+    q = np.concatenate([w[:, None], s[:, None] * phi], axis=1)
+    q /= np.linalg.norm(q, axis=1, keepdims=True)
+    q[q[:, 0] < 0] *= -1.0
+    P = _hat_batch(phi)
+    PP = P @ P
+    th2 = np.where(small, 1.0, theta ** 2)
+    a = np.where(theta < 1e-6, 0.5, (1.0 - np.cos(theta)) / th2)
+    b = np.where(theta < 1e-6, 1.0 / 6.0, (theta - np.sin(theta)) / (th2 * ts))
+    J = np.eye(3)[None] + a[:, None, None] * P + b[:, None, None] * PP
+    return q, np.einsum("nij,nj->ni", J, rho)
+
+
+def _hat_batch(v):
+    H = np.zeros((len(v), 3, 3))
+    H[:, 0, 1], H[:, 0, 2] = -v[:, 2], v[:, 1]
+    H[:, 1, 0], H[:, 1, 2] = v[:, 2], -v[:, 0]
+    H[:, 2, 0], H[:, 2, 1] = -v[:, 1], v[:, 0]
+    return H
+
+
+def quat_to_R(q):
+    w, x, y, z = q[..., 0], q[..., 1], q[..., 2], q[..., 3]
+    R = np.empty(q.shape[:-1] + (3, 3))
+    R[..., 0, 0] = 1 - 2 * (y * y + z * z)
+    R[..., 0, 1] = 2 * (x * y - w * z)
+    R[..., 0, 2] = 2 * (x * z + w * y)
+    R[..., 1, 0] = 2 * (x * y + w * z)
+    R[..., 1, 1] = 1 - 2 * (x * x + z * z)
+    R[..., 1, 2] = 2 * (y * z - w * x)
+    R[..., 2, 0] = 2 * (x * z - w * y)
+    R[..., 2, 1] = 2 * (y * z + w * x)
+    R[..., 2, 2] = 1 - 2 * (x * x + y * y)
+    return R
+
+
+def R_to_quat(R):
+    """Batched rotation matrix -> canonical quaternion (se3.py:59-77)."""
+    n = len(R)
+    q = np.empty((n, 4))
+    tr = np.trace(R, axis1=1, axis2=2)
+    for k in range(n):
+        r = R[k]
+        if tr[k] > 0:
+            s = np.sqrt(tr[k] + 1.0) * 2
+            q[k] = [0.25 * s, (r[2, 1] - r[1, 2]) / s, (r[0, 2] - r[2, 0]) / s,
+                    (r[1, 0] - r[0, 1]) / s]
+        else:
+            i = int(np.argmax(np.diag(r)))
+            j, l = (i + 1) % 3, (i + 2) % 3
+            s = np.sqrt(r[i, i] - r[j, j] - r[l, l] + 1.0) * 2
+            q[k, 0] = (r[l, j] - r[j, l]) / s
+            q[k, 1 + i] = 0.25 * s
+            q[k, 1 + j] = (r[j, i] + r[i, j]) / s
+            q[k, 1 + l] = (r[l, i] + r[i, l]) / s
+    q /= np.linalg.norm(q, axis=1, keepdims=True)
+    q[q[:, 0] < 0] *= -1.0
+    return q
+
+
+def _look_poses(centers, forward):
+    """cam_from_world with +z along `forward`, +y down (synth.py:89-96)."""
+    f = forward / np.linalg.norm(forward, axis=1, keepdims=True)
+    down = np.array([0.0, 0.0, -1.0])
+    right = np.cross(down, f)
+    right /= np.linalg.norm(right, axis=1, keepdims=True)
+    dn = np.cross(f, right)
+    R_wc = np.stack([right, dn, f], axis=2)      # columns
+    R_cw = np.transpose(R_wc, (0, 2, 1))
+    t = -np.einsum("nij,nj->ni", R_cw, centers)
+    return R_to_quat(R_cw), t
+
+
+@dataclass
+class Scene:
+    """Flattened BA scene: ground truth, initial state and measurements."""
+
+    cam_q_gt: np.ndarray
+    cam_t_gt: np.ndarray
+    points_gt: np.ndarray
+    cam_q: np.ndarray
+    cam_t: np.ndarray
+    points: np.ndarray
+    obs_frame: np.ndarray
+    obs_point: np.ndarray
+    obs_uv: np.ndarray
+    outlier: np.ndarray
+    frame_fixed: np.ndarray
+    camera: dict
+    seed: int
+    shape: str
+
+    @property
+    def n_frames(self):
+        return len(self.cam_q)
+
+    @property
+    def n_points(self):
+        return len(self.points)
+
+    @property
+    def n_obs(self):
+        return len(self.obs_frame)
+
+
+def _project(R, t, X, cam):
+    pc = np.einsum("nij,nj->ni", R, X) + t
+    z = pc[:, 2]
+    with np.errstate(divide="ignore", invalid="ignore"):
+        u = cam["fx"] * pc[:, 0] / z + cam["cx"]
+        v = cam["fy"] * pc[:, 1] / z + cam["cy"]
+    return u, v, z
+
+
+def make_scene(n_frames: int, n_points: int, n_obs: int, shape: str = "line", seed: int = 0,
+               noise_px: float = 0.5, pose_sigma: float = 0.002, point_sigma: float = 0.01,
+               outlier_frac: float = 0.0, fixed=(0,), window: int = None,
+               depth=(1.0, 40.0)) -> Scene:
+    rng = np.random.default_rng(seed)
+    cam = dict(CAMERA)
+    F = n_frames
+    if shape == "venice":
+        ang = 2 * np.pi * np.arange(F) / F
+        radius = 60.0
+        centers = np.stack([radius * np.cos(ang), radius * np.sin(ang),
+                            rng.uniform(1.0, 3.0, F)], axis=1)
+        target = np.stack([rng.normal(0, 5.0, F), rng.normal(0, 5.0, F), np.full(F, 5.0)], axis=1)
+        q_gt, t_gt = _look_poses(centers, target - centers)
+        window = window or 40
+    else:
+        s = np.arange(F) * 1.0
+        if shape == "curve":
+            r = max(F, 10) * 1.0 / np.pi
+            th = s / r
+            centers = np.stack([r * np.sin(th), r * (1 - np.cos(th)), np.zeros(F)], axis=1)
+        else:
+            centers = np.stack([s, 0.05 * np.sin(0.1 * s), np.zeros(F)], axis=1)
+        nxt = np.roll(centers, -1, axis=0)
+        nxt[-1] = centers[-1] + (centers[-1] - centers[-2]) if F > 1 else centers[-1] + [1, 0, 0]
+        q_gt, t_gt = _look_poses(centers, nxt - centers)
+        window = window or 12
+    R_gt = quat_to_R(q_gt)
+    kmean = n_obs / max(n_points, 1)
+
+    # per point: home frame, observation count
+    home = np.sort(rng.integers(0, F, n_points))
+    base = int(np.floor(kmean))
+    k = np.full(n_points, base)
+    k[rng.random(n_points) < (kmean - base)] += 1
+    k = np.maximum(k, 2)
+    # point in front of its home camera
+    u0 = rng.uniform(20, cam["width"] - 20, n_points)
+    v0 = rng.uniform(20, cam["height"] - 20, n_points)
+    d0 = rng.uniform(depth[0], depth[1] if shape != "venice" else 70.0, n_points)
+    ray = np.stack([(u0 - cam["cx"]) / cam["fx"], (v0 - cam["cy"]) / cam["fy"], np.ones(n_points)], 1)
+    pc = ray * d0[:, None]
+    X = np.einsum("nji,nj->ni", R_gt[home], pc - t_gt[home])  # R^T (p - t)
+
+    # candidate frames: home first, then neighbours
+    M = 2 * window
+    if shape == "venice":
+        offs = rng.integers(-window, window + 1, (n_points, M))
+        offs[offs == 0] = window + 1
+        cand = (home[:, None] + offs) % F
+    else:
+        offs = np.tile(np.arange(1, M + 1), (n_points, 1))
+        back = rng.random((n_points, M)) < 0.25
+        offs = np.where(back, -offs // 2 - 1, offs)
+        cand = home[:, None] + offs
+    valid = (cand >= 0) & (cand < F)
+    cand = np.clip(cand, 0, F - 1)
+    Xr = np.repeat(X, M, axis=0)
+    u, v, z = _project(R_gt[cand.ravel()], t_gt[cand.ravel()], Xr, cam)
+    vis = (valid.ravel() & (z > 0.5) & (z < 120.0) & (u >= 0) & (u < cam["width"]) &
+           (v >= 0) & (v < cam["height"])).reshape(n_points, M)
+    # drop duplicate frames per point (keep first occurrence)
+    order = np.argsort(cand, axis=1, kind="stable")
+    sc = np.take_along_axis(cand, order, 1)
+    dup_sorted = np.zeros_like(sc, dtype=bool)
+    dup_sorted[:, 1:] = sc[:, 1:] == sc[:, :-1]
+    dup = np.zeros_like(dup_sorted)
+    np.put_along_axis(dup, order, dup_sorted, 1)
+    vis &= ~dup
+    vis &= cand != home[:, None]
+    # take the first k-1 visible candidates
+    rank = np.cumsum(vis, axis=1)
+    take = vis & (rank <= (k - 1)[:, None])
+    n_take = take.sum(1)
+    keep_pt = n_take >= 1
+    frames_list = np.concatenate([home[:, None], np.where(take, cand, -1)], axis=1)
+    frames_list = frames_list[keep_pt]
+    X = X[keep_pt]
+    P = len(X)
+    # sort frames inside each track; gather observations
+    frames_list = np.where(frames_list < 0, np.iinfo(np.int64).max, frames_list)
+    frames_list.sort(axis=1)
+    mask = frames_list != np.iinfo(np.int64).max
+    cnt = mask.sum(1)
+    obs_point = np.repeat(np.arange(P), cnt).astype(np.int32)
+    obs_frame = frames_list[mask].astype(np.int32)
+    # re-order points by first frame (already sorted by home; first frame may
+    # precede home via backward candidates) -- stable sort keeps determinism
+    first = frames_list[:, 0]
+    perm = np.argsort(first, kind="stable")
+    inv = np.empty_like(perm)
+    inv[perm] = np.arange(P)
+    X = X[perm]
+    newpt = inv[obs_point]
+    o2 = np.lexsort((np.arange(len(newpt)), newpt))
+    obs_point = newpt[o2].astype(np.int32)
+    obs_frame = obs_frame[o2]
+    u, v, _ = _project(R_gt[obs_frame], t_gt[obs_frame], X[obs_point], cam)
+    uv = np.stack([u, v], 1) + rng.normal(0, noise_px, (len(u), 2)) if noise_px else np.stack([u, v], 1)
+    outlier = np.zeros(len(u), bool)
+    if outlier_frac > 0:
+        outlier = rng.random(len(u)) < outlier_frac
+        mag = rng.uniform(20, 50, outlier.sum())
+        ang = rng.uniform(0, 2 * np.pi, outlier.sum())
+        uv[outlier] += np.stack([mag * np.cos(ang), mag * np.sin(ang)], 1)
+    fixed_arr = np.zeros(F, np.uint8)
+    fixed_arr[list(fixed)] = 1
+    # perturbed initial state
+    dq, dt = _rodrigues_batch(rng.normal(0, pose_sigma, (F, 6)))
+    Rd = quat_to_R(dq)
+    R0 = Rd @ R_gt
+    t0 = np.einsum("nij,nj->ni", Rd, t_gt) + dt
+    q0 = R_to_quat(R0)
+    free = fixed_arr == 0
+    cam_q = np.where(free[:, None], q0, q_gt)
+    cam_t = np.where(free[:, None], t0, t_gt)
+    pts0 = X + rng.normal(0, point_sigma, X.shape)
+    return Scene(q_gt, t_gt, X, np.ascontiguousarray(cam_q), np.ascontiguousarray(cam_t),
+                 np.ascontiguousarray(pts0), np.ascontiguousarray(obs_frame),
+                 np.ascontiguousarray(obs_point), np.ascontiguousarray(uv), outlier, fixed_arr,
+                 cam, seed, shape)
+
+
+CONFIGS = {
+    # SURVEY.md §8(d)
+    1: dict(n_frames=20, n_points=2000, n_obs=10000, shape="line"),
+    2: dict(n_frames=500, n_points=100000, n_obs=1000000, shape="curve", outlier_frac=0.05),
+    3: dict(n_frames=1778, n_points=993923, n_obs=5001946, shape="venice"),
+    4: dict(n_frames=2000, n_points=2000000, n_obs=10000000, shape="line", outlier_frac=0.05),
+    5: dict(n_frames=10000, n_points=10000000, n_obs=50000000, shape="line"),
+}
+
+
+def config_scene(cfg: int, seed: int = 0, **kw) -> Scene:
+    args = dict(CONFIGS[cfg])
+    args.update(kw)
+    return make_scene(seed=seed, **args)
+
+
+def scene_arrays(scene: Scene, lambda_c: float = 1.0, lambda_a: float = 1.0):
+    """Scene -> mapping.BAArrays with the default bundle_adjust pose terms
+    (consecutive-frame edges, priors on free frames)."""
+    from .mapping import BAArrays, model_table
+    from .cameras import CameraModel
+    cm = CameraModel(**scene.camera)
+    models, n_models, fm = model_table([cm] * scene.n_frames)
+    F = scene.n_frames
+    edges = np.stack([np.arange(F - 1), np.arange(1, F)], 1).astype(np.int32) if lambda_c > 0 \
+        else np.zeros((0, 2), np.int32)
+    priors = np.flatnonzero(scene.frame_fixed == 0).astype(np.int32) if lambda_a > 0 \
+        else np.zeros(0, np.int32)
+    return BAArrays(scene.cam_q, scene.cam_t, fm, scene.frame_fixed, models, n_models,
+                    scene.points, scene.obs_frame, scene.obs_point, scene.obs_uv, edges, priors,
+                    float(lambda_c), float(lambda_a))

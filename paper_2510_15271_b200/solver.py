@@ -1,0 +1,60 @@
+"""Solver configuration / report records (solver.py:25-95).
+
+`RobustLoss`, `SolverOptions` and `SolverReport` keep the reference's fields
+and defaults; `DeviceOptions` holds the B200-only knobs (how the reduced
+camera system is solved).  The LM loop itself runs in csrc/ba.cu.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+
+@dataclass(frozen=True)
+class RobustLoss:
+    """rho applied to the squared residual norm s = ||r||^2 (solver.py:25-51)."""
+
+    kind: str = "trivial"        # trivial | huber | cauchy
+    param: float = 1.0
+
+    def __post_init__(self):
+        if self.kind not in ("trivial", "huber", "cauchy"):
+            raise ValueError(f"unknown loss kind {self.kind!r}")
+
+
+TRIVIAL_LOSS = RobustLoss()
+
+
+@dataclass
+class SolverOptions:
+    max_iters: int = 50
+    grad_tol: float = 1e-10
+    param_tol: float = 1e-12
+    initial_lambda: float = 1e-4
+    max_lambda: float = 1e32
+
+
+@dataclass
+class SolverReport:
+    initial_cost: float
+    final_cost: float
+    iterations: int
+    termination: str
+
+
+@dataclass
+class DeviceOptions:
+    """How the reduced camera system S dc = b is solved on the B200.
+
+    linear_solver: "auto" (dense Cholesky when 6*free_frames <= dense_max_dim,
+    block-Jacobi PCG otherwise), "dense" or "pcg".  pcg_rtol is the relative
+    residual |r|/|b| at which PCG stops.
+    """
+
+    linear_solver: str = "auto"
+    pcg_rtol: float = 1e-12
+    pcg_max_iters: int = 2000
+    dense_max_dim: int = 210
+
+
+DEFAULT_DEVICE_OPTIONS = DeviceOptions()

@@ -1,0 +1,425 @@
+"""Generates the golden fixtures tests/golden/*.npz by running the REFERENCE
+implementation (sfmkit, imported from /root/reference/pkg/src) on seeded
+synthetic inputs.  Run here (the survey container), never on the GPU box:
+
+    PYTHONDONTWRITEBYTECODE=1 python tests/golden/make_golden.py
+
+Each fixture stores the flattened inputs in the C-ABI layout
+(include/sfm_b200.h) together with the reference outputs, so the oracle
+(oracle/) and the CUDA path can both be checked against the reference
+without the reference being present.
+"""
+
+from __future__ import annotations
+
+import os
+import sys
+import time
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+REPO = os.path.dirname(os.path.dirname(HERE))
+sys.path.insert(0, "/root/reference/pkg/src")
+sys.path.insert(0, REPO)
+sys.dont_write_bytecode = True
+
+import sfmkit.mapping as M  # noqa: E402
+import sfmkit.solver as SV  # noqa: E402
+from sfmkit.cameras import CameraModel, project, project_with_pose_jacobian, unproject  # noqa: E402
+from sfmkit.keyframes import Keyframe  # noqa: E402
+from sfmkit.posegraph import PoseEdge, _edge_residual_fn  # noqa: E402
+from sfmkit.se3 import Pose, exp_map  # noqa: E402
+
+from paper_2510_15271_b200 import mapping as D  # noqa: E402  (flattening only)
+
+CAM = CameraModel("pinhole", 500.0, 500.0, 320.0, 240.0, 640, 480)
+
+
+def models_array(arrays_models, n):
+    out = np.zeros((n, 7))
+    for i in range(n):
+        m = arrays_models[i]
+        out[i] = [m.kind, m.fx, m.fy, m.cx, m.cy, m.k1, m.k2]
+    return out
+
+
+def flat_dict(arrays, prefix=""):
+    return {prefix + "cam_q": arrays.cam_q, prefix + "cam_t": arrays.cam_t,
+            prefix + "frame_model": arrays.frame_model, prefix + "frame_fixed": arrays.frame_fixed,
+            prefix + "models": models_array(arrays.models, arrays.n_models),
+            prefix + "points": arrays.points, prefix + "obs_frame": arrays.obs_frame,
+            prefix + "obs_point": arrays.obs_point, prefix + "obs_uv": arrays.obs_uv,
+            prefix + "edge_ab": arrays.edge_ab, prefix + "prior_frame": arrays.prior_frame,
+            prefix + "edge_weight": np.float64(arrays.edge_weight),
+            prefix + "prior_weight": np.float64(arrays.prior_weight)}
+
+
+LOSS_CODE = {"trivial": 0, "huber": 1, "cauchy": 2}
+
+
+# --- scenes (pattern of test_mapping.py:24-52, :275-295) ----------------------
+
+def cam_pose(center, rot_xi=(0.0, 0.0, 0.0)):
+    R = exp_map(np.array([*rot_xi, 0, 0, 0])).R
+    return Pose.from_rt(R, -R @ np.asarray(center, dtype=float))
+
+
+def scene(rng, n_frames=6, n_points=40, spacing=0.8):
+    points = rng.uniform([-4, -3, 6], [4, 3, 14], (n_points, 3))
+    poses = {i: cam_pose([spacing * i, 0.05 * i, 0], (0.02 * i, -0.03 * i, 0.01 * i))
+             for i in range(n_frames)}
+    return points, poses
+
+
+def observations(point, poses, noise=0.0, rng=None):
+    obs = []
+    for f in sorted(poses):
+        pix = project(CAM, poses[f], point)
+        if not (0 <= pix[0] < CAM.width and 0 <= pix[1] < CAM.height):
+            continue
+        if noise and rng is not None:
+            pix = pix + rng.normal(0, noise, 2)
+        obs.append(M.Observation(f, 0, pix))
+    return obs
+
+
+def map_from_scene(points, poses, perturb=0.0, rng=None, fixed_frames=(0, 1), noise=0.0,
+                   outlier_every=0, outlier_px=(35.0, -25.0)):
+    kfs = {f: Keyframe(f, float(f), 0, poses[f]) for f in poses}
+    smap = M.SparseMap(kfs, {0: CAM}, fixed_frames=set(fixed_frames))
+    for i, p in enumerate(points):
+        obs = observations(p, poses, noise, rng)
+        if len(obs) < 2:
+            continue
+        if outlier_every and i % outlier_every == 0:
+            obs[1].pixel = obs[1].pixel + np.array(outlier_px)
+        smap.landmarks.append(M.Landmark(p.copy(), M.Track(obs, status=M.TRIANGULATED),
+                                         np.ones(len(obs), bool)))
+    if perturb and rng is not None:
+        for f in poses:
+            if f in smap.fixed_frames:
+                continue
+            kfs[f].cam_from_world = exp_map(rng.normal(0, perturb, 6)) @ kfs[f].cam_from_world
+        for lm in smap.landmarks:
+            lm.position = lm.position + rng.normal(0, 5 * perturb, 3)
+    return smap
+
+
+def map_from_arrays(sc):
+    """paper_2510_15271_b200.scenes.Scene -> sfmkit SparseMap."""
+    kfs = {f: Keyframe(f, float(f), 0, Pose(sc.cam_q[f], sc.cam_t[f])) for f in range(sc.n_frames)}
+    smap = M.SparseMap(kfs, {0: CAM}, fixed_frames={int(f) for f in np.flatnonzero(sc.frame_fixed)})
+    ptr = np.searchsorted(sc.obs_point, np.arange(sc.n_points + 1))
+    for p in range(sc.n_points):
+        obs = [M.Observation(int(sc.obs_frame[o]), 0, sc.obs_uv[o]) for o in range(ptr[p], ptr[p + 1])]
+        smap.landmarks.append(M.Landmark(sc.points[p].copy(), M.Track(obs, status=M.TRIANGULATED),
+                                         np.ones(len(obs), bool)))
+    return smap
+
+
+# --- BA fixtures -----------------------------------------------------------------
+
+def run_ba(name, smap, config, stage=1, mode=M.PURE, capture_jacobian=True):
+    arrays, frames, lms, loss = D.flatten_ba(smap, config, stage, mode)
+    captured = {}
+    orig = M.solve
+
+    def spy(problem, options):
+        cost, res = problem.evaluate()
+        captured["ref_initial_residual"] = res
+        if capture_jacobian:
+            offsets, n = SV._free_layout(problem)
+            J, r = SV._assemble(problem, offsets, n)
+            captured["ref_J"] = J.toarray()
+            captured["ref_r"] = r
+        return orig(problem, options)
+
+    M.solve = spy
+    t0 = time.time()
+    out = {}
+    try:
+        rep = M.bundle_adjust(smap, config, stage=stage, mode=mode)
+        out.update(ref_initial_cost=rep.initial_cost, ref_final_cost=rep.final_cost,
+                   ref_iterations=rep.iterations, ref_termination=rep.termination,
+                   ref_exception="")
+    except Exception as e:  # noqa: BLE001 -- the exception class is the golden value
+        out.update(ref_exception=type(e).__name__, ref_message=str(e))
+    finally:
+        M.solve = orig
+    dt = time.time() - t0
+    q = np.array([smap.keyframes[f].cam_from_world.quat for f in frames])
+    t = np.array([smap.keyframes[f].cam_from_world.t for f in frames])
+    X = np.array([smap.landmarks[li].position for li in lms]).reshape(-1, 3)
+    out.update(ref_cam_q=q, ref_cam_t=t, ref_points=X, ref_seconds=dt)
+    out.update(captured)
+    out.update(flat_dict(arrays))
+    out.update(loss_kind=LOSS_CODE[loss.kind], loss_param=float(loss.param),
+               max_iters=config.max_solver_iters)
+    np.savez_compressed(os.path.join(HERE, f"ba_{name}.npz"), **out)
+    print(f"ba_{name}: N={len(arrays.obs_frame)} P={len(arrays.points)} "
+          f"{out.get('ref_termination', out.get('ref_exception'))} "
+          f"iters={out.get('ref_iterations')} {dt:.1f}s")
+
+
+def ba_fixtures():
+    rng = np.random.default_rng(42)
+    pts, poses = scene(rng, 6, 40)
+    run_ba("plain_stage2", map_from_scene(pts, poses, 0.01, rng),
+           M.MappingConfig(lambda_a=0.0, lambda_c=0.0, max_solver_iters=100), stage=2)
+    rng = np.random.default_rng(7)
+    pts, poses = scene(rng, 6, 40)
+    run_ba("huber_outliers", map_from_scene(pts, poses, 0.002, rng, fixed_frames=(0,), noise=0.3,
+                                            outlier_every=7),
+           M.MappingConfig(), stage=1)
+    rng = np.random.default_rng(11)
+    pts, poses = scene(rng, 7, 50)
+    cfg = M.MappingConfig(stage1=M.StageConfig(4.0, SV.RobustLoss("cauchy", 1.5)), lambda_c=2.0,
+                          lambda_a=0.5, max_solver_iters=30)
+    run_ba("cauchy_pose_terms", map_from_scene(pts, poses, 0.005, rng, fixed_frames=(0,), noise=0.5,
+                                               outlier_every=9), cfg, stage=1)
+    rng = np.random.default_rng(3)
+    pts, poses = scene(rng, 6, 30)
+    smap = map_from_scene(pts, poses, 0.01, rng, fixed_frames=())
+    smap.provenance = {f: ("prior" if f < 3 else "new") for f in poses}
+    for f in range(3):
+        smap.keyframes[f].cam_from_world = poses[f]
+    run_ba("localization_fixed", smap,
+           M.MappingConfig(lambda_a=0.0, lambda_c=0.0, max_solver_iters=100), stage=2,
+           mode=M.LOCALIZATION_FIXED)
+    rng = np.random.default_rng(5)
+    pts, poses = scene(rng, 6, 30)
+    smap = map_from_scene(pts, poses, 0.01, rng, fixed_frames=(0,))
+    smap.provenance = {f: ("prior" if f < 3 else "new") for f in poses}
+    run_ba("localization_adjust", smap,
+           M.MappingConfig(lambda_a=1e-4, lambda_c=0.0, max_solver_iters=100), stage=2,
+           mode=M.LOCALIZATION_ADJUST)
+    rng = np.random.default_rng(9)
+    pts, poses = scene(rng, 4, 20)
+    run_ba("prior_gauge", map_from_scene(pts, poses, 0.003, rng, fixed_frames=()),
+           M.MappingConfig(lambda_a=10.0, lambda_c=0.0), stage=2)
+    rng = np.random.default_rng(13)
+    pts, poses = scene(rng, 5, 25)
+    run_ba("pure_provenance_lc", _with_provenance(map_from_scene(pts, poses, 0.004, rng,
+                                                                 fixed_frames=(0,), noise=0.2)),
+           M.MappingConfig(lambda_c=100.0, lambda_a=3.0), stage=1)
+    # initial state with a point behind a camera: NonPositiveDepth from evaluate()
+    rng = np.random.default_rng(17)
+    pts, poses = scene(rng, 4, 12)
+    smap = map_from_scene(pts, poses, 0.0, rng, fixed_frames=(0,))
+    smap.landmarks[3].position = np.array([0.0, 0.0, -5.0])
+    run_ba("depth_error", smap, M.MappingConfig(), stage=1)
+    # config-1: 20 cams / ~2k pts / ~10k obs, 10 LM iterations, Huber
+    from paper_2510_15271_b200.scenes import config_scene
+    sc = config_scene(1, seed=1)
+    smap = map_from_arrays(sc)
+    run_ba("config1", smap, M.MappingConfig(max_solver_iters=10), stage=1, capture_jacobian=False)
+
+
+def _with_provenance(smap):
+    smap.provenance = {f: ("prior" if f in (1, 2) else "new") for f in smap.keyframes}
+    return smap
+
+
+# --- triangulation / gating fixtures ----------------------------------------------
+
+def track_fixture(name, tracks, poses, thr, min_angle, method):
+    frames = sorted(poses)
+    fidx = {f: i for i, f in enumerate(frames)}
+    ptr = np.zeros(len(tracks) + 1, np.int64)
+    ptr[1:] = np.cumsum([len(t.observations) for t in tracks])
+    of = np.array([fidx[o.frame_id] for t in tracks for o in t.observations], np.int32)
+    uv = np.array([o.pixel for t in tracks for o in t.observations]).reshape(-1, 2)
+    q = np.array([poses[f].quat for f in frames])
+    t = np.array([poses[f].t for f in frames])
+    cams = {f: CAM for f in frames}
+    X = np.full((len(tracks), 3), np.nan)
+    mask = np.zeros(len(of), np.uint8)
+    status = np.zeros(len(tracks), np.int8)
+    dX = np.full((len(tracks), 3), np.nan)
+    dstat = np.zeros(len(tracks), np.int8)
+    codes = {"InsufficientParallax": 1, "CheiralityViolation": 2, "ParallelRays": 3,
+             "ValueError": 4}
+    for i, tr in enumerate(tracks):
+        trc = M.Track(list(tr.observations))
+        lm = M.ransac_triangulate(trc, poses, cams, threshold_px=thr, min_angle=min_angle,
+                                  method=method)
+        if lm is None:
+            status[i] = 6
+        else:
+            X[i] = lm.position
+            mask[ptr[i]:ptr[i + 1]] = lm.inlier_mask
+        try:
+            if method == "dlt":
+                dX[i] = M.triangulate_dlt(tr.observations, poses, cams, min_angle=min_angle)
+            else:
+                dX[i] = M.triangulate_midpoint(tr.observations, poses, cams)
+        except Exception as e:  # noqa: BLE001
+            dstat[i] = codes.get(type(e).__name__, 9)
+    np.savez_compressed(os.path.join(HERE, f"tri_{name}.npz"), cam_q=q, cam_t=t,
+                        frame_model=np.zeros(len(frames), np.int32),
+                        models=np.array([[0, 500.0, 500.0, 320.0, 240.0, 0.0, 0.0]]),
+                        track_ptr=ptr, obs_frame=of, obs_uv=uv, threshold_px=thr,
+                        min_angle=min_angle, method=method, ref_X=X, ref_mask=mask,
+                        ref_status=status, ref_direct_X=dX, ref_direct_status=dstat)
+    print(f"tri_{name}: T={len(tracks)} ok={int((status == 0).sum())} "
+          f"direct_errors={int((dstat != 0).sum())}")
+
+
+def tri_fixtures():
+    for method in ("dlt", "midpoint"):
+        rng = np.random.default_rng(21)
+        pts, poses = scene(rng, 8, 120, spacing=0.6)
+        tracks = []
+        for i, p in enumerate(pts):
+            obs = observations(p, poses, 0.4, rng)
+            if len(obs) < 2:
+                continue
+            if i % 4 == 0 and len(obs) >= 3:
+                k = int(rng.integers(len(obs)))
+                obs[k] = M.Observation(obs[k].frame_id, 0,
+                                       obs[k].pixel + rng.uniform(15, 60, 2) * rng.choice([-1, 1], 2))
+            if i % 9 == 0:
+                obs = [M.Observation(o.frame_id, 0, o.pixel + rng.uniform(-80, 80, 2)) for o in obs]
+            tracks.append(M.Track(obs))
+        # degenerate: zero baseline (InsufficientParallax / ParallelRays)
+        dp = {0: cam_pose([0, 0, 0]), 1: cam_pose([0, 0, 0], (0.0, 0.05, 0))}
+        for f, pz in dp.items():
+            poses[100 + f] = pz
+        p = np.array([0.5, -0.3, 9.0])
+        tracks.append(M.Track([M.Observation(100 + f, 0, project(CAM, dp[f], p)) for f in dp]))
+        # cheirality: swapped pixels
+        poses[200], poses[201] = cam_pose([0, 0, 0]), cam_pose([1.0, 0, 0])
+        p = np.array([0.3, 0.2, 10.0])
+        pa, pb = project(CAM, poses[200], p), project(CAM, poses[201], p)
+        tracks.append(M.Track([M.Observation(200, 0, pb), M.Observation(201, 0, pa)]))
+        # parallel rays through the principal point
+        tracks.append(M.Track([M.Observation(200, 0, (CAM.cx, CAM.cy)),
+                               M.Observation(201, 0, (CAM.cx, CAM.cy))]))
+        track_fixture(method, tracks, poses, 4.0, np.radians(0.5), method)
+
+
+def gate_fixture():
+    rng = np.random.default_rng(31)
+    pts, poses = scene(rng, 6, 60)
+    smap = map_from_scene(pts, poses, 0.0, rng, fixed_frames=(0,), noise=0.5)
+    for i, lm in enumerate(smap.landmarks):
+        if i % 5 == 0:
+            lm.track.observations[1].pixel = lm.track.observations[1].pixel + np.array([10.0, 0.0])
+        if i % 11 == 0:
+            for o in lm.track.observations[1:]:
+                o.pixel = o.pixel + np.array([25.0, 25.0])
+        if i % 7 == 0:
+            lm.inlier_mask[0] = False
+    frames = sorted(smap.keyframes)
+    fidx = {f: i for i, f in enumerate(frames)}
+    tri = [lm for lm in smap.landmarks if lm.track.status == M.TRIANGULATED]
+    ptr = np.zeros(len(tri) + 1, np.int64)
+    ptr[1:] = np.cumsum([len(lm.track.observations) for lm in tri])
+    of = np.array([fidx[o.frame_id] for lm in tri for o in lm.track.observations], np.int32)
+    uv = np.array([o.pixel for lm in tri for o in lm.track.observations])
+    mask_in = np.concatenate([lm.inlier_mask for lm in tri]).astype(np.uint8)
+    P = np.array([lm.position for lm in tri])
+    q = np.array([smap.keyframes[f].cam_from_world.quat for f in frames])
+    t = np.array([smap.keyframes[f].cam_from_world.t for f in frames])
+    _, removed = M.remove_outliers(smap, 2.0)
+    mask_out = np.concatenate([lm.inlier_mask for lm in tri]).astype(np.uint8)
+    status = np.array([1 if lm.track.status == M.TRIANGULATED else 0 for lm in tri], np.int8)
+    np.savez_compressed(os.path.join(HERE, "gate.npz"), cam_q=q, cam_t=t,
+                        frame_model=np.zeros(len(frames), np.int32),
+                        models=np.array([[0, 500.0, 500.0, 320.0, 240.0, 0.0, 0.0]]),
+                        track_ptr=ptr, obs_frame=of, obs_uv=uv, points=P, mask_in=mask_in,
+                        threshold_px=2.0, ref_mask=mask_out, ref_removed=removed,
+                        ref_triangulated=status)
+    print(f"gate: L={len(tri)} removed={removed} demoted={int((status == 0).sum())}")
+
+
+def iterative_map_fixture():
+    rng = np.random.default_rng(42)
+    pts, poses = scene(rng, 6, 30)
+    kfs = [Keyframe(f, float(f), 0, poses[f]) for f in sorted(poses)]
+    tracks = []
+    for k, p in enumerate(pts):
+        obs = observations(p, poses, 0.3, rng)
+        if len(obs) < 3:
+            continue
+        if k % 5 == 0:
+            obs[1] = M.Observation(obs[1].frame_id, 0, obs[1].pixel + np.array([40.0, 30.0]))
+        tracks.append(M.Track(obs))
+    # perturb the non-anchor initial poses
+    for kf in kfs[1:]:
+        kf.cam_from_world = exp_map(rng.normal(0, 0.003, 6)) @ kf.cam_from_world
+    q0 = np.array([kf.cam_from_world.quat for kf in kfs])
+    t0 = np.array([kf.cam_from_world.t for kf in kfs])
+    ptr = np.zeros(len(tracks) + 1, np.int64)
+    ptr[1:] = np.cumsum([len(t.observations) for t in tracks])
+    of = np.array([o.frame_id for t in tracks for o in t.observations], np.int32)
+    uv = np.array([o.pixel for t in tracks for o in t.observations])
+    smap = M.iterative_map(kfs, tracks, {0: CAM})
+    lm_track = np.array([next(i for i, t in enumerate(tracks) if t is lm.track)
+                         for lm in smap.landmarks], np.int64)
+    rs = smap.round_stats
+    np.savez_compressed(
+        os.path.join(HERE, "iterative_map.npz"), cam_q=q0, cam_t=t0, track_ptr=ptr, obs_frame=of,
+        obs_uv=uv, ref_cam_q=np.array([smap.keyframes[f].cam_from_world.quat for f in sorted(poses)]),
+        ref_cam_t=np.array([smap.keyframes[f].cam_from_world.t for f in sorted(poses)]),
+        ref_lm_track=lm_track, ref_lm_X=np.array([lm.position for lm in smap.landmarks]),
+        ref_lm_mask=np.concatenate([lm.inlier_mask for lm in smap.landmarks]).astype(np.uint8),
+        ref_status=np.array([{"pending": 0, "triangulated": 1, "failed": 2}[t.status] for t in tracks]),
+        ref_round_added=np.array([r["added"] for r in rs]),
+        ref_round_removed=np.array([r["removed"] for r in rs]),
+        ref_round_landmarks=np.array([r["landmarks"] for r in rs]),
+        ref_mean_err=M.mean_reprojection_error(smap))
+    print(f"iterative_map: tracks={len(tracks)} landmarks={len(smap.landmarks)} rounds={len(rs)}")
+
+
+# --- known-answer vectors for the geometry --------------------------------------
+
+def kat_fixture():
+    rng = np.random.default_rng(55)
+    cams = [CAM, CameraModel("pinhole_radial", 420.0, 410.0, 300.0, 230.0, 640, 480, (-0.12, 0.03)),
+            CameraModel("equidistant_fisheye", 300.0, 300.0, 320.0, 240.0, 640, 480)]
+    rows = []
+    for ci, cam in enumerate(cams):
+        for _ in range(60):
+            pose = exp_map(rng.normal(0, [0.3, 0.3, 0.3, 1.0, 1.0, 1.0]))
+            X = rng.uniform([-3, -3, 4], [3, 3, 12])
+            X = pose.inverse().apply(X)  # point in front of the camera
+            pix, Jp, Jx = project_with_pose_jacobian(cam, pose, X)
+            ray = unproject(cam, pix)
+            rows.append(np.concatenate([[ci], pose.quat, pose.t, X, pix, Jp.ravel(), Jx.ravel(), ray]))
+    models = np.array([[0, 500.0, 500.0, 320.0, 240.0, 0.0, 0.0],
+                       [1, 420.0, 410.0, 300.0, 230.0, -0.12, 0.03],
+                       [2, 300.0, 300.0, 320.0, 240.0, 0.0, 0.0]])
+    # pose terms: edge and prior residual/Jacobians (posegraph.py:195-206, mapping.py:359-368)
+    prow = []
+    for _ in range(40):
+        Ta, Tb, Te = (exp_map(rng.normal(0, 0.4, 6)) for _ in range(3))
+        lam = float(rng.uniform(0.1, 5.0))
+        meas = Ta @ Tb.inverse()
+        meas = exp_map(rng.normal(0, 0.05, 6)) @ meas
+        fn = _edge_residual_fn(PoseEdge("sequential", 0, 1, meas, lam * np.eye(6)))
+        r, (Ja, Jb) = fn(Ta, Tb)
+        pfn = M.absolute_prior_residual_fn(Te, lam)
+        Tc = exp_map(rng.normal(0, 0.05, 6)) @ Te
+        rp, (Jpr,) = pfn(Tc)
+        prow.append(np.concatenate([[lam], Ta.quat, Ta.t, Tb.quat, Tb.t, meas.quat, meas.t, r,
+                                    Ja.ravel(), Jb.ravel(), Te.quat, Te.t, Tc.quat, Tc.t, rp,
+                                    Jpr.ravel()]))
+    np.savez_compressed(os.path.join(HERE, "kat_geometry.npz"), models=models, proj=np.array(rows),
+                        pose_terms=np.array(prow))
+    print(f"kat_geometry: {len(rows)} projections, {len(prow)} pose terms")
+
+
+if __name__ == "__main__":
+    which = sys.argv[1:] or ["kat", "tri", "gate", "imap", "ba"]
+    if "kat" in which:
+        kat_fixture()
+    if "tri" in which:
+        tri_fixtures()
+    if "gate" in which:
+        gate_fixture()
+    if "imap" in which:
+        iterative_map_fixture()
+    if "ba" in which:
+        ba_fixtures()
