@@ -1,0 +1,321 @@
+"""Benchmark: LM bundle-adjustment iterations/s on the BAL-Venice-shaped
+synthetic scene (BASELINE.json configs[2]: 1,778 cameras, ~994k points,
+~5.0M observations), fp64, Huber delta=2, lambda_c = lambda_a = 1 (the
+bundle_adjust stage-1 defaults, mapping.py:92-96).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+A step is one full LM iteration (linearisation + every damping trial until
+a step is accepted, solver.py:209-256) on the device-resident problem.
+Multi-GPU (torchrun, one process per GPU): points are sharded by
+observation count, the camera system and scalars are all-reduced with NCCL
+inside libsfm_b200.so; the timed region is the max over ranks.  Prints ONE
+JSON line on rank 0.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+METRIC = "BA LM iterations/s and residual+Jacobian obs/s at 1/2/4/8 B200 vs CPU ref"
+UNIT = "LM iterations/s"
+CPU_SAMPLE_FRAC = 0.10   # oracle runs on all cameras + the first 10% of the points
+
+
+def dist_init(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return rank, world, local
+
+
+def barrier_sync(world):
+    import torch
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+    torch.cuda.synchronize()
+
+
+def max_over_ranks(x, world):
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        self.lines = []
+        if self.proc:
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+                out, _ = self.proc.communicate()
+            self.lines = [ln for ln in out.splitlines() if ln.strip()]
+
+    def summary(self):
+        sm, smax, reasons = [], 0.0, set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for ln in getattr(self, "lines", []):
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax = max(smax, float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": smax or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def build_workload(seed):
+    from paper_2510_15271_b200.scenes import config_scene, scene_arrays
+    sc = config_scene(3, seed=seed)
+    return sc, scene_arrays(sc, lambda_c=1.0, lambda_a=1.0)
+
+
+def cpu_sample_problem(arrays, frac=CPU_SAMPLE_FRAC):
+    from oracle import ba as OB
+    P = int(len(arrays.points) * frac)
+    no = int(np.searchsorted(arrays.obs_point, P))
+    return OB.BAProblem(arrays.cam_q, arrays.cam_t, arrays.frame_model, arrays.frame_fixed,
+                        [(0, 500.0, 500.0, 320.0, 240.0, (0.0, 0.0))], arrays.points[:P],
+                        arrays.obs_frame[:no], arrays.obs_point[:no], arrays.obs_uv[:no],
+                        arrays.edge_ab, arrays.prior_frame, arrays.edge_weight,
+                        arrays.prior_weight), P, no
+
+
+def time_oracle_iterations(arrays, n_iters, threads):
+    """LM iterations of the CPU oracle (numpy restatement of sfmkit) on the
+    bounded sample; returns seconds per iteration."""
+    from threadpoolctl import threadpool_limits
+    prob, P, no = cpu_sample_problem(arrays)
+    with threadpool_limits(limits=threads):
+        t0 = time.perf_counter()
+        prob.solve(1, 2.0, n_iters)
+        dt = time.perf_counter() - t0
+    return dt / n_iters, P, no
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the reference algorithm's CPU implementation (the
+    oracle port; the reference is pure Python and has no compiled path) on
+    the host cores, rank 0 only."""
+    if rank != 0:
+        return
+    sc, arrays = build_workload(args.seed)
+    cores = os.cpu_count() or 1
+    from threadpoolctl import threadpool_limits
+    prob, P, no = cpu_sample_problem(arrays)
+    with threadpool_limits(limits=cores):
+        for _ in range(args.warmup):
+            prob.solve(1, 2.0, 1)
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            prob.solve(1, 2.0, 1)
+        dt = time.perf_counter() - t0
+    value = args.steps / dt
+    sample = (f"1 LM iteration (linearise + damping trials) of the oracle port on all "
+              f"{sc.n_frames} cameras + the first {P} points / {no} observations "
+              f"({int(CPU_SAMPLE_FRAC * 100)}% of the scene) per step")
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1000.0 * dt / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded generator, no dataset)",
+            "config": workload_config(sc, world),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
+                             "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def workload_config(sc, world):
+    return {"workload": "config 3: synthetic BAL-Venice-shaped BA (ring of cameras around a "
+                        "plaza, random co-visible subsets), 1 LM iteration per step",
+            "cameras": sc.n_frames, "points": sc.n_points, "observations": sc.n_obs,
+            "loss": "huber(2.0)", "lambda_c": 1.0, "lambda_a": 1.0, "seed": sc.seed,
+            "parallelism": f"point-shard x{world}" if world > 1 else "single GPU",
+            "l2": "inputs larger than L2 (observation + pair streams >> 126 MB per iteration)"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    rank, world, local = dist_init(args)
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+
+    import torch
+    from paper_2510_15271_b200 import _native as nat
+    from paper_2510_15271_b200.mapping import DeviceBA, solve_arrays
+    from paper_2510_15271_b200.solver import DeviceOptions, RobustLoss, SolverOptions
+
+    torch.cuda.set_device(local)
+    sc, arrays = build_workload(args.seed)
+    nccl_id = None
+    if world > 1:
+        import torch.distributed as dist
+        obj = [nat.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nccl_id = obj[0]
+    ctx = nat.Context(device=local, rank=rank, world=world, nccl_id=nccl_id)
+    part = arrays.shard(rank, world) if world > 1 else arrays
+    loss = RobustLoss("huber", 2.0)
+    total = args.warmup + args.steps
+    sopt = SolverOptions(max_iters=total + 1000)
+    dopt = DeviceOptions(linear_solver="pcg", pcg_rtol=1e-10, pcg_max_iters=500)
+
+    # ---- device-resident LM iterations (value) -------------------------------
+    ba = DeviceBA(part, loss, sopt, dopt, ctx)
+    rep = ba.iterate(args.warmup)
+    ctx.set_profiling(True)
+    ctx.reset_profile()
+    barrier_sync(world)
+    with ClockSampler(local) as clk:
+        t0 = time.perf_counter()
+        rep1 = ba.iterate(args.steps)
+        barrier_sync(world)
+        wall = time.perf_counter() - t0
+    ctx.set_profiling(False)
+    prof = ctx.profile()
+    iters_done = rep1.iterations - rep.iterations
+    dev_s = max_over_ranks(rep1.device_ms / 1000.0, world)
+    wall = max_over_ranks(wall, world)
+    t_step = max(dev_s, 1e-12)
+    value = iters_done / t_step if iters_done else 0.0
+
+    # residual+Jacobian throughput: linearisation kernels (point side + camera side)
+    lin_ms = sum(prof.get(k, {}).get("ms", 0.0) for k in ("point_lin", "cam_lin_chunks"))
+    lin_launch = prof.get("point_lin", {}).get("launches", 0)
+    n_obs_local = len(part.obs_frame)
+    obs_per_s_local = n_obs_local * lin_launch / (lin_ms / 1000.0) if lin_ms > 0 else 0.0
+
+    # roofline: the dominant kernel by time
+    top = max(prof.items(), key=lambda kv: kv[1]["ms"]) if prof else ("none", {"ms": 0, "launches": 1, "bytes": 0})
+    name, ent = top
+    avg_ms = ent["ms"] / max(ent["launches"], 1)
+    bytes_per_launch = ent["bytes"] / max(ent["launches"], 1)
+    peaks = json.load(open(os.path.join(REPO, "MEASURED_PEAKS.json"))) \
+        if os.path.exists(os.path.join(REPO, "MEASURED_PEAKS.json")) else {"hbm_gbs": 6650.0}
+    peak = float(peaks.get("hbm_gbs", 6650.0))
+    achieved = bytes_per_launch / (avg_ms / 1000.0) / 1e9 if avg_ms > 0 else 0.0
+
+    # ---- end-to-end through the C-ABI with host buffers (e2e) -----------------
+    e2e = None
+    if not args.no_e2e:
+        barrier_sync(world)
+        t0 = time.perf_counter()
+        q, t, X, rep_e, raw_e = solve_arrays(part, loss, SolverOptions(max_iters=args.steps),
+                                             dopt, ctx)
+        barrier_sync(world)
+        e2e_s = max_over_ranks(time.perf_counter() - t0, world)
+        h2d = sum(a.nbytes for a in (part.cam_q, part.cam_t, part.frame_model, part.frame_fixed,
+                                     part.points, part.obs_frame, part.obs_point, part.obs_uv,
+                                     part.edge_ab, part.prior_frame))
+        d2h = q.nbytes + t.nbytes + X.nbytes
+        e2e = {"value": rep_e.iterations / e2e_s, "unit": UNIT,
+               "h2d_bytes_per_step": int(h2d / max(rep_e.iterations, 1)),
+               "d2h_bytes_per_step": int(d2h / max(rep_e.iterations, 1)),
+               "iterations": rep_e.iterations, "seconds": e2e_s,
+               "note": "sfm_ba_solve from host arrays: H2D + structure build + initial cost + "
+                       "LM iterations + D2H, per call amortised over its iterations"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        sec, P, no = time_oracle_iterations(arrays, 1, threads=1)
+        cpu = {"value": 1.0 / sec, "unit": UNIT, "cores": 1, "kind": "port",
+               "sample": f"1 LM iteration of the numpy oracle (restatement of sfmkit's solve, "
+                         f"pinned to its golden vectors) on all {sc.n_frames} cameras + first "
+                         f"{P} points / {no} observations ({int(CPU_SAMPLE_FRAC * 100)}% sample), "
+                         f"{sec:.1f} s; sfmkit itself is DNF at this size (SURVEY §6)"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1000.0 * t_step / max(iters_done, 1),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded generator, no dataset)",
+            "config": workload_config(sc, world),
+            "iterations_timed": iters_done, "trials_timed": rep1.n_trials - rep.n_trials,
+            "pcg_iterations_timed": rep1.pcg_iterations - rep.pcg_iterations,
+            "wall_s": wall, "device_s": dev_s,
+            "linearize_obs_per_s": obs_per_s_local * world,
+            "cost": {"initial": rep1.initial_cost, "final": rep1.final_cost,
+                     "termination": nat.TERMINATIONS[rep1.termination]},
+            "n_blocks_S": int(rep1.n_blocks_S),
+            "roofline": {"kernel": name, "bound": "hbm", "achieved": achieved, "peak": peak,
+                         "unit": "GB/s", "frac": achieved / peak if peak else None,
+                         "traffic": None, "avg_ms": avg_ms, "bytes_per_launch": bytes_per_launch,
+                         "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)"},
+            "kernels": {k: {"launches": v["launches"], "ms": round(v["ms"], 4),
+                            "GBps": (v["bytes"] / (v["ms"] / 1000.0) / 1e9) if v["ms"] > 0 and v["bytes"] else None}
+                        for k, v in sorted(prof.items(), key=lambda kv: -kv[1]["ms"])},
+            "gpu_launches": int(rep1.kernel_launches),
+            "clocks": clk.summary(),
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

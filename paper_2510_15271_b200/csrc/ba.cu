@@ -1726,7 +1726,8 @@ void BASolver::linearize() {
     ca.pairs = pairs_.get(); ca.op = obs_point_.get(); ca.of = obs_frame_.get(); ca.uv = obs_uv_.get();
     ca.frame_model = frame_model_.get(); ca.models = models_.get(); ca.Rt = Rt_[cur_].get();
     ca.X = X_[cur_].get(); ca.lk = opt_.loss_kind; ca.lp = opt_.loss_param; ca.out = chunk_buf_.get();
-    ProfScope ps(*prof_, "cam_lin_chunks", 32.0 * N_, s);
+    // compulsory: diagonal pairs (8 B) + observation records (24 B) + points
+    ProfScope ps(*prof_, "cam_lin_chunks", 32.0 * N_ + 24.0 * P_ + (double)n_diag_chunks_ * kPart * 8.0, s);
     k_chunks<0><<<grid_for(n_diag_chunks_, kBlock), kBlock, 0, s>>>(ca);
   }
   if (nfree_) {
@@ -1771,7 +1772,10 @@ void BASolver::build_schur(double lam) {
     ca.frame_model = frame_model_.get(); ca.models = models_.get(); ca.Rt = Rt_[cur_].get();
     ca.X = X_[cur_].get(); ca.Vinv = Vinv_.get(); ca.e = e_.get(); ca.lk = opt_.loss_kind; ca.lp = opt_.loss_param;
     ca.out = chunk_buf_.get();
-    ProfScope ps(*prof_, "schur_chunks", 8.0 * n_pairs_ + (double)n_chunks_ * kPart * 8.0, s);
+    // compulsory: pair list + observation records + point state (X, V*^-1, e)
+    // + chunk partials written
+    ProfScope ps(*prof_, "schur_chunks",
+                 8.0 * n_pairs_ + 24.0 * N_ + (24.0 + 72.0) * P_ + (double)n_chunks_ * kPart * 8.0, s);
     k_chunks<1><<<grid_for(n_chunks_, kBlock), kBlock, 0, s>>>(ca);
   }
   if (n_ub_) {
@@ -1859,6 +1863,8 @@ bool BASolver::trial(double lam, double* new_cost, double* step_norm) {
   }
   read_scalars();
   pcg_total_ += h_sc_.pcg_iters;
+  if (!use_dense_ && nfree_)  // S read + 7 length-6nf vectors touched per PCG iteration
+    prof_->add_bytes("pcg", (double)h_sc_.pcg_iters * (288.0 * n_full_ + 7.0 * 48.0 * nfree_));
   if (h_sc_.nonfinite) return false;
   if (h_sc_.depth_obs != ~0ull) raise_projection_error(true);
   *new_cost = h_sc_.cost;

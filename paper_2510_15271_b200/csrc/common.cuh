@@ -144,6 +144,11 @@ struct Profiler {
     flush();
     entries.clear();
   }
+  // Adds algorithmic bytes known only after a launch (e.g. PCG iterations).
+  void add_bytes(const char* name, double bytes) {
+    if (!enabled) return;
+    entries[index(name)].bytes += bytes;
+  }
 };
 
 // RAII launch bracket: `PROF(prof, "name", bytes, stream) kernel<<<...>>>(...);`

@@ -557,3 +557,33 @@ __all__ = [
     "ransac_triangulate_batch", "remove_outliers", "iterative_map", "mean_reprojection_error",
     "CameraModel", "Keyframe",
 ]
+
+
+class DeviceBA:
+    """Stepwise, device-resident form of solve_arrays (sfm_ba_setup /
+    sfm_ba_iterate / sfm_ba_download): the problem is uploaded and its
+    structure built once, then LM iterations run with no host<->device
+    traffic beyond one small scalar read-back per trial."""
+
+    def __init__(self, arrays: BAArrays, loss: RobustLoss = TRIVIAL_LOSS,
+                 options: SolverOptions = None, device: DeviceOptions = None, ctx=None):
+        self.ctx = ctx or nat.default_context()
+        self.arrays = arrays
+        self._prob = arrays.struct()
+        self._opt = _options(loss, options or SolverOptions(), device or DEFAULT_DEVICE_OPTIONS)
+        self.ctx.check(self.ctx.lib.sfm_ba_setup(self.ctx.handle, ctypes.byref(self._prob),
+                                                 ctypes.byref(self._opt)))
+
+    def iterate(self, n: int) -> nat.BAReportC:
+        rep = nat.BAReportC()
+        self.ctx.check(self.ctx.lib.sfm_ba_iterate(self.ctx.handle, int(n), ctypes.byref(rep)))
+        return rep
+
+    def download(self):
+        a = self.arrays
+        q = np.empty_like(a.cam_q)
+        t = np.empty_like(a.cam_t)
+        X = np.empty_like(a.points)
+        self.ctx.check(self.ctx.lib.sfm_ba_download(self.ctx.handle, nat.ptr(q), nat.ptr(t),
+                                                    nat.ptr(X)))
+        return q, t, X
