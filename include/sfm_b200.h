@@ -131,7 +131,8 @@ typedef struct {
   int32_t pcg_max_iters;
   double pcg_rtol;            /* relative residual tolerance of PCG       */
   int32_t dense_max_dim;      /* AUTO: dense Cholesky when 6*free <= this */
-  int32_t _pad;
+  int32_t coarse_cluster;     /* PCG coarse level: frames per cluster (0 =
+                                 default 16, < 0 = block-Jacobi only)      */
 } sfm_ba_options;
 
 /* SolverReport (solver.py:90-95) + device-side statistics. */

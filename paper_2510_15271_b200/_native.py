@@ -81,7 +81,7 @@ class BAOptionsC(ctypes.Structure):
                 ("param_tol", ctypes.c_double), ("initial_lambda", ctypes.c_double),
                 ("max_lambda", ctypes.c_double), ("linear_solver", ctypes.c_int32),
                 ("pcg_max_iters", ctypes.c_int32), ("pcg_rtol", ctypes.c_double),
-                ("dense_max_dim", ctypes.c_int32), ("_pad", ctypes.c_int32)]
+                ("dense_max_dim", ctypes.c_int32), ("coarse_cluster", ctypes.c_int32)]
 
 
 class BAReportC(ctypes.Structure):

@@ -13,9 +13,9 @@
 //     per-point quantity (V_i, g_i, V*_i^-1, delta_p, trial cost) is a
 //     thread-per-point loop over the point's contiguous observations;
 //   * every camera-indexed sum (U_j, g_c, S blocks, b_S) is a fixed-order
-//     segmented reduction over a pair list sorted by S block then point,
-//     split into <=kChunk-pair chunks: no floating-point atomics anywhere,
-//     so results are bit-reproducible run to run;
+//     reduction over a pair list sorted by S block then point, one warp per
+//     block: no floating-point atomics anywhere, so results are
+//     bit-reproducible run to run;
 //   * Jacobians are recomputed from the 24-byte observation record instead
 //     of being stored (HBM traffic is the bound, fp64 FMAs are cheap);
 //   * the reduced camera system is solved by a single-CTA dense Cholesky when
@@ -28,16 +28,55 @@
 #include <cstdio>
 
 #include "ba.cuh"
+#include "pcg.cuh"
 #include "sfm_math.cuh"
 
 namespace cg = cooperative_groups;
 
 namespace sfm {
 
+// Arguments of the per-S-block kernels (k_blocks).
+struct BlkArgs {
+  int n;                       // warps of work
+  const int* work;             // MODE 1: upper-block ids, heaviest first
+  int nf;
+  int rank;
+  double lam;
+  const unsigned long long* ub_key;
+  const int* ub_pb;
+  const int* ub_edge;
+  const int* pos_up;
+  const int* pos_lo;
+  const int* diag_ub;
+  const int64_t* pb_pair_ptr;
+  const unsigned long long* pairs;
+  const int* op;
+  const int* of;
+  const double* uv;
+  const int* free_frame;
+  const int* frame_model;
+  const sfm_camera_model* models;
+  const double* Rt;
+  const double4* geo;
+  const double* pv;            // [P*12] packed V*^-1 (6) | e (3) | pad
+  const int* pair_pt;          // [n_pairs] point of each pair
+  const int64_t* cm_ptr;       // [nf+1] camera-major observation ranges
+  const int* cm_pt;            // camera-major point ids
+  const double* cm_uv;         // camera-major pixels
+  const double4* geo_cm;       // camera-major linearisation records
+  const int* diag_pos;         // [nf] BSR slot of the diagonal blocks
+  const double* U;
+  const double* Dc;
+  const double* gc;
+  const double* edge_H;
+  double* S;
+  double* b;
+  double* Uout;
+  double* gout;
+};
+
 namespace {
 
-constexpr int kChunk = 16;        // pairs per chunk (one thread each)
-constexpr int kPart = 42;         // 36 (6x6 block) + 6 (b / g) per chunk
 constexpr int kDenseMax = 210;    // packed lower triangle of 6*nf fits in smem
 constexpr int kBlock = 128;
 
@@ -65,25 +104,40 @@ __device__ __forceinline__ Pose load_pose(const double* q, const double* t, cons
   return p;
 }
 
-// Projection + weighted Jacobians of one observation (cameras.py:169-179,
-// solver.py:170-178).  Returns PROJ_* code.
-__device__ __forceinline__ int obs_linearize(const sfm_camera_model& cm, const Mat3& R, Vec3 t,
-                                             Vec3 X, double uo, double vo, int lk, double lp,
-                                             double Jc[12], double Jp[6], double r[2]) {
-  double u, v;
-  int st = project_with_jacobians(cm, R, t, X, u, v, Jc, Jp);
-  if (st != PROJ_OK) return st;
-  r[0] = u - uo;
-  r[1] = v - vo;
-  double s = r[0] * r[0] + r[1] * r[1];
-  double w = sqrt(loss_rho_prime(lk, lp, s));
-  r[0] *= w;
-  r[1] *= w;
+// Per-observation linearisation record g = (x, y, 1/Z, w) with (x, y) the
+// normalised image point and w = sqrt(rho'(s)), written once per
+// linearisation by k_point_lin.  Every later evaluation of the weighted
+// Jacobians at that linearisation point rebuilds them from g and the camera
+// (cameras.py:137-148, :169-179 regrouped): no projection, no division,
+// no sqrt -- and only 32 bytes per observation instead of uv + point.
+//   J~c = w [A N, (1/Z) A [[1,0,-x],[0,1,-y]]],  J~p = (right half) R
+//   N = [[-xy, 1+x^2, -y], [-(1+y^2), xy, x]],   A = diag(fx,fy) J_dist(x,y)
+__device__ __forceinline__ void geo_jacobians(const sfm_camera_model& cm, const Mat3& R, const double4 g,
+                                              double Jc[12], double Jp[6]) {
+  const double x = g.x, y = g.y, iz = g.z, w = g.w;
+  double A00, A01, A10, A11;
+  if (cm.kind == SFM_CAM_PINHOLE) {
+    A00 = cm.fx * w; A01 = 0.0; A10 = 0.0; A11 = cm.fy * w;
+  } else {
+    double Jd[4];
+    distort_jacobian(cm, x, y, Jd);
+    A00 = cm.fx * Jd[0] * w; A01 = cm.fx * Jd[1] * w;
+    A10 = cm.fy * Jd[2] * w; A11 = cm.fy * Jd[3] * w;
+  }
+  const double xy = x * y;
+  const double n00 = -xy, n01 = 1.0 + x * x, n02 = -y;
+  const double n10 = -(1.0 + y * y), n11 = xy, n12 = x;
+  Jc[0] = A00 * n00 + A01 * n10; Jc[1] = A00 * n01 + A01 * n11; Jc[2] = A00 * n02 + A01 * n12;
+  Jc[6] = A10 * n00 + A11 * n10; Jc[7] = A10 * n01 + A11 * n11; Jc[8] = A10 * n02 + A11 * n12;
+  const double K00 = iz * A00, K01 = iz * A01, K02 = -(K00 * x + K01 * y);
+  const double K10 = iz * A10, K11 = iz * A11, K12 = -(K10 * x + K11 * y);
+  Jc[3] = K00; Jc[4] = K01; Jc[5] = K02;
+  Jc[9] = K10; Jc[10] = K11; Jc[11] = K12;
 #pragma unroll
-  for (int i = 0; i < 12; ++i) Jc[i] *= w;
-#pragma unroll
-  for (int i = 0; i < 6; ++i) Jp[i] *= w;
-  return PROJ_OK;
+  for (int j = 0; j < 3; ++j) {
+    Jp[j] = K00 * R.m[j] + K01 * R.m[3 + j] + K02 * R.m[6 + j];
+    Jp[3 + j] = K10 * R.m[j] + K11 * R.m[3 + j] + K12 * R.m[6 + j];
+  }
 }
 
 // Deterministic block sum (fixed shuffle tree + fixed smem order).
@@ -190,33 +244,6 @@ __global__ void k_div_ceil(int n, const int* __restrict__ cnt, int64_t* __restri
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i > n) return;
   out[i] = (i == n) ? 0 : (cnt[i] + d - 1) / d;
-}
-
-__global__ void k_chunk_gen(int n_pb, const int64_t* __restrict__ pb_pair_ptr,
-                            const int64_t* __restrict__ pb_chunk_ptr, int64_t n_pairs,
-                            int64_t* __restrict__ chunk_start, int* __restrict__ chunk_pb) {
-  int pb = blockIdx.x * blockDim.x + threadIdx.x;
-  if (pb >= n_pb) return;
-  int64_t c0 = pb_chunk_ptr[pb], c1 = pb_chunk_ptr[pb + 1];
-  int64_t s = pb_pair_ptr[pb];
-  for (int64_t c = c0; c < c1; ++c) {
-    chunk_start[c] = s + (c - c0) * kChunk;
-    chunk_pb[c] = pb;
-  }
-  if (pb == n_pb - 1) chunk_start[c1] = n_pairs;
-}
-
-__global__ void k_diag_flags(int64_t n_chunks, int nf, const int* __restrict__ chunk_pb,
-                             const unsigned long long* __restrict__ pb_key, char* __restrict__ flag) {
-  int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= n_chunks) return;
-  unsigned long long k = pb_key[chunk_pb[c]];
-  flag[c] = (k / nf) == (k % nf);
-}
-
-__global__ void k_iota64(int64_t n, int64_t* __restrict__ out) {
-  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) out[i] = i;
 }
 
 __device__ __forceinline__ int64_t lower_bound_u64(const unsigned long long* a, int64_t n,
@@ -366,9 +393,11 @@ struct PointArgs {
   const double* X;        // linearization state points
   const double* Rt_eval;  // state whose cost is evaluated
   double* X_out;          // trial points (TRIAL) or unused
-  const double* Vinv;
-  const double* e;
+  const double* pv;       // packed V*^-1 | e per point
   const double* dc;
+  const double4* geo;     // linearisation records (TRIAL) / output (LIN)
+  const int* cm_pos;      // camera-major slot of each observation (-1: fixed)
+  double4* geo_cm;        // camera-major copy of the records (LIN)
   int64_t obs_offset;
   double* part_cost;
   double* part_dp2;
@@ -397,12 +426,8 @@ __global__ void __launch_bounds__(kBlock) k_point_cost(PointArgs a) {
         Mat3 R; Vec3 t;
         load_cam(a.Rt, f, R, t);
         const sfm_camera_model cm = a.models[a.frame_model[f]];
-        double Jc[12], Jp[6], r[2];
-        const double2 uv = reinterpret_cast<const double2*>(a.uv)[o];
-        if (obs_linearize(cm, R, t, X, uv.x, uv.y, a.lk, a.lp, Jc, Jp, r) != PROJ_OK) {
-          nonfinite = true;
-          continue;
-        }
+        double Jc[12], Jp[6];
+        geo_jacobians(cm, R, a.geo[o], Jc, Jp);
         const double* d = a.dc + (int64_t)j * 6;
         double y0 = 0.0, y1 = 0.0;
 #pragma unroll
@@ -411,8 +436,8 @@ __global__ void __launch_bounds__(kBlock) k_point_cost(PointArgs a) {
         acc1 += Jp[1] * y0 + Jp[4] * y1;
         acc2 += Jp[2] * y0 + Jp[5] * y1;
       }
-      const double* Vi = a.Vinv + p * 6;  // xx xy xz yy yz zz
-      const double* ei = a.e + p * 3;
+      const double* Vi = a.pv + p * 12;  // xx xy xz yy yz zz | e
+      const double* ei = Vi + 6;
       double d0 = -ei[0] - (Vi[0] * acc0 + Vi[1] * acc1 + Vi[2] * acc2);
       double d1 = -ei[1] - (Vi[1] * acc0 + Vi[3] * acc1 + Vi[4] * acc2);
       double d2 = -ei[2] - (Vi[2] * acc0 + Vi[4] * acc1 + Vi[5] * acc2);
@@ -529,8 +554,20 @@ __global__ void __launch_bounds__(kBlock) k_point_lin(PointArgs a, double* __res
       load_cam(a.Rt, f, R, t);
       const sfm_camera_model cm = a.models[a.frame_model[f]];
       const double2 uv = reinterpret_cast<const double2*>(a.uv)[o];
-      double Jc[12], Jp[6], r[2];
-      if (obs_linearize(cm, R, t, X, uv.x, uv.y, a.lk, a.lp, Jc, Jp, r) != PROJ_OK) { bad = true; continue; }
+      const Vec3 pc = add(mul(R, X), t);
+      double u, vv;
+      if (project_point(cm, pc, u, vv) != PROJ_OK) { bad = true; continue; }
+      double r[2] = {u - uv.x, vv - uv.y};
+      const double w = sqrt(loss_rho_prime(a.lk, a.lp, r[0] * r[0] + r[1] * r[1]));
+      r[0] *= w;
+      r[1] *= w;
+      const double iz = 1.0 / pc.z;
+      const double4 rec = make_double4(pc.x * iz, pc.y * iz, iz, w);
+      const_cast<double4*>(a.geo)[o] = rec;
+      const int cp = a.cm_pos[o];
+      if (cp >= 0) a.geo_cm[cp] = rec;
+      double Jc[12], Jp[6];
+      geo_jacobians(cm, R, rec, Jc, Jp);
       v[0] += Jp[0] * Jp[0] + Jp[3] * Jp[3];
       v[1] += Jp[0] * Jp[1] + Jp[3] * Jp[4];
       v[2] += Jp[0] * Jp[2] + Jp[3] * Jp[5];
@@ -553,130 +590,239 @@ __global__ void __launch_bounds__(kBlock) k_point_lin(PointArgs a, double* __res
   if ((threadIdx.x & 31) == 0) atomicMax(&a.sc->gmax, m);
 }
 
-struct ChunkArgs {
-  int64_t n;               // chunks to process
-  const int64_t* ids;      // chunk ids (LIN) or nullptr (all)
-  const int64_t* start;
-  const unsigned long long* pairs;
-  const int* op;
-  const int* of;
-  const double* uv;
-  const int* frame_model;
-  const sfm_camera_model* models;
-  const double* Rt;
-  const double* X;
-  const double* Vinv;
-  const double* e;
-  int lk;
-  double lp;
-  double* out;             // [chunk*42]
-};
+constexpr int kBlkWarps = 4;
 
-// MODE 0 (linearize, diagonal chunks): sum Jc^T Jc (36) and Jc^T r (6).
-// MODE 1 (Schur): for each pair (obs a in camera lo, obs b in camera hi) of
-// the same point: -Jc_a^T (Jp_a V*^-1 Jp_b^T) Jc_b; diagonal chunks also add
-// Jc_a^T Jp_a e_i to b_S.  One thread per chunk, fixed pair order.
-template <int MODE>
-__global__ void __launch_bounds__(kBlock) k_chunks(ChunkArgs a) {
-  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx >= a.n) return;
-  const int64_t cid = a.ids ? a.ids[idx] : idx;
-  const int64_t k0 = a.start[cid], k1 = a.start[cid + 1];
-  double acc[36], accb[6];
+// One warp per off-diagonal S block (lo < hi), blocks in row-major order so
+// consecutive warps share cameras and points (L2 reuse).  The block's pairs
+// (observation a in camera lo, b in camera hi of the same point, sorted by
+// point) are taken 32 at a time, one per lane; each lane writes
+// -J~c_a^T (J~p_a V*^-1 J~p_b^T) J~c_b to a shared-memory row and lane l sums
+// column l over the rows -- fixed order, no partial buffers in HBM.  The
+// lambda_c edge block is added on rank 0 and both BSR triangles written.
+__global__ void __launch_bounds__(kBlkWarps * 32) k_offdiag_blocks(BlkArgs a) {
+  __shared__ double Tsm[kBlkWarps][32][37];
+  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (w >= a.n) return;
+  const int u = a.work[w];
+  const unsigned long long key = a.ub_key[u];
+  const int lo = (int)(key / a.nf), hi = (int)(key % a.nf);
+  const int pb = a.ub_pb[u];
+  double acc0 = 0.0, acc1 = 0.0;
+  if (pb >= 0) {
+    const int fa = a.free_frame[lo], fb = a.free_frame[hi];
+    Mat3 Ra, Rb; Vec3 ta, tb;
+    load_cam(a.Rt, fa, Ra, ta);
+    load_cam(a.Rt, fb, Rb, tb);
+    const sfm_camera_model ca = a.models[a.frame_model[fa]];
+    const sfm_camera_model cb = a.models[a.frame_model[fb]];
+    const int64_t k0 = a.pb_pair_ptr[pb], k1 = a.pb_pair_ptr[pb + 1];
+    double* row = &Tsm[warp][lane][0];
+    for (int64_t kb = k0; kb < k1; kb += 32) {
+      const int64_t k = kb + lane;
+      const int nv = (int)min((int64_t)32, k1 - kb);
+      if (k < k1) {
+        const unsigned long long pr = a.pairs[k];
+        const int64_t oa = (int64_t)(pr >> 32), ob = (int64_t)(uint32_t)pr;
+        const double* pv = a.pv + (int64_t)a.pair_pt[k] * 12;
+        double Jca[12], Jpa[6], Jcb[12], Jpb[6];
+        geo_jacobians(ca, Ra, a.geo[oa], Jca, Jpa);
+        geo_jacobians(cb, Rb, a.geo[ob], Jcb, Jpb);
+        const double v0 = pv[0], v1 = pv[1], v2 = pv[2], v3_ = pv[3], v4 = pv[4], v5 = pv[5];
+        const double P00 = v0 * Jpb[0] + v1 * Jpb[1] + v2 * Jpb[2];
+        const double P01 = v1 * Jpb[0] + v3_ * Jpb[1] + v4 * Jpb[2];
+        const double P02 = v2 * Jpb[0] + v4 * Jpb[1] + v5 * Jpb[2];
+        const double P10 = v0 * Jpb[3] + v1 * Jpb[4] + v2 * Jpb[5];
+        const double P11 = v1 * Jpb[3] + v3_ * Jpb[4] + v4 * Jpb[5];
+        const double P12 = v2 * Jpb[3] + v4 * Jpb[4] + v5 * Jpb[5];
+        const double m00 = Jpa[0] * P00 + Jpa[1] * P01 + Jpa[2] * P02;
+        const double m01 = Jpa[0] * P10 + Jpa[1] * P11 + Jpa[2] * P12;
+        const double m10 = Jpa[3] * P00 + Jpa[4] * P01 + Jpa[5] * P02;
+        const double m11 = Jpa[3] * P10 + Jpa[4] * P11 + Jpa[5] * P12;
+        double MJ[12];
 #pragma unroll
-  for (int i = 0; i < 36; ++i) acc[i] = 0.0;
+        for (int c = 0; c < 6; ++c) {
+          MJ[c] = m00 * Jcb[c] + m01 * Jcb[6 + c];
+          MJ[6 + c] = m10 * Jcb[c] + m11 * Jcb[6 + c];
+        }
 #pragma unroll
-  for (int i = 0; i < 6; ++i) accb[i] = 0.0;
-
-  unsigned long long pr0 = a.pairs[k0];
-  const int fa = a.of[(int64_t)(pr0 >> 32)];
-  const int fb = a.of[(int64_t)(uint32_t)pr0];
-  Mat3 Ra, Rb; Vec3 ta, tb;
-  load_cam(a.Rt, fa, Ra, ta);
-  load_cam(a.Rt, fb, Rb, tb);
-  const sfm_camera_model ca = a.models[a.frame_model[fa]];
-  const sfm_camera_model cb = a.models[a.frame_model[fb]];
-
-  for (int64_t k = k0; k < k1; ++k) {
-    const unsigned long long pr = a.pairs[k];
-    const int64_t oa = (int64_t)(pr >> 32), ob = (int64_t)(uint32_t)pr;
-    const int64_t i = a.op[oa];
-    const Vec3 X = load_X(a.X, i);
-    const double2 uva = reinterpret_cast<const double2*>(a.uv)[oa];
-    double Jca[12], Jpa[6], ra[2];
-    obs_linearize(ca, Ra, ta, X, uva.x, uva.y, a.lk, a.lp, Jca, Jpa, ra);
-    if (MODE == 0) {
+        for (int r = 0; r < 6; ++r)
 #pragma unroll
-      for (int r = 0; r < 6; ++r) {
-#pragma unroll
-        for (int c = 0; c < 6; ++c) acc[r * 6 + c] += Jca[r] * Jca[c] + Jca[6 + r] * Jca[6 + c];
-        accb[r] += Jca[r] * ra[0] + Jca[6 + r] * ra[1];
+          for (int c = 0; c < 6; ++c) row[r * 6 + c] = -(Jca[r] * MJ[c] + Jca[6 + r] * MJ[6 + c]);
       }
-    } else {
-      const double* Vi = a.Vinv + i * 6;
-      const double v0 = Vi[0], v1 = Vi[1], v2 = Vi[2], v3_ = Vi[3], v4 = Vi[4], v5 = Vi[5];
-      double MJ[12];
-      double Jpb[6];
-      if (ob == oa) {
-#pragma unroll
-        for (int m = 0; m < 6; ++m) Jpb[m] = Jpa[m];
+      __syncwarp();
+      for (int l = 0; l < nv; ++l) {
+        acc0 += Tsm[warp][l][lane];
+        if (lane < 4) acc1 += Tsm[warp][l][32 + lane];
       }
-      double Jcb[12];
-      if (ob != oa) {
-        const double2 uvb = reinterpret_cast<const double2*>(a.uv)[ob];
-        double rb[2];
-        obs_linearize(cb, Rb, tb, X, uvb.x, uvb.y, a.lk, a.lp, Jcb, Jpb, rb);
-      } else {
-#pragma unroll
-        for (int m = 0; m < 12; ++m) Jcb[m] = Jca[m];
-      }
-      // P = V*^-1 Jp_b^T (3x2)
-      double P0[3], P1[3];
-      P0[0] = v0 * Jpb[0] + v1 * Jpb[1] + v2 * Jpb[2];
-      P0[1] = v1 * Jpb[0] + v3_ * Jpb[1] + v4 * Jpb[2];
-      P0[2] = v2 * Jpb[0] + v4 * Jpb[1] + v5 * Jpb[2];
-      P1[0] = v0 * Jpb[3] + v1 * Jpb[4] + v2 * Jpb[5];
-      P1[1] = v1 * Jpb[3] + v3_ * Jpb[4] + v4 * Jpb[5];
-      P1[2] = v2 * Jpb[3] + v4 * Jpb[4] + v5 * Jpb[5];
-      // M = Jp_a P (2x2)
-      const double m00 = Jpa[0] * P0[0] + Jpa[1] * P0[1] + Jpa[2] * P0[2];
-      const double m01 = Jpa[0] * P1[0] + Jpa[1] * P1[1] + Jpa[2] * P1[2];
-      const double m10 = Jpa[3] * P0[0] + Jpa[4] * P0[1] + Jpa[5] * P0[2];
-      const double m11 = Jpa[3] * P1[0] + Jpa[4] * P1[1] + Jpa[5] * P1[2];
-#pragma unroll
-      for (int c = 0; c < 6; ++c) {
-        MJ[c] = m00 * Jcb[c] + m01 * Jcb[6 + c];
-        MJ[6 + c] = m10 * Jcb[c] + m11 * Jcb[6 + c];
-      }
-#pragma unroll
-      for (int r = 0; r < 6; ++r)
-#pragma unroll
-        for (int c = 0; c < 6; ++c) acc[r * 6 + c] -= Jca[r] * MJ[c] + Jca[6 + r] * MJ[6 + c];
-      if (ob == oa) {
-        const double* ei = a.e + i * 3;
-        const double y0 = Jpa[0] * ei[0] + Jpa[1] * ei[1] + Jpa[2] * ei[2];
-        const double y1 = Jpa[3] * ei[0] + Jpa[4] * ei[1] + Jpa[5] * ei[2];
-#pragma unroll
-        for (int r = 0; r < 6; ++r) accb[r] += Jca[r] * y0 + Jca[6 + r] * y1;
-      }
+      __syncwarp();
     }
   }
-  double* o = a.out + cid * kPart;
-#pragma unroll
-  for (int i = 0; i < 36; ++i) o[i] = acc[i];
-#pragma unroll
-  for (int i = 0; i < 6; ++i) o[36 + i] = accb[i];
+  if (a.rank == 0 && a.ub_edge[u] >= 0) {
+    const double* H = a.edge_H + (int64_t)a.ub_edge[u] * 36;
+    acc0 += H[lane];
+    if (lane < 4) acc1 += H[32 + lane];
+  }
+  double* up = a.S + (int64_t)a.pos_up[u] * 36;
+  up[lane] = acc0;
+  if (lane < 4) up[32 + lane] = acc1;
+  double* dn = a.S + (int64_t)a.pos_lo[u] * 36;
+  dn[(lane % 6) * 6 + lane / 6] = acc0;
+  if (lane < 4) dn[((32 + lane) % 6) * 6 + (32 + lane) / 6] = acc1;
 }
+
+constexpr int kCamWarps = 4;
+
+// One CTA per free camera j over its observations in camera-major order
+// (contiguous linearisation records, point ids and pixels): the diagonal
+// S block and the camera half of the normal equations.  Warps take 32-
+// observation batches round-robin; each lane writes its contribution row to
+// shared memory, lane l sums column l over the rows, then the warp sums
+// are added in warp order -- a fixed order, independent of timing.
+//   MODE 0: U_j = sum J~c^T J~c, g_j = sum J~c^T r~              (linearise)
+//   MODE 1: S_jj = U*_j - sum J~c^T (J~p V*^-1 J~p^T) J~c,
+//           b_j = -g_j + sum J~c^T J~p e_i                        (each trial)
+template <int MODE>
+__global__ void __launch_bounds__(kCamWarps * 32) k_cam_blocks(BlkArgs a) {
+  __shared__ double Tsm[kCamWarps][32][43];
+  __shared__ double Wsum[kCamWarps][42];
+  const int j = blockIdx.x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int f = a.free_frame[j];
+  Mat3 R; Vec3 t;
+  load_cam(a.Rt, f, R, t);
+  const sfm_camera_model cm = a.models[a.frame_model[f]];
+  const int64_t k0 = a.cm_ptr[j], k1 = a.cm_ptr[j + 1];
+  double acc0 = 0.0, acc1 = 0.0;
+  double* row = &Tsm[warp][lane][0];
+  for (int64_t kb = k0 + (int64_t)warp * 32; kb < k1; kb += kCamWarps * 32) {
+    const int64_t k = kb + lane;
+    const int nv = (int)min((int64_t)32, k1 - kb);
+    if (k < k1) {
+      const double4 g = a.geo_cm[k];
+      double Jc[12], Jp[6];
+      geo_jacobians(cm, R, g, Jc, Jp);
+      if (MODE == 0) {
+        const double2 uv = reinterpret_cast<const double2*>(a.cm_uv)[k];
+        double xd, yd;
+        distort(cm, g.x, g.y, xd, yd);
+        const double r0 = g.w * (cm.fx * xd + cm.cx - uv.x);
+        const double r1 = g.w * (cm.fy * yd + cm.cy - uv.y);
+#pragma unroll
+        for (int r = 0; r < 6; ++r) {
+#pragma unroll
+          for (int c = r; c < 6; ++c) {
+            const double v = Jc[r] * Jc[c] + Jc[6 + r] * Jc[6 + c];
+            row[r * 6 + c] = v;
+            row[c * 6 + r] = v;
+          }
+          row[36 + r] = Jc[r] * r0 + Jc[6 + r] * r1;
+        }
+      } else {
+        const double* pv = a.pv + (int64_t)a.cm_pt[k] * 12;
+        const double v0 = pv[0], v1 = pv[1], v2 = pv[2], v3_ = pv[3], v4 = pv[4], v5 = pv[5];
+        const double P00 = v0 * Jp[0] + v1 * Jp[1] + v2 * Jp[2];
+        const double P01 = v1 * Jp[0] + v3_ * Jp[1] + v4 * Jp[2];
+        const double P02 = v2 * Jp[0] + v4 * Jp[1] + v5 * Jp[2];
+        const double P10 = v0 * Jp[3] + v1 * Jp[4] + v2 * Jp[5];
+        const double P11 = v1 * Jp[3] + v3_ * Jp[4] + v4 * Jp[5];
+        const double P12 = v2 * Jp[3] + v4 * Jp[4] + v5 * Jp[5];
+        const double m00 = Jp[0] * P00 + Jp[1] * P01 + Jp[2] * P02;
+        const double m01 = Jp[0] * P10 + Jp[1] * P11 + Jp[2] * P12;
+        const double m11 = Jp[3] * P10 + Jp[4] * P11 + Jp[5] * P12;
+        double MJ[12];
+#pragma unroll
+        for (int c = 0; c < 6; ++c) {
+          MJ[c] = m00 * Jc[c] + m01 * Jc[6 + c];
+          MJ[6 + c] = m01 * Jc[c] + m11 * Jc[6 + c];
+        }
+#pragma unroll
+        for (int r = 0; r < 6; ++r)
+#pragma unroll
+          for (int c = r; c < 6; ++c) {
+            const double v = -(Jc[r] * MJ[c] + Jc[6 + r] * MJ[6 + c]);
+            row[r * 6 + c] = v;
+            row[c * 6 + r] = v;
+          }
+        const double y0 = Jp[0] * pv[6] + Jp[1] * pv[7] + Jp[2] * pv[8];
+        const double y1 = Jp[3] * pv[6] + Jp[4] * pv[7] + Jp[5] * pv[8];
+#pragma unroll
+        for (int r = 0; r < 6; ++r) row[36 + r] = Jc[r] * y0 + Jc[6 + r] * y1;
+      }
+    }
+    __syncwarp();
+    for (int l = 0; l < nv; ++l) {
+      acc0 += Tsm[warp][l][lane];
+      if (lane < 10) acc1 += Tsm[warp][l][32 + lane];
+    }
+    __syncwarp();
+  }
+  Wsum[warp][lane] = acc0;
+  if (lane < 10) Wsum[warp][32 + lane] = acc1;
+  __syncthreads();
+  if (warp != 0) return;
+  double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+  for (int w = 0; w < kCamWarps; ++w) {
+    s0 += Wsum[w][lane];
+    if (lane < 10) s1 += Wsum[w][32 + lane];
+  }
+  if (MODE == 0) {
+    a.Uout[(int64_t)j * 36 + lane] = s0;
+    if (lane < 4) a.Uout[(int64_t)j * 36 + 32 + lane] = s1;
+    else if (lane < 10) a.gout[(int64_t)j * 6 + lane - 4] = s1;
+    return;
+  }
+  if (a.rank == 0) {
+    const double* Uj = a.U + (int64_t)j * 36;
+    s0 += Uj[lane];
+    if (lane % 7 == 0) s0 += a.lam * a.Dc[j * 6 + lane / 7];
+    if (lane < 4) {
+      s1 += Uj[32 + lane];
+      if (lane == 3) s1 += a.lam * a.Dc[j * 6 + 5];
+    } else if (lane < 10) {
+      s1 -= a.gc[j * 6 + lane - 4];
+    }
+  }
+  double* up = a.S + (int64_t)a.diag_pos[j] * 36;
+  up[lane] = s0;
+  if (lane < 4) up[32 + lane] = s1;
+  else if (lane < 10) a.b[j * 6 + lane - 4] = s1;
+}
+
+// Camera-major observation streams (built once per bundle_adjust): the
+// diagonal pair blocks already hold each free camera's observations in point
+// order; copy them out contiguously with their pixels and point ids.
+__global__ void k_cm_build(int nf, const int* __restrict__ diag_ub, const int* __restrict__ ub_pb,
+                           const int64_t* __restrict__ pb_pair_ptr, const unsigned long long* __restrict__ pairs,
+                           const int64_t* __restrict__ cm_ptr, const int* __restrict__ op,
+                           const double* __restrict__ uv, int64_t* __restrict__ cm_obs, int* __restrict__ cm_pt,
+                           double* __restrict__ cm_uv, int* __restrict__ cm_pos) {
+  const int j = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (j >= nf) return;
+  const int pb = ub_pb[diag_ub[j]];
+  if (pb < 0) return;
+  const int64_t p0 = pb_pair_ptr[pb], c0 = cm_ptr[j], n = cm_ptr[j + 1] - c0;
+  for (int64_t q = lane; q < n; q += 32) {
+    const int64_t o = (int64_t)(pairs[p0 + q] >> 32);
+    cm_obs[c0 + q] = o;
+    cm_pt[c0 + q] = op[o];
+    cm_uv[(c0 + q) * 2] = uv[o * 2];
+    cm_uv[(c0 + q) * 2 + 1] = uv[o * 2 + 1];
+    cm_pos[o] = (int)(c0 + q);
+  }
+}
+
+__global__ void k_pair_pt(int64_t n, const unsigned long long* __restrict__ pairs, const int* __restrict__ op,
+                          int* __restrict__ pair_pt) {
+  int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < n) pair_pt[k] = op[(int64_t)(pairs[k] >> 32)];
+}
+
 
 struct CamArgs {
   int nf;
-  int rank;
-  const int* free_frame;
-  const int* diag_ub;
-  const int* ub_pb;
-  const int64_t* pb_chunk_ptr;
-  const double* chunk_buf;
-  // pose terms
   const int* term_ptr;
   const int* term_list;
   const int* ab;
@@ -692,22 +838,12 @@ struct CamArgs {
   double* gc;
 };
 
-// U_j, g_j = reprojection part (sum of diagonal chunk partials in order)
-// + incident pose terms (rank 0 only holds them).
-__global__ void k_cam_lin(CamArgs a) {
+// + the incident pose terms (rank 0 only holds them), in term order.
+__global__ void k_cam_terms(CamArgs a) {
   int j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= a.nf) return;
-  double U[36], g[6];
-  for (int i = 0; i < 36; ++i) U[i] = 0.0;
-  for (int i = 0; i < 6; ++i) g[i] = 0.0;
-  int pb = a.ub_pb[a.diag_ub[j]];
-  if (pb >= 0) {
-    for (int64_t c = a.pb_chunk_ptr[pb]; c < a.pb_chunk_ptr[pb + 1]; ++c) {
-      const double* s = a.chunk_buf + c * kPart;
-      for (int i = 0; i < 36; ++i) U[i] += s[i];
-      for (int i = 0; i < 6; ++i) g[i] += s[36 + i];
-    }
-  }
+  if (j >= a.nf || a.term_ptr[j] == a.term_ptr[j + 1]) return;
+  double* U = a.U + (int64_t)j * 36;
+  double* g = a.gc + (int64_t)j * 6;
   for (int k = a.term_ptr[j]; k < a.term_ptr[j + 1]; ++k) {
     const int code = a.term_list[k];
     const int term = code >> 2, side = code & 3;
@@ -733,8 +869,6 @@ __global__ void k_cam_lin(CamArgs a) {
       g[rr] += s;
     }
   }
-  for (int i = 0; i < 36; ++i) a.U[(int64_t)j * 36 + i] = U[i];
-  for (int i = 0; i < 6; ++i) a.gc[(int64_t)j * 6 + i] = g[i];
 }
 
 __global__ void k_cam_post(int nf, const double* __restrict__ U, const double* __restrict__ gc,
@@ -781,8 +915,7 @@ __global__ void k_edge_lin(int E, const int* __restrict__ ab, const int* __restr
 // V* = V + lam*max(diag V, 1e-12) (solver.py:217-220), V*^-1 (adjugate),
 // e = V*^-1 g_p.
 __global__ void k_point_prep(int64_t P, double lam, const double* __restrict__ V,
-                             const double* __restrict__ gp, double* __restrict__ Vinv,
-                             double* __restrict__ e, BAScalars* sc) {
+                             const double* __restrict__ gp, double* __restrict__ pv, BAScalars* sc) {
   int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= P) return;
   const double* v = V + p * 6;
@@ -795,76 +928,19 @@ __global__ void k_point_prep(int64_t P, double lam, const double* __restrict__ V
   double D = a * f - c * c, Ee = b * c - a * ee, Fm = a * d - b * b;
   double det = a * A + b * B + c * C;
   double inv = 1.0 / det;
-  double* o = Vinv + p * 6;
-  o[0] = A * inv; o[1] = B * inv; o[2] = C * inv; o[3] = D * inv; o[4] = Ee * inv; o[5] = Fm * inv;
+  double* o = pv + p * 12;
+  const double i0 = A * inv, i1 = B * inv, i2 = C * inv, i3 = D * inv, i4 = Ee * inv, i5 = Fm * inv;
   const double* g = gp + p * 3;
-  double e0 = o[0] * g[0] + o[1] * g[1] + o[2] * g[2];
-  double e1 = o[1] * g[0] + o[3] * g[1] + o[4] * g[2];
-  double e2 = o[2] * g[0] + o[4] * g[1] + o[5] * g[2];
-  e[p * 3] = e0; e[p * 3 + 1] = e1; e[p * 3 + 2] = e2;
+  const double e0 = i0 * g[0] + i1 * g[1] + i2 * g[2];
+  const double e1 = i1 * g[0] + i3 * g[1] + i4 * g[2];
+  const double e2 = i2 * g[0] + i4 * g[1] + i5 * g[2];
+  reinterpret_cast<double2*>(o)[0] = make_double2(i0, i1);
+  reinterpret_cast<double2*>(o)[1] = make_double2(i2, i3);
+  reinterpret_cast<double2*>(o)[2] = make_double2(i4, i5);
+  reinterpret_cast<double2*>(o)[3] = make_double2(e0, e1);
+  reinterpret_cast<double2*>(o)[4] = make_double2(e2, 0.0);
   if (!(det > 0.0) || !isfinite(inv) || !isfinite(e0) || !isfinite(e1) || !isfinite(e2))
     atomicOr(&sc->nonfinite, 1);
-}
-
-struct BlockArgs {
-  int n_ub;
-  int nf;
-  int rank;
-  double lam;
-  const unsigned long long* ub_key;
-  const int* ub_pb;
-  const int* ub_edge;
-  const int* pos_up;
-  const int* pos_lo;
-  const int64_t* pb_chunk_ptr;
-  const double* chunk_buf;
-  const double* U;
-  const double* Dc;
-  const double* gc;
-  const double* edge_H;
-  double* S;
-  double* b;
-};
-
-__global__ void k_block_finalize(BlockArgs a) {
-  int u = blockIdx.x * blockDim.x + threadIdx.x;
-  if (u >= a.n_ub) return;
-  const unsigned long long key = a.ub_key[u];
-  const int lo = (int)(key / a.nf), hi = (int)(key % a.nf);
-  double acc[36], accb[6];
-  for (int i = 0; i < 36; ++i) acc[i] = 0.0;
-  for (int i = 0; i < 6; ++i) accb[i] = 0.0;
-  const int pb = a.ub_pb[u];
-  if (pb >= 0) {
-    for (int64_t c = a.pb_chunk_ptr[pb]; c < a.pb_chunk_ptr[pb + 1]; ++c) {
-      const double* s = a.chunk_buf + c * kPart;
-      for (int i = 0; i < 36; ++i) acc[i] += s[i];
-      if (lo == hi)
-        for (int i = 0; i < 6; ++i) accb[i] += s[36 + i];
-    }
-  }
-  if (a.rank == 0) {
-    if (lo == hi) {
-      const double* Uj = a.U + (int64_t)lo * 36;
-      for (int i = 0; i < 36; ++i) acc[i] += Uj[i];
-      for (int i = 0; i < 6; ++i) {
-        acc[i * 7] += a.lam * a.Dc[lo * 6 + i];
-        accb[i] -= a.gc[lo * 6 + i];
-      }
-    } else if (a.ub_edge[u] >= 0) {
-      const double* H = a.edge_H + (int64_t)a.ub_edge[u] * 36;
-      for (int i = 0; i < 36; ++i) acc[i] += H[i];
-    }
-  }
-  double* up = a.S + (int64_t)a.pos_up[u] * 36;
-  for (int i = 0; i < 36; ++i) up[i] = acc[i];
-  if (lo != hi) {
-    double* dn = a.S + (int64_t)a.pos_lo[u] * 36;
-    for (int r = 0; r < 6; ++r)
-      for (int c = 0; c < 6; ++c) dn[c * 6 + r] = acc[r * 6 + c];
-  } else {
-    for (int i = 0; i < 6; ++i) a.b[lo * 6 + i] = accb[i];
-  }
 }
 
 // ---------------------------------------------------------------------------
@@ -961,210 +1037,6 @@ __global__ void __launch_bounds__(1024) k_dense_solve(int nf, const int* __restr
   for (int i = tid; i < n; i += nt) x[i] = y[i];
   for (int i = tid; i < n; i += nt)
     if (!isfinite(y[i])) sc->nonfinite = 1;
-}
-
-// Block-Jacobi preconditioner: inverse of each 6x6 diagonal block of S.
-__global__ void k_block_jacobi(int nf, const int* __restrict__ diag_pos, const double* __restrict__ S,
-                               double* __restrict__ Minv, BAScalars* sc) {
-  int j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= nf) return;
-  const double* A = S + (int64_t)diag_pos[j] * 36;
-  double L[36];
-  for (int i = 0; i < 36; ++i) L[i] = 0.0;
-  bool ok = true;
-  for (int c = 0; c < 6; ++c) {
-    double s = A[c * 6 + c];
-    for (int k = 0; k < c; ++k) s -= L[c * 6 + k] * L[c * 6 + k];
-    if (!(s > 0.0)) { ok = false; s = 1.0; }
-    double d = sqrt(s);
-    L[c * 6 + c] = d;
-    for (int r = c + 1; r < 6; ++r) {
-      double v = A[r * 6 + c];
-      for (int k = 0; k < c; ++k) v -= L[r * 6 + k] * L[c * 6 + k];
-      L[r * 6 + c] = v / d;
-    }
-  }
-  // inverse of L (lower), then Minv = L^-T L^-1
-  double Li[36];
-  for (int i = 0; i < 36; ++i) Li[i] = 0.0;
-  for (int c = 0; c < 6; ++c) {
-    Li[c * 6 + c] = 1.0 / L[c * 6 + c];
-    for (int r = c + 1; r < 6; ++r) {
-      double s = 0.0;
-      for (int k = c; k < r; ++k) s += L[r * 6 + k] * Li[k * 6 + c];
-      Li[r * 6 + c] = -s / L[r * 6 + r];
-    }
-  }
-  double* M = Minv + (int64_t)j * 36;
-  for (int r = 0; r < 6; ++r)
-    for (int c = 0; c < 6; ++c) {
-      double s = 0.0;
-      for (int k = max(r, c); k < 6; ++k) s += Li[k * 6 + r] * Li[k * 6 + c];
-      M[r * 6 + c] = s;
-    }
-  if (!ok) atomicOr(&sc->nonfinite, 1);
-}
-
-struct PcgArgs {
-  int nf;
-  const int* row_ptr;
-  const int* col;
-  const double* S;
-  const double* Minv;
-  const double* b;
-  double* x;
-  double* r;
-  double* z;
-  double* p0;
-  double* p1;
-  double* q;
-  double* part;  // [4*grid]
-  BAScalars* sc;
-  int max_it;
-  double rtol;
-};
-
-constexpr int kPcgThreads = 256;
-
-__device__ __forceinline__ double grid_sum(const double* part, int G, double* bcast) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double s = 0.0;
-    for (int i = 0; i < G; ++i) s += part[i];
-    *bcast = s;
-  }
-  __syncthreads();
-  return *bcast;
-}
-
-// Persistent cooperative block-Jacobi PCG on the BSR reduced camera system.
-// Two grid barriers per iteration: the search direction p = z + beta*p_prev
-// is formed on the fly inside the SpMV (double-buffered p), so the update
-// phase and the SpMV phase are the only synchronisation points.  All dot
-// products are reduced in a fixed order, so every rank/run takes identical
-// decisions.
-__global__ void __launch_bounds__(kPcgThreads) k_pcg(PcgArgs a) {
-  cg::grid_group grid = cg::this_grid();
-  __shared__ double red[kPcgThreads / 32];
-  __shared__ double bc;
-  const int lane = threadIdx.x & 31;
-  const int wpb = kPcgThreads / 32;
-  const int gw = blockIdx.x * wpb + (threadIdx.x >> 5);
-  const int nw = gridDim.x * wpb;
-  const int G = gridDim.x;
-  double* part_pq = a.part;
-  double* part_rz = a.part + G;
-  double* part_rr = a.part + 2 * G;
-  double* part_bb = a.part + 3 * G;
-  const unsigned full = 0xffffffffu;
-
-  double rz_l = 0.0, bb_l = 0.0;
-  for (int row = gw; row < a.nf; row += nw) {
-    double bi = 0.0, zi = 0.0;
-    if (lane < 6) bi = a.b[row * 6 + lane];
-    double rj[6];
-#pragma unroll
-    for (int j = 0; j < 6; ++j) rj[j] = __shfl_sync(full, bi, j);
-    if (lane < 6) {
-      const double* M = a.Minv + (int64_t)row * 36 + lane * 6;
-#pragma unroll
-      for (int j = 0; j < 6; ++j) zi += M[j] * rj[j];
-      a.x[row * 6 + lane] = 0.0;
-      a.r[row * 6 + lane] = bi;
-      a.z[row * 6 + lane] = zi;
-      a.p0[row * 6 + lane] = 0.0;
-      rz_l += bi * zi;
-      bb_l += bi * bi;
-    }
-  }
-  double s1 = block_sum<kPcgThreads>(rz_l, red);
-  double s2 = block_sum<kPcgThreads>(bb_l, red);
-  if (threadIdx.x == 0) { part_rz[blockIdx.x] = s1; part_bb[blockIdx.x] = s2; }
-  grid.sync();
-  double rz_old = grid_sum(part_rz, G, &bc);
-  const double bnorm = sqrt(grid_sum(part_bb, G, &bc));
-  double beta = 0.0;
-  double* pp = a.p0;
-  double* pn = a.p1;
-  int it = 0, fail = 0;
-  if (bnorm > 0.0 && isfinite(bnorm)) {
-    for (it = 0; it < a.max_it;) {
-      // phase 1: q = S (z + beta*p_prev); p_next for owned rows
-      double pq_l = 0.0;
-      const int grp = lane / 6, comp = lane % 6;
-      for (int row = gw; row < a.nf; row += nw) {
-        double acc = 0.0;
-        if (lane < 30) {
-          for (int k = a.row_ptr[row] + grp; k < a.row_ptr[row + 1]; k += 5) {
-            const int c = a.col[k];
-            const double* sv = a.S + (int64_t)k * 36 + comp * 6;
-            const double* zc = a.z + c * 6;
-            const double* pc = pp + c * 6;
-#pragma unroll
-            for (int j = 0; j < 6; ++j) acc += sv[j] * (zc[j] + beta * pc[j]);
-          }
-        }
-        double v1 = __shfl_sync(full, acc, comp + 6);
-        double v2 = __shfl_sync(full, acc, comp + 12);
-        double v3 = __shfl_sync(full, acc, comp + 18);
-        double v4 = __shfl_sync(full, acc, comp + 24);
-        if (lane < 6) {
-          double qv = (((acc + v1) + v2) + v3) + v4;
-          double pv = a.z[row * 6 + lane] + beta * pp[row * 6 + lane];
-          a.q[row * 6 + lane] = qv;
-          pn[row * 6 + lane] = pv;
-          pq_l += pv * qv;
-        }
-      }
-      double s = block_sum<kPcgThreads>(pq_l, red);
-      if (threadIdx.x == 0) part_pq[blockIdx.x] = s;
-      grid.sync();
-      const double pq = grid_sum(part_pq, G, &bc);
-      if (!(pq > 0.0) || !isfinite(pq)) { fail = 1; break; }
-      const double alpha = rz_old / pq;
-      // phase 2: x += alpha p; r -= alpha q; z = M^-1 r
-      double rz_n = 0.0, rr_n = 0.0;
-      for (int row = gw; row < a.nf; row += nw) {
-        double ri = 0.0;
-        if (lane < 6) {
-          a.x[row * 6 + lane] += alpha * pn[row * 6 + lane];
-          ri = a.r[row * 6 + lane] - alpha * a.q[row * 6 + lane];
-          a.r[row * 6 + lane] = ri;
-        }
-        double rj[6];
-#pragma unroll
-        for (int j = 0; j < 6; ++j) rj[j] = __shfl_sync(full, ri, j);
-        if (lane < 6) {
-          const double* M = a.Minv + (int64_t)row * 36 + lane * 6;
-          double zi = 0.0;
-#pragma unroll
-          for (int j = 0; j < 6; ++j) zi += M[j] * rj[j];
-          a.z[row * 6 + lane] = zi;
-          rz_n += ri * zi;
-          rr_n += ri * ri;
-        }
-      }
-      double t1 = block_sum<kPcgThreads>(rz_n, red);
-      double t2 = block_sum<kPcgThreads>(rr_n, red);
-      if (threadIdx.x == 0) { part_rz[blockIdx.x] = t1; part_rr[blockIdx.x] = t2; }
-      grid.sync();
-      const double rz_new = grid_sum(part_rz, G, &bc);
-      const double rr = grid_sum(part_rr, G, &bc);
-      ++it;
-      if (!isfinite(rr)) { fail = 1; break; }
-      if (sqrt(rr) <= a.rtol * bnorm) break;
-      beta = rz_new / rz_old;
-      rz_old = rz_new;
-      double* tmp = pp; pp = pn; pn = tmp;
-    }
-  } else {
-    if (!isfinite(bnorm)) fail = 1;
-  }
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    a.sc->pcg_iters = it;
-    a.sc->pcg_fail = fail;
-    if (fail) a.sc->nonfinite = 1;
-  }
 }
 
 // ---------------------------------------------------------------------------
@@ -1309,6 +1181,7 @@ void BASolver::setup(const sfm_ba_problem& pr, const sfm_ba_options& opt) {
   obs_frame_.upload(pr.obs_frame, N_, s);
   obs_point_.upload(pr.obs_point, N_, s);
   obs_uv_.upload(pr.obs_uv, (size_t)N_ * 2, s);
+  geo_.resize(N_);
   sc_.resize(1);
   SFM_CUDA(cudaMemsetAsync(sc_.get(), 0, sizeof(BAScalars), s));
 
@@ -1370,49 +1243,15 @@ void BASolver::setup(const sfm_ba_problem& pr, const sfm_ba_options& opt) {
   n_pb_ = h_runs;
   keys_out.release();
   keys_in.release();
-  // pair-block -> pair range, chunk range
-  DevBuf<int64_t> pb_pair_cnt64, pb_pair_ptr, pb_nch;
-  pb_pair_ptr.resize(n_pb_ + 1);
-  pb_chunk_ptr_.resize(n_pb_ + 1);
-  pb_nch.resize(n_pb_ + 1);
-  pb_pair_cnt64.resize(n_pb_ + 1);
-  k_div_ceil<<<grid_for(n_pb_ + 1, 256), 256, 0, s>>>(n_pb_, pb_cnt.get(), pb_pair_cnt64.get(), 1);
-  SFM_CHECK_LAUNCH();
-  k_div_ceil<<<grid_for(n_pb_ + 1, 256), 256, 0, s>>>(n_pb_, pb_cnt.get(), pb_nch.get(), kChunk);
-  SFM_CHECK_LAUNCH();
-  SFM_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, pb_pair_cnt64.get(), pb_pair_ptr.get(), n_pb_ + 1, s));
-  SFM_CUDA(cub::DeviceScan::ExclusiveSum(tmp.get(tb), tb, pb_pair_cnt64.get(), pb_pair_ptr.get(), n_pb_ + 1, s));
-  SFM_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, pb_nch.get(), pb_chunk_ptr_.get(), n_pb_ + 1, s));
-  SFM_CUDA(cub::DeviceScan::ExclusiveSum(tmp.get(tb), tb, pb_nch.get(), pb_chunk_ptr_.get(), n_pb_ + 1, s));
-  int64_t n_chunks = 0;
-  SFM_CUDA(cudaMemcpyAsync(&n_chunks, pb_chunk_ptr_.get() + n_pb_, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
-  SFM_CUDA(cudaStreamSynchronize(s));
-  n_chunks_ = n_chunks;
-  chunk_start_.resize(n_chunks_ + 1);
-  chunk_pb_.resize(n_chunks_ + 1);
-  if (n_pb_) { k_chunk_gen<<<grid_for(n_pb_, 256), 256, 0, s>>>(n_pb_, pb_pair_ptr.get(), pb_chunk_ptr_.get(), n_pairs_, chunk_start_.get(), chunk_pb_.get()); SFM_CHECK_LAUNCH(); }
-  else SFM_CUDA(cudaMemsetAsync(chunk_start_.get(), 0, sizeof(int64_t), s));
-  // diagonal chunk ids
+  // pair-block -> pair range
   {
-    DevBuf<char> flags;
-    DevBuf<int64_t> iota;
-    DevBuf<int64_t> nsel;
-    flags.resize(n_chunks_);
-    iota.resize(n_chunks_);
-    diag_chunks_.resize(n_chunks_);
-    nsel.resize(1);
-    int64_t hs = 0;
-    if (n_chunks_) {
-      k_diag_flags<<<grid_for(n_chunks_, 256), 256, 0, s>>>(n_chunks_, nfree_, chunk_pb_.get(), pb_key.get(), flags.get());
-      SFM_CHECK_LAUNCH();
-      k_iota64<<<grid_for(n_chunks_, 256), 256, 0, s>>>(n_chunks_, iota.get());
-      SFM_CHECK_LAUNCH();
-      SFM_CUDA(cub::DeviceSelect::Flagged(nullptr, tb, iota.get(), flags.get(), diag_chunks_.get(), nsel.get(), n_chunks_, s));
-      SFM_CUDA(cub::DeviceSelect::Flagged(tmp.get(tb), tb, iota.get(), flags.get(), diag_chunks_.get(), nsel.get(), n_chunks_, s));
-      nsel.download(&hs, 1, s);
-      SFM_CUDA(cudaStreamSynchronize(s));
-    }
-    n_diag_chunks_ = hs;
+    DevBuf<int64_t> pb_pair_cnt64;
+    pb_pair_cnt64.resize(n_pb_ + 1);
+    pb_pair_ptr_.resize(n_pb_ + 1);
+    k_div_ceil<<<grid_for(n_pb_ + 1, 256), 256, 0, s>>>(n_pb_, pb_cnt.get(), pb_pair_cnt64.get(), 1);
+    SFM_CHECK_LAUNCH();
+    SFM_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, pb_pair_cnt64.get(), pb_pair_ptr_.get(), n_pb_ + 1, s));
+    SFM_CUDA(cub::DeviceScan::ExclusiveSum(tmp.get(tb), tb, pb_pair_cnt64.get(), pb_pair_ptr_.get(), n_pb_ + 1, s));
   }
 
   // ---- S block pattern: pair blocks U diagonal U lambda_c edges ----------
@@ -1519,6 +1358,11 @@ void BASolver::setup(const sfm_ba_problem& pr, const sfm_ba_options& opt) {
     SFM_CUDA(cudaMemsetAsync(ub_edge_.get(), 0xff, sizeof(int) * n_ub_, s));
   }
   if (n_pb_) { k_scatter_pb<<<grid_for(n_pb_, 256), 256, 0, s>>>(n_pb_, n_ub_, pb_key.get(), ub_key_.get(), ub_pb_.get()); SFM_CHECK_LAUNCH(); }
+  std::vector<int> hpb(n_ub_);
+  std::vector<int64_t> hptr(n_pb_ + 1);
+  if (n_ub_) ub_pb_.download(hpb.data(), n_ub_, s);
+  pb_pair_ptr_.download(hptr.data(), n_pb_ + 1, s);
+  SFM_CUDA(cudaStreamSynchronize(s));
   edge_ab_.upload(h_ab.data(), h_ab.size(), s);
   prior_frame_.upload(h_pf.data(), h_pf.size(), s);
   if (n_edges_) { k_scatter_edges<<<grid_for(n_edges_, 128), 128, 0, s>>>(n_edges_, nfree_, edge_ab_.get(), free_idx_.get(), n_ub_, ub_key_.get(), ub_edge_.get()); SFM_CHECK_LAUNCH(); }
@@ -1540,6 +1384,41 @@ void BASolver::setup(const sfm_ba_problem& pr, const sfm_ba_options& opt) {
     diag_ub_host_ = dub;
     diag_ub_.upload(dub.data(), nfree_, s);
     diag_pos_.upload(dpos.data(), nfree_, s);
+  }
+  // camera-major observation streams + off-diagonal block list
+  {
+    std::vector<int64_t> cptr(nfree_ + 1, 0);
+    for (int j = 0; j < nfree_; ++j) {
+      const int pb = hpb[diag_ub_host_[j]];
+      cptr[j + 1] = cptr[j] + (pb < 0 ? 0 : hptr[pb + 1] - hptr[pb]);
+    }
+    n_cm_ = cptr[nfree_];
+    cm_ptr_.upload(cptr.data(), cptr.size(), s);
+    cm_obs_.resize(n_cm_);
+    cm_pt_.resize(n_cm_);
+    cm_uv_.resize((size_t)n_cm_ * 2);
+    geo_cm_.resize(n_cm_);
+    cm_pos_.resize(N_);
+    if (N_) SFM_CUDA(cudaMemsetAsync(cm_pos_.get(), 0xff, sizeof(int) * N_, s));
+    if (nfree_) {
+      k_cm_build<<<grid_for((int64_t)nfree_ * 32, 128), 128, 0, s>>>(
+          nfree_, diag_ub_.get(), ub_pb_.get(), pb_pair_ptr_.get(), pairs_.get(), cm_ptr_.get(),
+          obs_point_.get(), obs_uv_.get(), cm_obs_.get(), cm_pt_.get(), cm_uv_.get(), cm_pos_.get());
+      SFM_CHECK_LAUNCH();
+    }
+    pair_pt_.resize(n_pairs_);
+    if (n_pairs_) {
+      k_pair_pt<<<grid_for(n_pairs_, 256), 256, 0, s>>>(n_pairs_, pairs_.get(), obs_point_.get(), pair_pt_.get());
+      SFM_CHECK_LAUNCH();
+    }
+    std::vector<unsigned long long> hk(n_ub_);
+    if (n_ub_) ub_key_.download(hk.data(), n_ub_, s);
+    SFM_CUDA(cudaStreamSynchronize(s));
+    std::vector<int> off;
+    for (int u = 0; u < n_ub_; ++u)
+      if (hk[u] / nfree_ != hk[u] % nfree_) off.push_back(u);
+    n_off_ = (int)off.size();
+    work_.upload(off.data(), off.size(), s);
   }
   // pose terms per free camera (edge side 0 = from/a, 1 = to/b, prior 2)
   {
@@ -1572,21 +1451,13 @@ void BASolver::setup(const sfm_ba_problem& pr, const sfm_ba_options& opt) {
   // work buffers
   V_.resize((size_t)P_ * 6);
   gp_.resize((size_t)P_ * 3);
-  Vinv_.resize((size_t)P_ * 6);
-  e_.resize((size_t)P_ * 3);
+  pv_.resize((size_t)P_ * 12);
   U_.resize((size_t)nfree_ * 36);
   gc_.resize((size_t)nfree_ * 6);
   Dc_.resize((size_t)nfree_ * 6);
-  chunk_buf_.resize((size_t)n_chunks_ * kPart);
   S_.resize((size_t)n_full_ * 36);
   b_.resize((size_t)nfree_ * 6);
   dc_.resize((size_t)nfree_ * 6);
-  Minv_.resize((size_t)nfree_ * 36);
-  r_.resize((size_t)nfree_ * 6);
-  z_.resize((size_t)nfree_ * 6);
-  p0_.resize((size_t)nfree_ * 6);
-  p1_.resize((size_t)nfree_ * 6);
-  qv_.resize((size_t)nfree_ * 6);
   part_a_.resize(grid_for(std::max<int64_t>(P_, 1), kBlock));
   part_b_.resize(grid_for(std::max<int64_t>(P_, 1), kBlock));
   part_c_.resize(grid_for(std::max(n_edges_ + n_priors_, 1), kBlock));
@@ -1607,13 +1478,9 @@ void BASolver::setup(const sfm_ba_problem& pr, const sfm_ba_options& opt) {
     SFM_CUDA(cudaFuncSetAttribute(k_dense_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max<size_t>(smem, 1)));
   }
   if (!use_dense_ && nfree_ > 0) {
-    int dev = 0, nsm = 0, per_sm = 0;
-    SFM_CUDA(cudaGetDevice(&dev));
-    SFM_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-    SFM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pcg, kPcgThreads, 0));
-    int want = (nfree_ + (kPcgThreads / 32) - 1) / (kPcgThreads / 32);
-    pcg_grid_ = std::max(1, std::min(want, nsm * std::max(per_sm, 1)));
-    pcg_part_.resize(4 * (size_t)pcg_grid_);
+    const int cl = opt_.coarse_cluster == 0 ? 16 : opt_.coarse_cluster;
+    pcg_.setup(nfree_, cl, s);
+    pcg_.set_pattern(row_ptr_.get(), col_idx_.get(), n_full_, s);
   }
 
   // all_fixed (solver.py:200-203) and the initial cost (solver.py:201)
@@ -1715,32 +1582,33 @@ void BASolver::linearize() {
   pa.P = P_; pa.lk = opt_.loss_kind; pa.lp = opt_.loss_param;
   pa.ptr = pt_ptr_.get(); pa.of = obs_frame_.get(); pa.uv = obs_uv_.get();
   pa.frame_model = frame_model_.get(); pa.models = models_.get(); pa.free_idx = free_idx_.get();
-  pa.Rt = Rt_[cur_].get(); pa.X = X_[cur_].get(); pa.sc = sc_.get();
+  pa.Rt = Rt_[cur_].get(); pa.X = X_[cur_].get(); pa.sc = sc_.get(); pa.geo = geo_.get();
+  pa.cm_pos = cm_pos_.get(); pa.geo_cm = geo_cm_.get();
   if (P_) {
-    ProfScope ps(*prof_, "point_lin", 24.0 * N_ + 24.0 * P_ + 72.0 * P_, s);
+    // compulsory: observation records in, points in, V/g_p and the 32-byte
+    // linearisation record per observation out
+    ProfScope ps(*prof_, "point_lin", 24.0 * N_ + 24.0 * P_ + 72.0 * P_ + 32.0 * N_, s);
     k_point_lin<<<grid_for(P_, kBlock), kBlock, 0, s>>>(pa, V_.get(), gp_.get());
   }
-  if (n_diag_chunks_) {
-    ChunkArgs ca{};
-    ca.n = n_diag_chunks_; ca.ids = diag_chunks_.get(); ca.start = chunk_start_.get();
-    ca.pairs = pairs_.get(); ca.op = obs_point_.get(); ca.of = obs_frame_.get(); ca.uv = obs_uv_.get();
-    ca.frame_model = frame_model_.get(); ca.models = models_.get(); ca.Rt = Rt_[cur_].get();
-    ca.X = X_[cur_].get(); ca.lk = opt_.loss_kind; ca.lp = opt_.loss_param; ca.out = chunk_buf_.get();
-    // compulsory: diagonal pairs (8 B) + observation records (24 B) + points
-    ProfScope ps(*prof_, "cam_lin_chunks", 32.0 * N_ + 24.0 * P_ + (double)n_diag_chunks_ * kPart * 8.0, s);
-    k_chunks<0><<<grid_for(n_diag_chunks_, kBlock), kBlock, 0, s>>>(ca);
+  if (nfree_) {
+    BlkArgs ba = blk_args(0.0);
+    ba.Uout = U_.get();
+    ba.gout = gc_.get();
+    // compulsory: camera-major linearisation record (32 B) + pixel (16 B)
+    // per observation; U, g_c out
+    ProfScope ps(*prof_, "cam_lin", 48.0 * n_cm_ + 336.0 * nfree_, s);
+    k_cam_blocks<0><<<nfree_, kCamWarps * 32, 0, s>>>(ba);
   }
   if (nfree_) {
     CamArgs c{};
-    c.nf = nfree_; c.rank = rank_; c.free_frame = free_frame_.get(); c.diag_ub = diag_ub_.get();
-    c.ub_pb = ub_pb_.get(); c.pb_chunk_ptr = pb_chunk_ptr_.get(); c.chunk_buf = chunk_buf_.get();
+    c.nf = nfree_;
     c.term_ptr = term_ptr_.get(); c.term_list = term_list_.get(); c.ab = edge_ab_.get();
     c.pf = prior_frame_.get(); c.E = n_edges_; c.meas_inv = edge_meas_inv_.get();
     c.init_inv = prior_init_inv_.get(); c.we = edge_w_; c.wa = prior_w_;
     c.q = q_[cur_].get(); c.t = t_[cur_].get(); c.Rt = Rt_[cur_].get(); c.U = U_.get(); c.gc = gc_.get();
-    {
-      ProfScope ps(*prof_, "cam_lin", 0.0, s);
-      k_cam_lin<<<grid_for(nfree_, 64), 64, 0, s>>>(c);
+    if (n_edges_ + n_priors_) {
+      ProfScope ps(*prof_, "cam_terms", 0.0, s);
+      k_cam_terms<<<grid_for(nfree_, 64), 64, 0, s>>>(c);
     }
     if (comm_ && comm_->active()) {
       comm_->sum(U_.get(), (size_t)nfree_ * 36, s);
@@ -1755,37 +1623,48 @@ void BASolver::linearize() {
     ProfScope ps(*prof_, "edge_lin", 0.0, s);
     k_edge_lin<<<grid_for(n_edges_, 64), 64, 0, s>>>(n_edges_, edge_ab_.get(), free_idx_.get(), edge_meas_inv_.get(), edge_w_, q_[cur_].get(), t_[cur_].get(), Rt_[cur_].get(), edge_H_.get());
   }
+  if (!use_dense_ && nfree_)
+    pcg_.set_basis(free_frame_.get(), q_[cur_].get(), t_[cur_].get(), Rt_[cur_].get(), s, prof_);
   if (comm_ && comm_->active()) comm_->max_u64(&sc_.get()->gmax, 1, s);
   read_scalars();
+}
+
+BlkArgs BASolver::blk_args(double lam) const {
+  BlkArgs ba{};
+  ba.work = work_.get(); ba.nf = nfree_; ba.rank = rank_; ba.lam = lam;
+  ba.ub_key = ub_key_.get(); ba.ub_pb = ub_pb_.get(); ba.ub_edge = ub_edge_.get();
+  ba.pos_up = ub_pos_up_.get(); ba.pos_lo = ub_pos_lo_.get(); ba.diag_ub = diag_ub_.get();
+  ba.pb_pair_ptr = pb_pair_ptr_.get(); ba.pairs = pairs_.get(); ba.op = obs_point_.get();
+  ba.of = obs_frame_.get(); ba.uv = obs_uv_.get(); ba.free_frame = free_frame_.get();
+  ba.frame_model = frame_model_.get(); ba.models = models_.get(); ba.Rt = Rt_[cur_].get();
+  ba.geo = geo_.get(); ba.pv = pv_.get(); ba.pair_pt = pair_pt_.get(); ba.cm_ptr = cm_ptr_.get();
+  ba.cm_pt = cm_pt_.get(); ba.cm_uv = cm_uv_.get(); ba.geo_cm = geo_cm_.get(); ba.diag_pos = diag_pos_.get();
+  ba.U = U_.get(); ba.Dc = Dc_.get();
+  ba.gc = gc_.get(); ba.edge_H = edge_H_.get(); ba.S = S_.get(); ba.b = b_.get();
+  return ba;
 }
 
 void BASolver::build_schur(double lam) {
   cudaStream_t s = stream_;
   if (P_) {
-    ProfScope ps(*prof_, "point_prep", 72.0 * P_ + 72.0 * P_, s);
-    k_point_prep<<<grid_for(P_, 256), 256, 0, s>>>(P_, lam, V_.get(), gp_.get(), Vinv_.get(), e_.get(), sc_.get());
+    ProfScope ps(*prof_, "point_prep", 72.0 * P_ + 96.0 * P_, s);
+    k_point_prep<<<grid_for(P_, 256), 256, 0, s>>>(P_, lam, V_.get(), gp_.get(), pv_.get(), sc_.get());
   }
-  if (n_chunks_) {
-    ChunkArgs ca{};
-    ca.n = n_chunks_; ca.ids = nullptr; ca.start = chunk_start_.get();
-    ca.pairs = pairs_.get(); ca.op = obs_point_.get(); ca.of = obs_frame_.get(); ca.uv = obs_uv_.get();
-    ca.frame_model = frame_model_.get(); ca.models = models_.get(); ca.Rt = Rt_[cur_].get();
-    ca.X = X_[cur_].get(); ca.Vinv = Vinv_.get(); ca.e = e_.get(); ca.lk = opt_.loss_kind; ca.lp = opt_.loss_param;
-    ca.out = chunk_buf_.get();
-    // compulsory: pair list + observation records + point state (X, V*^-1, e)
-    // + chunk partials written
-    ProfScope ps(*prof_, "schur_chunks",
-                 8.0 * n_pairs_ + 24.0 * N_ + (24.0 + 72.0) * P_ + (double)n_chunks_ * kPart * 8.0, s);
-    k_chunks<1><<<grid_for(n_chunks_, kBlock), kBlock, 0, s>>>(ca);
+  if (nfree_) {
+    BlkArgs ba = blk_args(lam);
+    // compulsory: camera-major record + point id per observation, packed
+    // point record (V*^-1, e), diagonal blocks and b out
+    ProfScope ps(*prof_, "schur_diag", (32.0 + 4.0) * n_cm_ + 96.0 * P_ + 336.0 * nfree_, s);
+    k_cam_blocks<1><<<nfree_, kCamWarps * 32, 0, s>>>(ba);
   }
-  if (n_ub_) {
-    BlockArgs ba{};
-    ba.n_ub = n_ub_; ba.nf = nfree_; ba.rank = rank_; ba.lam = lam; ba.ub_key = ub_key_.get();
-    ba.ub_pb = ub_pb_.get(); ba.ub_edge = ub_edge_.get(); ba.pos_up = ub_pos_up_.get(); ba.pos_lo = ub_pos_lo_.get();
-    ba.pb_chunk_ptr = pb_chunk_ptr_.get(); ba.chunk_buf = chunk_buf_.get(); ba.U = U_.get(); ba.Dc = Dc_.get();
-    ba.gc = gc_.get(); ba.edge_H = edge_H_.get(); ba.S = S_.get(); ba.b = b_.get();
-    ProfScope ps(*prof_, "schur_blocks", (double)n_chunks_ * kPart * 8.0 + 288.0 * n_full_, s);
-    k_block_finalize<<<grid_for(n_ub_, 128), 128, 0, s>>>(ba);
+  if (n_off_) {
+    BlkArgs ba = blk_args(lam);
+    ba.n = n_off_;
+    // compulsory: off-diagonal pair list (8 B) + pair point (4 B), both
+    // observation records, point V*^-1 once; both triangles of S out
+    ProfScope ps(*prof_, "schur_offdiag",
+                 12.0 * (n_pairs_ - n_cm_) + 32.0 * N_ + 48.0 * P_ + 288.0 * (n_full_ - nfree_), s);
+    k_offdiag_blocks<<<grid_for((int64_t)n_off_ * 32, kBlkWarps * 32), kBlkWarps * 32, 0, s>>>(ba);
   }
   if (comm_ && comm_->active()) {
     comm_->sum(S_.get(), (size_t)n_full_ * 36, s);
@@ -1803,19 +1682,11 @@ bool BASolver::solve_reduced() {
     k_dense_solve<<<1, 1024, smem, s>>>(nfree_, row_ptr_.get(), col_idx_.get(), S_.get(), b_.get(), dc_.get(), sc_.get());
     return true;
   }
-  {
-    ProfScope ps(*prof_, "block_jacobi", 0.0, s);
-    k_block_jacobi<<<grid_for(nfree_, 64), 64, 0, s>>>(nfree_, diag_pos_.get(), S_.get(), Minv_.get(), sc_.get());
-  }
-  PcgArgs a{};
-  a.nf = nfree_; a.row_ptr = row_ptr_.get(); a.col = col_idx_.get(); a.S = S_.get(); a.Minv = Minv_.get();
-  a.b = b_.get(); a.x = dc_.get(); a.r = r_.get(); a.z = z_.get(); a.p0 = p0_.get(); a.p1 = p1_.get();
-  a.q = qv_.get(); a.part = pcg_part_.get(); a.sc = sc_.get();
-  a.max_it = opt_.pcg_max_iters > 0 ? opt_.pcg_max_iters : 1000;
-  a.rtol = opt_.pcg_rtol > 0 ? opt_.pcg_rtol : 1e-10;
-  void* args[] = {&a};
-  ProfScope ps(*prof_, "pcg", 0.0, s);
-  SFM_CUDA(cudaLaunchCooperativeKernel((void*)k_pcg, pcg_grid_, kPcgThreads, args, 0, s));
+  PcgProblem pp{};
+  pp.nf = nfree_; pp.row_ptr = row_ptr_.get(); pp.col = col_idx_.get(); pp.S = S_.get(); pp.nnzb = n_full_;
+  pp.diag_pos = diag_pos_.get(); pp.b = b_.get(); pp.x = dc_.get();
+  pcg_.solve(pp, opt_.pcg_max_iters > 0 ? opt_.pcg_max_iters : 1000, opt_.pcg_rtol > 0 ? opt_.pcg_rtol : 1e-10,
+             sc_.get(), s, prof_);
   return true;
 }
 
@@ -1839,11 +1710,13 @@ bool BASolver::trial(double lam, double* new_cost, double* step_norm) {
   pa.ptr = pt_ptr_.get(); pa.of = obs_frame_.get(); pa.uv = obs_uv_.get();
   pa.frame_model = frame_model_.get(); pa.models = models_.get(); pa.free_idx = free_idx_.get();
   pa.Rt = Rt_[cur_].get(); pa.X = X_[cur_].get(); pa.Rt_eval = Rt_[o].get(); pa.X_out = X_[o].get();
-  pa.Vinv = Vinv_.get(); pa.e = e_.get(); pa.dc = dc_.get();
+  pa.pv = pv_.get(); pa.dc = dc_.get(); pa.geo = geo_.get();
   pa.obs_offset = obs_offset_; pa.part_cost = part_a_.get(); pa.part_dp2 = part_b_.get(); pa.sc = sc_.get();
   const unsigned gp = grid_for(std::max<int64_t>(P_, 1), kBlock);
   {
-    ProfScope ps(*prof_, "point_trial", 24.0 * N_ + 24.0 * N_ + (24.0 + 72.0 + 24.0) * P_, s);
+    // compulsory: observation records + linearisation records, point state
+    // (X, V*^-1, e) in, trial points out
+    ProfScope ps(*prof_, "point_trial", 24.0 * N_ + 32.0 * N_ + (24.0 + 72.0 + 24.0) * P_, s);
     k_point_cost<true><<<gp, kBlock, 0, s>>>(pa);
   }
   const int T = n_edges_ + n_priors_;

@@ -9,8 +9,11 @@
 #pragma once
 #include "comm.cuh"
 #include "common.cuh"
+#include "pcg.cuh"
 
 namespace sfm {
+
+struct BlkArgs;
 
 inline double __longlong_as_double_host(unsigned long long b) {
   double d;
@@ -54,6 +57,7 @@ class BASolver {
   bool solve_reduced();
   void raise_projection_error(bool trial_state);
   void read_scalars();
+  BlkArgs blk_args(double lam) const;
 
   cudaStream_t stream_;
   Profiler* prof_;
@@ -87,22 +91,26 @@ class BASolver {
   DevBuf<int> obs_frame_, obs_point_;
   DevBuf<double> obs_uv_;   // [N*2]
   DevBuf<int64_t> pt_ptr_;  // [P+1]
+  DevBuf<double4> geo_;     // [N] linearisation records (x, y, 1/Z, w)
 
   // pair structure (sorted by S block, then point)
   int64_t n_pairs_ = 0;
   int n_pb_ = 0, n_ub_ = 0, n_full_ = 0;
-  int64_t n_chunks_ = 0, n_diag_chunks_ = 0;
   DevBuf<unsigned long long> pairs_;     // (obs_lo << 32) | obs_hi
-  DevBuf<int64_t> chunk_start_;          // [n_chunks+1] pair index
-  DevBuf<int> chunk_pb_;                 // [n_chunks] pair block
-  DevBuf<int64_t> diag_chunks_;          // [n_diag_chunks] chunk ids of diagonal blocks
-  DevBuf<int64_t> pb_chunk_ptr_;         // [n_pb+1]
+  DevBuf<int64_t> pb_pair_ptr_;          // [n_pb+1] pair range per pair block
+  DevBuf<int> work_;                     // [n_off] off-diagonal S blocks (row-major)
+  DevBuf<int> pair_pt_;                  // [n_pairs] point of each pair
+  int n_off_ = 0;
+  int64_t n_cm_ = 0;                     // observations in free cameras
+  DevBuf<int64_t> cm_ptr_, cm_obs_;      // camera-major observation streams
+  DevBuf<int> cm_pt_, cm_pos_;
+  DevBuf<double> cm_uv_;
+  DevBuf<double4> geo_cm_;
   DevBuf<unsigned long long> ub_key_;    // [n_ub] upper block keys lo*nfree+hi
   DevBuf<int> ub_pb_;                    // [n_ub] pair block or -1
   DevBuf<int> ub_edge_;                  // [n_ub] edge or -1
   DevBuf<int> ub_pos_up_, ub_pos_lo_;    // [n_ub] BSR slots (lo = -1 on diagonal)
   DevBuf<int> row_ptr_, col_idx_;        // BSR full pattern
-  DevBuf<double> chunk_buf_;             // [n_chunks*42]
 
   // pose terms
   DevBuf<int> edge_ab_, prior_frame_;
@@ -115,11 +123,10 @@ class BASolver {
   DevBuf<double> V_, gp_;                // [P*6], [P*3]
   DevBuf<double> U_, gc_, Dc_;           // [nf*36], [nf*6], [nf*6]
   // trial
-  DevBuf<double> Vinv_, e_;              // [P*6], [P*3]
+  DevBuf<double> pv_;                    // [P*12] V*^-1 (6) | e (3) | pad
   DevBuf<double> S_, b_;                 // [n_full*36], [nf*6]
   DevBuf<double> dc_;                    // [nf*6]
-  DevBuf<double> Minv_, r_, z_, p0_, p1_, qv_, pcg_part_;  // PCG
-  DevBuf<double> dense_;                 // dense factor scratch (global fallback)
+  TwoLevelPcg pcg_;
 
   // reductions
   DevBuf<double> part_a_, part_b_, part_c_, part_d_;
@@ -127,7 +134,6 @@ class BASolver {
   std::vector<int> diag_ub_host_;
   DevBuf<BAScalars> sc_;
   BAScalars h_sc_{};
-  int pcg_grid_ = 0;
 };
 
 }  // namespace sfm

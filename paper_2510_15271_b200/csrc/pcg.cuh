@@ -1,0 +1,58 @@
+// pcg.cuh -- two-level preconditioned CG on the reduced camera system S.
+//
+// Replaces the exact sparse solve of the damped normal equations
+// (solver.py:220-222, SuperLU on the un-reduced system) for large problems.
+// Preconditioner: additive two-level
+//     M^-1 r = D^-1 r + P A_c^-1 P^T r
+// with D the 6x6 block diagonal of S (block-Jacobi) and P the rigid-motion
+// coarse space: cameras are aggregated into clusters of C consecutive free
+// frames and camera j's coarse basis is Adj(T_j) (a world-frame rigid motion
+// of the whole cluster, expressed as left perturbations).  A_c = P^T S P is
+// assembled on device and inverted by a cooperative blocked Gauss-Jordan.
+// The Krylov loop is one persistent cooperative kernel with two grid
+// barriers per iteration; every reduction has a fixed order.
+#pragma once
+#include "common.cuh"
+
+namespace sfm {
+
+struct BAScalars;
+
+struct PcgProblem {
+  int nf;
+  const int* row_ptr;     // BSR (both triangles), [nf+1]
+  const int* col;         // [nnzb]
+  const double* S;        // [nnzb*36] row-major blocks
+  int nnzb;
+  const int* diag_pos;    // [nf] BSR slot of the diagonal block
+  const double* b;        // [nf*6]
+  double* x;              // [nf*6] solution
+};
+
+class TwoLevelPcg {
+ public:
+  // cluster <= 0 disables the coarse level (plain block-Jacobi).
+  void setup(int nf, int cluster, cudaStream_t s);
+  // Coarse assembly runs from the (fixed) BSR pattern of S.
+  void set_pattern(const int* row_ptr, const int* col, int nnzb, cudaStream_t s);
+  // Coarse basis P_j = Adj(T_j) from the linearisation-point poses.
+  void set_basis(const int* free_frame, const double* q, const double* t, const double* Rt,
+                 cudaStream_t s, Profiler* prof);
+  // Solves S x = b; writes iteration count / failure into sc.
+  void solve(const PcgProblem& p, int max_it, double rtol, BAScalars* sc, cudaStream_t s,
+             Profiler* prof);
+  int last_grid() const { return grid_; }
+
+ private:
+  int nf_ = 0, C_ = 0, nc_ = 0, ncp_ = 0, npad_ = 0, kc_ = 0, grid_ = 0, gj_grid_ = 0;
+  size_t smem_ = 0;
+  int npairs_ = 0;
+  bool coarse_valid_ = false;
+  const double* Aci_ = nullptr;
+  DevBuf<double> Minv_, Pm_, Ac_[2], r_, z_, p_, q_, qc_, rc0_, part_;
+  DevBuf<int2> pair_cd_;
+  DevBuf<int> pair_ptr_;
+  DevBuf<int4> runs_;
+};
+
+}  // namespace sfm

@@ -216,7 +216,8 @@ def _options(loss: RobustLoss, sopt: SolverOptions, dopt: DeviceOptions) -> nat.
     return nat.BAOptionsC(nat.LOSS_KINDS[loss.kind], int(sopt.max_iters), float(loss.param),
                           float(sopt.grad_tol), float(sopt.param_tol), float(sopt.initial_lambda),
                           float(sopt.max_lambda), nat.LINSOLVE[dopt.linear_solver],
-                          int(dopt.pcg_max_iters), float(dopt.pcg_rtol), int(dopt.dense_max_dim), 0)
+                          int(dopt.pcg_max_iters), float(dopt.pcg_rtol), int(dopt.dense_max_dim),
+                          int(dopt.coarse_cluster))
 
 
 def solve_arrays(arrays: BAArrays, loss: RobustLoss = TRIVIAL_LOSS,

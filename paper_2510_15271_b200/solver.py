@@ -47,14 +47,17 @@ class DeviceOptions:
     """How the reduced camera system S dc = b is solved on the B200.
 
     linear_solver: "auto" (dense Cholesky when 6*free_frames <= dense_max_dim,
-    block-Jacobi PCG otherwise), "dense" or "pcg".  pcg_rtol is the relative
-    residual |r|/|b| at which PCG stops.
+    two-level PCG otherwise), "dense" or "pcg".  pcg_rtol is the relative
+    residual |r|/|b| at which PCG stops; the PCG preconditioner is block-Jacobi
+    plus a rigid-motion coarse space over clusters of `coarse_cluster`
+    consecutive free frames.
     """
 
     linear_solver: str = "auto"
     pcg_rtol: float = 1e-12
     pcg_max_iters: int = 2000
     dense_max_dim: int = 210
+    coarse_cluster: int = 16     # frames per coarse cluster; < 0 = block-Jacobi only
 
 
 DEFAULT_DEVICE_OPTIONS = DeviceOptions()
