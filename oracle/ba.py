@@ -203,17 +203,33 @@ class BAProblem:
         for (ja, jb), H in lin["Hoff"].items():
             S4[ja, jb] += H
             S4[jb, ja] += H.T
+        S_pt, b_pt = self.point_schur_terms(lin, Vinv, e)
+        S = S4.transpose(0, 2, 1, 3).reshape(6 * nf, 6 * nf) + S_pt
+        return S, -gc.reshape(-1) + b_pt, Vinv, e, dV, dU
+
+    def point_schur_terms(self, lin, Vinv, e):
+        """The points' share of the reduced system: -sum_i W V*_i^-1 W^T and
+        sum_i W e_i.  Under point sharding each rank holds only its points'
+        share; the camera blocks are added once."""
+        nf, W, j = self.nf, lin["W"], lin["j"]
+        S4 = np.zeros((nf, nf, 6, 6))
         a, b = self._pairs()
         CH = 1 << 18
         for s0 in range(0, len(a), CH):
             aa, bb = a[s0:s0 + CH], b[s0:s0 + CH]
             C = np.einsum("nij,njk,nlk->nil", W[aa], Vinv[self.op[aa]], W[bb])
             np.add.at(S4, (j[aa], j[bb]), -C)
-        rhs = -gc.copy()
+        rhs = np.zeros((nf, 6))
         fr = j >= 0
         np.add.at(rhs, j[fr], np.einsum("nij,nj->ni", W[fr], e[self.op[fr]]))
-        S = S4.transpose(0, 2, 1, 3).reshape(6 * nf, 6 * nf)
-        return S, rhs.reshape(-1), Vinv, e, dV, dU
+        return S4.transpose(0, 2, 1, 3).reshape(6 * nf, 6 * nf), rhs.reshape(-1)
+
+    def damped_points(self, lin, lam):
+        """V* = V + lam max(diag V, 1e-12) (solver.py:217-220), V*^-1, e."""
+        V, gp = lin["V"], lin["gp"]
+        dV = np.maximum(np.einsum("pii->pi", V), 1e-12)
+        Vinv = np.linalg.inv(V + lam * np.einsum("pi,ij->pij", dV, np.eye(3)))
+        return Vinv, np.einsum("pij,pj->pi", Vinv, gp)
 
     def solve_step(self, lin, lam):
         """(H + lam D) delta = -g via the Schur complement -> (dc, dp) or None."""

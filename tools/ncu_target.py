@@ -1,4 +1,5 @@
-"""Small driver for ncu captures: a few LM iterations on a config scene."""
+"""Small driver for ncu captures: a few LM iterations on a config scene with
+the bench's solver options (bench.py).  usage: ncu_target.py [CFG] [ITERS]"""
 import sys
 sys.path.insert(0, ".")
 from paper_2510_15271_b200.scenes import config_scene, scene_arrays
@@ -8,6 +9,6 @@ cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 3
 iters = int(sys.argv[2]) if len(sys.argv) > 2 else 2
 a = scene_arrays(config_scene(cfg, seed=0))
 ba = DeviceBA(a, RobustLoss("huber", 2.0), SolverOptions(max_iters=100),
-              DeviceOptions(linear_solver="pcg", pcg_rtol=1e-6, pcg_max_iters=2000))
+              DeviceOptions(linear_solver="pcg", pcg_rtol=1e-10, pcg_max_iters=500))
 r = ba.iterate(iters)
 print("iters", r.iterations, "trials", r.n_trials, "pcg", r.pcg_iterations, "ms", r.device_ms)
