@@ -25,7 +25,7 @@
 extern "C" {
 #endif
 
-#define SFM_ABI_VERSION 1
+#define SFM_ABI_VERSION 2
 
 /* ---- error codes (mapped to sfmkit.errors classes by the Python layer) --- */
 #define SFM_OK 0
@@ -132,7 +132,9 @@ typedef struct {
   double pcg_rtol;            /* relative residual tolerance of PCG       */
   int32_t dense_max_dim;      /* AUTO: dense Cholesky when 6*free <= this */
   int32_t coarse_cluster;     /* PCG coarse level: frames per cluster (0 =
-                                 default 16, < 0 = block-Jacobi only)      */
+                                 default 8, < 0 = block-Jacobi only)       */
+  int32_t coarse_refresh;     /* rebuild the coarse operator every this many
+                                 linearisations (0 = default 4)            */
 } sfm_ba_options;
 
 /* SolverReport (solver.py:90-95) + device-side statistics. */

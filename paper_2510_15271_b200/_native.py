@@ -17,6 +17,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libsfm_b200.so")
 
 # ---- constants (mirror include/sfm_b200.h) ---------------------------------
+ABI_VERSION = 2
 SFM_OK = 0
 SFM_E_INVALID = -1
 SFM_E_NON_POSITIVE_DEPTH = -2
@@ -81,7 +82,8 @@ class BAOptionsC(ctypes.Structure):
                 ("param_tol", ctypes.c_double), ("initial_lambda", ctypes.c_double),
                 ("max_lambda", ctypes.c_double), ("linear_solver", ctypes.c_int32),
                 ("pcg_max_iters", ctypes.c_int32), ("pcg_rtol", ctypes.c_double),
-                ("dense_max_dim", ctypes.c_int32), ("coarse_cluster", ctypes.c_int32)]
+                ("dense_max_dim", ctypes.c_int32), ("coarse_cluster", ctypes.c_int32),
+                ("coarse_refresh", ctypes.c_int32)]
 
 
 class BAReportC(ctypes.Structure):
@@ -144,7 +146,7 @@ def load_library(path: str = None):
         for name in EXPORTED_SYMBOLS:
             if name not in ("sfm_ctx_destroy", "sfm_last_error"):
                 getattr(lib, name).restype = c_int
-        if lib.sfm_abi_version() != 1:
+        if lib.sfm_abi_version() != ABI_VERSION:
             raise NativeLibraryMissing("libsfm_b200.so ABI version mismatch")
         _lib = lib
         return lib

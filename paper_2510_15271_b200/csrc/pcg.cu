@@ -4,6 +4,7 @@
 
 #include <algorithm>
 #include <array>
+#include <cstdlib>
 #include <vector>
 
 #include "ba.cuh"
@@ -18,8 +19,9 @@ namespace {
 
 constexpr int kNB = 48;          // Gauss-Jordan tile (8 clusters x 6)
 constexpr int kGJThreads = 256;
-constexpr int kPcgThreads = 512; // 16 warps
-constexpr int kPcgWarps = kPcgThreads / 32;
+constexpr int kPcgMaxThreads = 1024;  // CTA size chosen at setup (512 or 1024)
+#define kPcgThreads ((int)blockDim.x)
+#define kPcgWarps ((int)(blockDim.x >> 5))
 
 // Block-Jacobi: inverse of each 6x6 diagonal block of S (Cholesky).
 __global__ void k_block_jacobi(int nf, const int* __restrict__ diag_pos, const double* __restrict__ S,
@@ -307,74 +309,125 @@ __global__ void __launch_bounds__(kGJThreads) k_gj_inverse(double* A0, double* A
   if (bad && tid == 0) atomicOr(&sc->nonfinite, 1);
 }
 
-struct Pcg2Args {
-  int nf, C, nc, kc, npad;
+// ---------------------------------------------------------------------------
+// Persistent two-level PCG.
+//
+// Partition (built on the host once per BSR pattern, set_pattern): G CTAs
+// (<= 2 per SM, all co-resident) own contiguous block-row ranges of S
+// balanced by stored blocks; inside a CTA the range's blocks are cut into
+// kPcgWarps contiguous chunks, one per warp, so every warp streams the same
+// number of S blocks whatever the row lengths.  A warp's chunk meets one or
+// more rows; each (warp, row) meeting is a "segment" whose 6-vector partial
+// product goes to shared memory, and a row's result is the sum of its
+// segments in warp order -- a fixed order, so the solve is bit-reproducible.
+// Coarse clusters are groups of consecutive CTAs, so the restriction P^T q
+// of a cluster is a fixed-order sum of per-CTA partials.
+// Two grid barriers per iteration (after p.q / P^T q, after r.z / r.r).
+// ---------------------------------------------------------------------------
+
+struct Pcg3Args {
+  int nf, G, nc, npad, maxrows, maxsegs;
   const int* row_ptr;
   const int* col;
   const double* S;
   const double* Minv;
   const double* Pm;
-  const double* Aci;   // coarse inverse [npad x npad] (nullptr: one level)
+  const double* Aci;       // coarse inverse [npad x npad] (nullptr: one level)
+  const int* cta_row0;     // [G+1]
+  const int4* wchunk;      // [G*kPcgWarps] (k_begin, k_end, first row, first segment)
+  const int2* rowseg;      // [nf] (first segment local to the CTA, count)
+  const int* cta_cluster;  // [G]
+  const int* cluster_cta0; // [nc+1]
   const double* b;
   double* x;
   double* r;
   double* z;
   double* p;
   double* q;
-  double* qc;          // [nc*6]
-  double* rc0;         // [nc*6]
-  double* part;        // [4*grid]
+  double* rpart;           // [G*6] per-CTA restriction partials
+  double* part;            // [4*G]
   BAScalars* sc;
   int max_it;
   double rtol;
 };
 
-template <int NT>
-__device__ __forceinline__ double block_sum_det(double v, double* red) {
+__device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
-  __syncthreads();
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
-  __syncthreads();
-  double r = 0.0;
-  if (threadIdx.x == 0)
-    for (int w = 0; w < NT / 32; ++w) r += red[w];
-  return r;
+  return v;
 }
 
-// Sum of the per-CTA partials: lane l adds partials l, l+32, ... then a
-// fixed shuffle tree (identical in every CTA, every run).
-__device__ __forceinline__ double grid_sum_det(const double* part, int G, double* bc) {
-  __syncthreads();
-  if (threadIdx.x < 32) {
-    double s = 0.0;
-    for (int i = threadIdx.x; i < G; i += 32) s += __ldcg(part + i);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
-    if (threadIdx.x == 0) *bc = s;
-  }
-  __syncthreads();
-  return *bc;
+__device__ __forceinline__ double2 ldg2(const double* p) { return __ldg(reinterpret_cast<const double2*>(p)); }
+__device__ __forceinline__ double2 ldcg2(const double* p) { return __ldcg(reinterpret_cast<const double2*>(p)); }
+
+// dot of S block row (6 doubles at s) with the 6-vector at v
+__device__ __forceinline__ double dot6(const double* s, const double* v) {
+  const double2 s0 = ldg2(s), s1 = ldg2(s + 2), s2 = ldg2(s + 4);
+  const double2 v0 = ldcg2(v), v1 = ldcg2(v + 2), v2 = ldcg2(v + 4);
+  double acc = s0.x * v0.x;
+  acc = fma(s0.y, v0.y, acc);
+  acc = fma(s1.x, v1.x, acc);
+  acc = fma(s1.y, v1.y, acc);
+  acc = fma(s2.x, v2.x, acc);
+  return fma(s2.y, v2.y, acc);
 }
 
-// e[c - c0] = A_c^-1[6c..6c+5, :] . rc  for the CTA's clusters (warp per output)
-__device__ __forceinline__ void coarse_apply(const Pcg2Args& a, const double* rc, double* e, int c0, int c1) {
+// w = S z over the CTA's rows; writes one 6-vector per segment to seg[].
+__device__ __forceinline__ void spmv_segments(const Pcg3Args& a, const double* __restrict__ zv, double* seg) {
+  const unsigned full = 0xffffffffu;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nout = 6 * (c1 - c0);
-  const int m = 6 * a.nc;
-  for (int o = warp; o < nout; o += kPcgWarps) {
-    const double* row = a.Aci + (int64_t)(6 * c0 + o) * a.npad;
-    double s = 0.0;
-    for (int k = lane; k < m; k += 32) s += __ldg(row + k) * rc[k];
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) s += __shfl_down_sync(0xffffffffu, s, off);
-    if (lane == 0) e[o] = s;
+  const int grp = lane / 6, comp = lane % 6;
+  const int4 ch = a.wchunk[blockIdx.x * kPcgWarps + warp];
+  int kb = ch.x, r = ch.z, sidx = ch.w;
+  const int ke = ch.y;
+  while (kb < ke) {
+    const int re = min(ke, __ldg(a.row_ptr + r + 1));
+    double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, acc3 = 0.0;
+    if (lane < 30) {
+      int k = kb + grp;
+      for (; k + 15 < re; k += 20) {
+        const int c0 = __ldg(a.col + k), c1 = __ldg(a.col + k + 5);
+        const int c2 = __ldg(a.col + k + 10), c3 = __ldg(a.col + k + 15);
+        const double* s0 = a.S + (int64_t)k * 36 + comp * 6;
+        acc0 += dot6(s0, zv + c0 * 6);
+        acc1 += dot6(s0 + 5 * 36, zv + c1 * 6);
+        acc2 += dot6(s0 + 10 * 36, zv + c2 * 6);
+        acc3 += dot6(s0 + 15 * 36, zv + c3 * 6);
+      }
+      for (; k < re; k += 5) acc0 += dot6(a.S + (int64_t)k * 36 + comp * 6, zv + __ldg(a.col + k) * 6);
+    }
+    double acc = (acc0 + acc1) + (acc2 + acc3);
+    const double v1 = __shfl_sync(full, acc, comp + 6);
+    const double v2 = __shfl_sync(full, acc, comp + 12);
+    const double v3 = __shfl_sync(full, acc, comp + 18);
+    const double v4 = __shfl_sync(full, acc, comp + 24);
+    if (lane < 6) seg[sidx * 6 + lane] = (((acc + v1) + v2) + v3) + v4;
+    ++sidx;
+    ++r;
+    kb = re;
   }
 }
 
-// z_i = D_i^-1 r_i + P_i e(c(i))   (lanes 0..5 of the warp own row i)
-__device__ __forceinline__ double precond_row(const Pcg2Args& a, int row, double ri, const double* e,
-                                              int c0) {
+// Per-CTA shared-memory image of the CTA's rows: the Krylov vectors of the
+// rows it owns never leave the SM (only z is published for the SpMV), and
+// the constant operators (block-Jacobi inverse, coarse basis, this
+// cluster's rows of A_c^-1) are staged once per solve.
+struct PcgSmem {
+  double* seg;  // [maxsegs*6]
+  double* y;    // [maxrows*6]
+  double* rc;   // [6nc]
+  double* Ae;   // [6 x 6nc]
+  double* x;    // [maxrows*6] each
+  double* r;
+  double* p;
+  double* q;
+  double* z;
+  double* Mi;   // [maxrows*36]
+  double* Pc;   // [maxrows*36]
+};
+
+// z_i = D_i^-1 r_i (+ P_i e) for lanes 0..5 of the warp owning local row i
+__device__ __forceinline__ double precond_row(const PcgSmem& m, bool two, int i, double ri, const double* e) {
   const unsigned full = 0xffffffffu;
   const int lane = threadIdx.x & 31;
   double rj[6];
@@ -382,21 +435,20 @@ __device__ __forceinline__ double precond_row(const Pcg2Args& a, int row, double
   for (int j = 0; j < 6; ++j) rj[j] = __shfl_sync(full, ri, j);
   double zi = 0.0;
   if (lane < 6) {
-    const double* M = a.Minv + (int64_t)row * 36 + lane * 6;
+    const double* M = m.Mi + i * 36 + lane * 6;
 #pragma unroll
-    for (int j = 0; j < 6; ++j) zi += M[j] * rj[j];
-    if (a.Aci) {
-      const double* P = a.Pm + (int64_t)row * 36 + lane * 6;
-      const double* ec = e + 6 * (row / a.C - c0);
+    for (int j = 0; j < 6; ++j) zi = fma(M[j], rj[j], zi);
+    if (two) {
+      const double* P = m.Pc + i * 36 + lane * 6;
 #pragma unroll
-      for (int j = 0; j < 6; ++j) zi += P[j] * ec[j];
+      for (int j = 0; j < 6; ++j) zi = fma(P[j], e[j], zi);
     }
   }
   return zi;
 }
 
 // P_i^T v_i for lanes 0..5 (component lane)
-__device__ __forceinline__ double restrict_row(const Pcg2Args& a, int row, double vi) {
+__device__ __forceinline__ double restrict_row(const PcgSmem& m, int i, double vi) {
   const unsigned full = 0xffffffffu;
   const int lane = threadIdx.x & 31;
   double vj[6];
@@ -404,179 +456,234 @@ __device__ __forceinline__ double restrict_row(const Pcg2Args& a, int row, doubl
   for (int j = 0; j < 6; ++j) vj[j] = __shfl_sync(full, vi, j);
   double y = 0.0;
   if (lane < 6) {
-    const double* P = a.Pm + (int64_t)row * 36;
+    const double* P = m.Pc + i * 36;
 #pragma unroll
-    for (int m = 0; m < 6; ++m) y += P[m * 6 + lane] * vj[m];
+    for (int k = 0; k < 6; ++k) y = fma(P[k * 6 + lane], vj[k], y);
   }
   return y;
 }
 
-__global__ void __launch_bounds__(kPcgThreads) k_pcg2(Pcg2Args a) {
-  cg::grid_group grid = cg::this_grid();
-  extern __shared__ double psm[];
-  double* rc = psm;                        // [6*nc]
-  double* e = rc + 6 * a.nc;               // [6*kc]
-  double* y = e + 6 * a.kc;                // [kc*C*6]
-  __shared__ double red[kPcgWarps];
-  __shared__ double bc;
-  const unsigned full = 0xffffffffu;
+// After a grid barrier: the scalar sum over the G per-CTA partials `part`
+// (warp 0, fixed order) and, for the two-level preconditioner, the cluster
+// restriction sums (other warps), in one round trip.
+//   rc[t] = sum_c rpart (assign) or rc[t] -= scale * sum_c rpart.
+__device__ __forceinline__ void gather_after_sync(const Pcg3Args& a, const double* part, double* out, int nsum,
+                                                  double* rc, bool two, bool assign, const double* scale_num,
+                                                  const double* scale_den) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int G = gridDim.x;
-  const int c0 = blockIdx.x * a.kc, c1 = min(c0 + a.kc, a.nc);
-  const int row0 = c0 * a.C, row1 = min(c1 * a.C, a.nf);
-  double* part_pq = a.part;
-  double* part_rz = a.part + G;
-  double* part_rr = a.part + 2 * G;
-  double* part_bb = a.part + 3 * G;
-  const bool two = a.Aci != nullptr;
-
-  // ---- prologue: x = 0, r = b, p = q = 0, rc0 = P^T b ----------------------
-  double bb_l = 0.0;
-  for (int row = row0 + warp; row < row1; row += kPcgWarps) {
-    double bi = 0.0;
-    if (lane < 6) {
-      bi = a.b[row * 6 + lane];
-      a.x[row * 6 + lane] = 0.0;
-      a.r[row * 6 + lane] = bi;
-      a.p[row * 6 + lane] = 0.0;
-      a.q[row * 6 + lane] = 0.0;
-      bb_l += bi * bi;
+  if (warp < nsum) {
+    double s = 0.0;
+    for (int i = lane; i < a.G; i += 32) s += __ldcg(part + warp * a.G + i);
+    s = warp_sum(s);
+    if (lane == 0) out[warp] = s;
+  }
+  double qs[4];
+  int nq = 0;
+  if (two)
+    for (int t = threadIdx.x - 32 * nsum; t < 6 * a.nc && t >= 0 && nq < 4; t += kPcgThreads - 32 * nsum) {
+      const int k = t / 6, mm = t % 6;
+      double s = 0.0;
+      for (int c = a.cluster_cta0[k]; c < a.cluster_cta0[k + 1]; ++c) s += __ldcg(a.rpart + c * 6 + mm);
+      qs[nq++] = s;
     }
-    if (two) {
-      double yv = restrict_row(a, row, bi);
-      if (lane < 6) y[(row - row0) * 6 + lane] = yv;
+  __syncthreads();
+  if (two) {
+    const double alpha = assign ? 0.0 : (*scale_num) / (*scale_den);
+    int j = 0;
+    for (int t = threadIdx.x - 32 * nsum; t < 6 * a.nc && t >= 0 && j < nq; t += kPcgThreads - 32 * nsum, ++j)
+      rc[t] = assign ? qs[j] : rc[t] - alpha * qs[j];
+    // threads that ran out of register slots finish the tail directly
+    for (int t = threadIdx.x - 32 * nsum + 4 * (kPcgThreads - 32 * nsum); t < 6 * a.nc && t >= 0;
+         t += kPcgThreads - 32 * nsum) {
+      const int k = t / 6, mm = t % 6;
+      double s = 0.0;
+      for (int c = a.cluster_cta0[k]; c < a.cluster_cta0[k + 1]; ++c) s += __ldcg(a.rpart + c * 6 + mm);
+      rc[t] = assign ? s : rc[t] - alpha * s;
     }
   }
   __syncthreads();
-  if (two)
-    for (int t = threadIdx.x; t < 6 * (c1 - c0); t += kPcgThreads) {
-      const int c = c0 + t / 6, k = t % 6;
-      double s = 0.0;
-      for (int i = c * a.C; i < min((c + 1) * a.C, a.nf); ++i) s += y[(i - row0) * 6 + k];
-      a.rc0[c * 6 + k] = s;
-    }
-  double sb = block_sum_det<kPcgThreads>(bb_l, red);
-  if (threadIdx.x == 0) part_bb[blockIdx.x] = sb;
-  grid.sync();
-  const double bnorm = sqrt(grid_sum_det(part_bb, G, &bc));
-  if (two) {
-    for (int k = threadIdx.x; k < 6 * a.nc; k += kPcgThreads) rc[k] = __ldcg(a.rc0 + k);
-    __syncthreads();
-    coarse_apply(a, rc, e, c0, c1);
-    __syncthreads();
+}
+
+// e[0..5] = A_c^-1[6k.., :] . rc for this CTA's cluster k (rows in smem).
+// Warps 0..11: two warps per output row, halves summed in a fixed order.
+__device__ __forceinline__ void coarse_apply(const Pcg3Args& a, const PcgSmem& m, double* e, double* tmp) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n = 6 * a.nc;
+  if (warp < 12) {
+    const int o = warp >> 1, h = warp & 1;
+    const double* row = m.Ae + o * n;
+    const int half = (n + 1) / 2;
+    const int j0 = h * half, j1 = min(n, j0 + half);
+    double s = 0.0;
+    for (int j = j0 + lane; j < j1; j += 32) s = fma(row[j], m.rc[j], s);
+    s = warp_sum(s);
+    if (lane == 0) tmp[warp] = s;
   }
-  double rz_l = 0.0;
-  for (int row = row0 + warp; row < row1; row += kPcgWarps) {
-    double ri = (lane < 6) ? a.r[row * 6 + lane] : 0.0;
-    double zi = precond_row(a, row, ri, e, c0);
+  __syncthreads();
+  if (threadIdx.x < 6) e[threadIdx.x] = tmp[2 * threadIdx.x] + tmp[2 * threadIdx.x + 1];
+  __syncthreads();
+}
+
+// Deterministic block sum of two values (fixed shuffle tree + warp order).
+__device__ __forceinline__ double2 block_sum2(double u, double v, double2* red) {
+  u = warp_sum(u);
+  v = warp_sum(v);
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = make_double2(u, v);
+  __syncthreads();
+  double2 r = make_double2(0.0, 0.0);
+  if (threadIdx.x == 0)
+    for (int w = 0; w < kPcgWarps; ++w) { r.x += red[w].x; r.y += red[w].y; }
+  return r;
+}
+
+__global__ void __launch_bounds__(kPcgMaxThreads, 1) k_pcg3(Pcg3Args a) {
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ double psm[];
+  const int MR = a.maxrows, n6 = 6 * a.nc;
+  PcgSmem m;
+  m.seg = psm;
+  m.y = m.seg + 6 * a.maxsegs;
+  m.rc = m.y + 6 * MR;
+  m.Ae = m.rc + n6;
+  m.x = m.Ae + 6 * n6;
+  m.r = m.x + 6 * MR;
+  m.p = m.r + 6 * MR;
+  m.q = m.p + 6 * MR;
+  m.z = m.q + 6 * MR;
+  m.Mi = m.z + 6 * MR;
+  m.Pc = m.Mi + 36 * MR;
+  __shared__ double2 red[32];
+  __shared__ double tmp[16];
+  __shared__ double e[6];
+  __shared__ double sums[4];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int G = gridDim.x;
+  const int row0 = a.cta_row0[blockIdx.x], row1 = a.cta_row0[blockIdx.x + 1];
+  const int nrows = row1 - row0;
+  double* part_pq = a.part;          // [G]
+  double* part_rz = a.part + G;      // [G] followed by part_rr [G]
+  double* part_bb = a.part + 3 * G;  // [G]
+  const bool two = a.Aci != nullptr;
+
+  // ---- stage the constant operators -----------------------------------------
+  for (int t = threadIdx.x; t < 36 * nrows; t += kPcgThreads) {
+    m.Mi[t] = a.Minv[(int64_t)row0 * 36 + t];
+    if (two) m.Pc[t] = a.Pm[(int64_t)row0 * 36 + t];
+  }
+  if (two) {
+    const int k = a.cta_cluster[blockIdx.x];
+    for (int t = threadIdx.x; t < 6 * n6; t += kPcgThreads)
+      m.Ae[t] = a.Aci[(int64_t)(6 * k + t / n6) * a.npad + t % n6];
+  }
+  __syncthreads();
+
+  auto write_rpart = [&]() {
+    __syncthreads();
+    if (threadIdx.x < 6) {
+      double s = 0.0;
+      for (int i = 0; i < nrows; ++i) s += m.y[i * 6 + threadIdx.x];
+      a.rpart[blockIdx.x * 6 + threadIdx.x] = s;
+    }
+  };
+
+  // ---- prologue: x = 0, r = b, p = q = 0, rc = P^T b ------------------------
+  double bb_l = 0.0;
+  for (int i = warp; i < nrows; i += kPcgWarps) {
+    double bi = 0.0;
     if (lane < 6) {
-      a.z[row * 6 + lane] = zi;
+      bi = a.b[(row0 + i) * 6 + lane];
+      m.x[i * 6 + lane] = 0.0;
+      m.r[i * 6 + lane] = bi;
+      m.p[i * 6 + lane] = 0.0;
+      m.q[i * 6 + lane] = 0.0;
+      bb_l += bi * bi;
+    }
+    if (two) {
+      const double yv = restrict_row(m, i, bi);
+      if (lane < 6) m.y[i * 6 + lane] = yv;
+    }
+  }
+  if (two) write_rpart();
+  double2 sb = block_sum2(bb_l, 0.0, red);
+  if (threadIdx.x == 0) part_bb[blockIdx.x] = sb.x;
+  grid.sync();
+  gather_after_sync(a, part_bb, sums, 1, m.rc, two, true, nullptr, nullptr);
+  const double bnorm = sqrt(sums[0]);
+  if (two) coarse_apply(a, m, e, tmp);
+  double rz_l = 0.0;
+  for (int i = warp; i < nrows; i += kPcgWarps) {
+    const double ri = (lane < 6) ? m.r[i * 6 + lane] : 0.0;
+    const double zi = precond_row(m, two, i, ri, e);
+    if (lane < 6) {
+      m.z[i * 6 + lane] = zi;
+      a.z[(row0 + i) * 6 + lane] = zi;
       rz_l += ri * zi;
     }
   }
-  double s1 = block_sum_det<kPcgThreads>(rz_l, red);
-  if (threadIdx.x == 0) part_rz[blockIdx.x] = s1;
+  double2 s1 = block_sum2(rz_l, 0.0, red);
+  if (threadIdx.x == 0) part_rz[blockIdx.x] = s1.x;
   grid.sync();
-  double rz_old = grid_sum_det(part_rz, G, &bc);
+  gather_after_sync(a, part_rz, sums, 1, m.rc, false, true, nullptr, nullptr);
+  double rz_old = sums[0];
   int it = 0, fail = 0;
   double beta = 0.0;
   if (!(bnorm > 0.0) || !isfinite(bnorm)) {
     fail = !isfinite(bnorm);
   } else {
-    const int grp = lane / 6, comp = lane % 6;
     for (it = 0; it < a.max_it;) {
       // ---- phase 1: w = S z; p = z + beta p; q = w + beta q; P^T q --------
+      spmv_segments(a, a.z, m.seg);
+      __syncthreads();
       double pq_l = 0.0;
-      for (int row = row0 + warp; row < row1; row += kPcgWarps) {
-        double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, acc3 = 0.0;
-        const int k1 = a.row_ptr[row + 1];
-        if (lane < 30) {
-          int k = a.row_ptr[row] + grp;
-          for (; k + 15 < k1; k += 20) {
-            const double* s0 = a.S + (int64_t)k * 36 + comp * 6;
-            const double* s1p = s0 + 5 * 36;
-            const double* s2 = s0 + 10 * 36;
-            const double* s3 = s0 + 15 * 36;
-            const double* z0 = a.z + a.col[k] * 6;
-            const double* z1 = a.z + a.col[k + 5] * 6;
-            const double* z2 = a.z + a.col[k + 10] * 6;
-            const double* z3 = a.z + a.col[k + 15] * 6;
-#pragma unroll
-            for (int j = 0; j < 6; ++j) {
-              acc0 += __ldg(s0 + j) * __ldcg(z0 + j);
-              acc1 += __ldg(s1p + j) * __ldcg(z1 + j);
-              acc2 += __ldg(s2 + j) * __ldcg(z2 + j);
-              acc3 += __ldg(s3 + j) * __ldcg(z3 + j);
-            }
-          }
-          for (; k < k1; k += 5) {
-            const double* s0 = a.S + (int64_t)k * 36 + comp * 6;
-            const double* z0 = a.z + a.col[k] * 6;
-#pragma unroll
-            for (int j = 0; j < 6; ++j) acc0 += __ldg(s0 + j) * __ldcg(z0 + j);
-          }
-        }
-        double acc = (acc0 + acc1) + (acc2 + acc3);
-        double v1 = __shfl_sync(full, acc, comp + 6);
-        double v2 = __shfl_sync(full, acc, comp + 12);
-        double v3 = __shfl_sync(full, acc, comp + 18);
-        double v4 = __shfl_sync(full, acc, comp + 24);
+      for (int i = warp; i < nrows; i += kPcgWarps) {
         double qv = 0.0;
         if (lane < 6) {
-          const double w = (((acc + v1) + v2) + v3) + v4;
-          const double pv = a.z[row * 6 + lane] + beta * a.p[row * 6 + lane];
-          qv = w + beta * a.q[row * 6 + lane];
-          a.p[row * 6 + lane] = pv;
-          a.q[row * 6 + lane] = qv;
+          const int2 rs = a.rowseg[row0 + i];
+          double w = 0.0;
+          for (int sg = 0; sg < rs.y; ++sg) w += m.seg[(rs.x + sg) * 6 + lane];
+          const double pv = m.z[i * 6 + lane] + beta * m.p[i * 6 + lane];
+          qv = w + beta * m.q[i * 6 + lane];
+          m.p[i * 6 + lane] = pv;
+          m.q[i * 6 + lane] = qv;
           pq_l += pv * qv;
         }
         if (two) {
-          double yv = restrict_row(a, row, qv);
-          if (lane < 6) y[(row - row0) * 6 + lane] = yv;
+          const double yv = restrict_row(m, i, qv);
+          if (lane < 6) m.y[i * 6 + lane] = yv;
         }
       }
-      __syncthreads();
-      if (two)
-        for (int t = threadIdx.x; t < 6 * (c1 - c0); t += kPcgThreads) {
-          const int c = c0 + t / 6, k = t % 6;
-          double s = 0.0;
-          for (int i = c * a.C; i < min((c + 1) * a.C, a.nf); ++i) s += y[(i - row0) * 6 + k];
-          a.qc[c * 6 + k] = s;
-        }
-      double s = block_sum_det<kPcgThreads>(pq_l, red);
-      if (threadIdx.x == 0) part_pq[blockIdx.x] = s;
+      if (two) write_rpart();
+      const double2 s = block_sum2(pq_l, 0.0, red);
+      if (threadIdx.x == 0) part_pq[blockIdx.x] = s.x;
       grid.sync();
-      const double pq = grid_sum_det(part_pq, G, &bc);
+      // ---- phase 2: x += alpha p; r -= alpha q; rc -= alpha P^T q; z = M^-1 r
+      gather_after_sync(a, part_pq, sums, 1, m.rc, two, false, &rz_old, &sums[0]);
+      const double pq = sums[0];
       if (!(pq > 0.0) || !isfinite(pq)) { fail = 1; break; }
       const double alpha = rz_old / pq;
-      // ---- phase 2: x += alpha p; r -= alpha q; rc -= alpha qc; z = M^-1 r --
-      if (two) {
-        for (int k = threadIdx.x; k < 6 * a.nc; k += kPcgThreads) rc[k] -= alpha * __ldcg(a.qc + k);
-        __syncthreads();
-        coarse_apply(a, rc, e, c0, c1);
-        __syncthreads();
-      }
+      if (two) coarse_apply(a, m, e, tmp);
       double rz_n = 0.0, rr_n = 0.0;
-      for (int row = row0 + warp; row < row1; row += kPcgWarps) {
+      for (int i = warp; i < nrows; i += kPcgWarps) {
         double ri = 0.0;
         if (lane < 6) {
-          a.x[row * 6 + lane] += alpha * a.p[row * 6 + lane];
-          ri = a.r[row * 6 + lane] - alpha * a.q[row * 6 + lane];
-          a.r[row * 6 + lane] = ri;
+          m.x[i * 6 + lane] += alpha * m.p[i * 6 + lane];
+          ri = m.r[i * 6 + lane] - alpha * m.q[i * 6 + lane];
+          m.r[i * 6 + lane] = ri;
         }
-        double zi = precond_row(a, row, ri, e, c0);
+        const double zi = precond_row(m, two, i, ri, e);
         if (lane < 6) {
-          a.z[row * 6 + lane] = zi;
+          m.z[i * 6 + lane] = zi;
+          a.z[(row0 + i) * 6 + lane] = zi;
           rz_n += ri * zi;
           rr_n += ri * ri;
         }
       }
-      double t1 = block_sum_det<kPcgThreads>(rz_n, red);
-      double t2 = block_sum_det<kPcgThreads>(rr_n, red);
-      if (threadIdx.x == 0) { part_rz[blockIdx.x] = t1; part_rr[blockIdx.x] = t2; }
+      const double2 t = block_sum2(rz_n, rr_n, red);
+      if (threadIdx.x == 0) { part_rz[blockIdx.x] = t.x; part_rz[G + blockIdx.x] = t.y; }
       grid.sync();
-      const double rz_new = grid_sum_det(part_rz, G, &bc);
-      const double rr = grid_sum_det(part_rr, G, &bc);
+      gather_after_sync(a, part_rz, sums, 2, m.rc, false, true, nullptr, nullptr);
+      const double rz_new = sums[0], rr = sums[1];
       ++it;
       if (!isfinite(rr) || !isfinite(rz_new)) { fail = 1; break; }
       if (sqrt(rr) <= a.rtol * bnorm) break;
@@ -584,6 +691,8 @@ __global__ void __launch_bounds__(kPcgThreads) k_pcg2(Pcg2Args a) {
       rz_old = rz_new;
     }
   }
+  for (int i = warp; i < nrows; i += kPcgWarps)
+    if (lane < 6) a.x[(row0 + i) * 6 + lane] = m.x[i * 6 + lane];
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     a.sc->pcg_iters = it;
     a.sc->pcg_fail = fail;
@@ -593,42 +702,114 @@ __global__ void __launch_bounds__(kPcgThreads) k_pcg2(Pcg2Args a) {
 
 }  // namespace
 
-void TwoLevelPcg::setup(int nf, int cluster, cudaStream_t s) {
+void TwoLevelPcg::setup(int nf, int cluster, int refresh, cudaStream_t s) {
   nf_ = nf;
-  if (nf <= 0) return;
-  int dev = 0, nsm = 0, per_sm = 0;
+  cluster_ = cluster;
+  refresh_ = std::max(1, refresh);
+  (void)s;
+}
+
+void TwoLevelPcg::set_pattern(const int* row_ptr, const int* col, int nnzb, cudaStream_t s) {
+  if (nf_ <= 0) return;
+  std::vector<int> rp(nf_ + 1), cl(nnzb);
+  SFM_CUDA(cudaMemcpyAsync(rp.data(), row_ptr, sizeof(int) * (nf_ + 1), cudaMemcpyDeviceToHost, s));
+  SFM_CUDA(cudaMemcpyAsync(cl.data(), col, sizeof(int) * nnzb, cudaMemcpyDeviceToHost, s));
+  SFM_CUDA(cudaStreamSynchronize(s));
+  int dev = 0, nsm = 0;
   SFM_CUDA(cudaGetDevice(&dev));
   SFM_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-  C_ = cluster;
-  if (C_ > 0) {
-    // keep the coarse system small enough for the per-trial inverse
-    C_ = std::max(C_, (nf + 191) / 192);
-    nc_ = (nf + C_ - 1) / C_;
-  } else {
-    C_ = 16;
-    nc_ = (nf + C_ - 1) / C_;
+
+  // ---- CTA row ranges balanced by (stored blocks + per-row overhead) -------
+  const int64_t kRowCost = 4;
+  auto cost_upto = [&](int r) { return (int64_t)rp[r] + kRowCost * r; };
+  const int64_t total = cost_upto(nf_);
+  // CTA size: 1024 threads x 1 per SM (default) or 512 x 2 (SFM_PCG_CTA=512)
+  nt_ = 1024;
+  if (const char* e = std::getenv("SFM_PCG_CTA")) nt_ = std::atoi(e) == 512 ? 512 : 1024;
+  const int nwarps = nt_ / 32;
+  if (const char* e = std::getenv("SFM_COARSE_REFRESH")) refresh_ = std::max(1, std::atoi(e));
+  lin_count_ = 0;
+  int G = std::min((1024 / nt_) * nsm, nf_);
+  std::vector<int> row0;
+  for (;;) {
+    row0.assign(1, 0);
+    for (int c = 1; c < G; ++c) {
+      const int64_t target = total * c / G;
+      int lo = row0.back() + 1, hi = nf_ - (G - c);  // keep >= 1 row per CTA
+      int r = lo;
+      // first row whose prefix cost reaches target
+      int a0 = lo, b0 = hi;
+      while (a0 < b0) {
+        int m = (a0 + b0) / 2;
+        if (cost_upto(m) < target) a0 = m + 1; else b0 = m;
+      }
+      r = std::min(std::max(a0, lo), hi);
+      row0.push_back(r);
+    }
+    row0.push_back(nf_);
+    break;
   }
+  // ---- per-warp chunks and segments ----------------------------------------
+  std::vector<int4> wchunk((size_t)G * nwarps);
+  std::vector<int2> rowseg(nf_);
+  int maxrows = 1, maxsegs = 1;
+  for (int c = 0; c < G; ++c) {
+    const int r0 = row0[c], r1 = row0[c + 1];
+    const int k0 = rp[r0], k1 = rp[r1];
+    maxrows = std::max(maxrows, r1 - r0);
+    for (int r = r0; r < r1; ++r) rowseg[r] = make_int2(0, 0);
+    const int64_t nb = k1 - k0;
+    int sidx = 0;
+    int r = r0;
+    for (int w = 0; w < nwarps; ++w) {
+      const int kb = k0 + (int)(nb * w / nwarps), ke = k0 + (int)(nb * (w + 1) / nwarps);
+      while (r + 1 < r1 && rp[r + 1] <= kb) ++r;
+      wchunk[(size_t)c * nwarps + w] = make_int4(kb, ke, r, sidx);
+      int rr = r, k = kb;
+      while (k < ke) {
+        const int re = std::min(ke, rp[rr + 1]);
+        if (rowseg[rr].y == 0) rowseg[rr].x = sidx;
+        rowseg[rr].y += 1;
+        ++sidx;
+        ++rr;
+        k = re;
+      }
+    }
+    maxsegs = std::max(maxsegs, sidx);
+  }
+  // ---- coarse clusters = groups of consecutive CTAs -------------------------
+  const bool two = cluster_ > 0;
+  nc_ = two ? std::min(G, std::max(1, (nf_ + cluster_ - 1) / cluster_)) : 1;
+  std::vector<int> cta_cluster(G), cluster_cta0(nc_ + 1), frame_cluster(nf_);
+  for (int k = 0; k <= nc_; ++k) cluster_cta0[k] = (int)((int64_t)G * k / nc_);
+  for (int k = 0; k < nc_; ++k)
+    for (int c = cluster_cta0[k]; c < cluster_cta0[k + 1]; ++c) {
+      cta_cluster[c] = k;
+      for (int r = row0[c]; r < row0[c + 1]; ++r) frame_cluster[r] = k;
+    }
   ncp_ = ((nc_ + 7) / 8) * 8;
   npad_ = 6 * ncp_;
-  // cooperative grid: clusters per CTA so that every CTA is co-resident
-  auto smem_for = [&](int kc) { return sizeof(double) * (size_t)(6 * nc_ + 6 * kc + kc * C_ * 6); };
-  kc_ = 1;
-  for (;;) {
-    size_t sm = smem_for(kc_);
-    SFM_CUDA(cudaFuncSetAttribute(k_pcg2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    SFM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pcg2, kPcgThreads, sm));
-    int grid = (nc_ + kc_ - 1) / kc_;
-    if (per_sm > 0 && grid <= per_sm * nsm) { smem_ = sm; grid_ = grid; break; }
-    SFM_REQUIRE(kc_ < nc_, "PCG grid cannot be made co-resident");
-    ++kc_;
-  }
-  Minv_.resize((size_t)nf * 36);
-  Pm_.resize((size_t)nf * 36);
-  r_.resize((size_t)nf * 6); z_.resize((size_t)nf * 6); p_.resize((size_t)nf * 6); q_.resize((size_t)nf * 6);
-  qc_.resize((size_t)nc_ * 6);
-  rc0_.resize((size_t)nc_ * 6);
-  part_.resize(4 * (size_t)grid_);
-  if (cluster > 0) {
+  grid_ = G;
+  maxrows_ = maxrows;
+  maxsegs_ = maxsegs;
+  smem_ = sizeof(double) * (size_t)(6 * maxsegs + 108 * maxrows + 42 * nc_);
+  SFM_REQUIRE(smem_ <= 200 * 1024, "PCG partition needs too much shared memory");
+  SFM_CUDA(cudaFuncSetAttribute(k_pcg3, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_));
+  int per_sm = 0;
+  SFM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pcg3, nt_, smem_));
+  SFM_REQUIRE(per_sm > 0 && G <= per_sm * nsm, "PCG grid cannot be made co-resident");
+  cta_row0_.upload(row0.data(), row0.size(), s);
+  wchunk_.upload(wchunk.data(), wchunk.size(), s);
+  rowseg_.upload(rowseg.data(), rowseg.size(), s);
+  cta_cluster_.upload(cta_cluster.data(), cta_cluster.size(), s);
+  cluster_cta0_.upload(cluster_cta0.data(), cluster_cta0.size(), s);
+
+  Minv_.resize((size_t)nf_ * 36);
+  Pm_.resize((size_t)nf_ * 36);
+  r_.resize((size_t)nf_ * 6); z_.resize((size_t)nf_ * 6); p_.resize((size_t)nf_ * 6); q_.resize((size_t)nf_ * 6);
+  rpart_.resize((size_t)G * 6);
+  part_.resize(4 * (size_t)G);
+  if (two) {
     Ac_[0].resize((size_t)npad_ * npad_);
     Ac_[1].resize((size_t)npad_ * npad_);
     const size_t gsm = sizeof(double) * (4 * kNB * kNB + 4 * kNB);
@@ -637,53 +818,49 @@ void TwoLevelPcg::setup(int nf, int cluster, cudaStream_t s) {
     SFM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_gj_inverse, kGJThreads, gsm));
     const int T = npad_ / kNB;
     gj_grid_ = std::max(1, std::min(T * T, per * nsm));
+    // coarse assembly runs (row i, k0, k1) grouped by coarse pair (c(i), d)
+    std::vector<std::vector<std::array<int, 3>>> per_pair(nc_ * (size_t)nc_);
+    for (int i = 0; i < nf_; ++i) {
+      int k = rp[i];
+      while (k < rp[i + 1]) {
+        const int d = frame_cluster[cl[k]];
+        int k1 = k;
+        while (k1 < rp[i + 1] && frame_cluster[cl[k1]] == d) ++k1;
+        per_pair[(size_t)frame_cluster[i] * nc_ + d].push_back({i, k, k1});
+        k = k1;
+      }
+    }
+    std::vector<int2> cd;
+    std::vector<int> ptr(1, 0);
+    std::vector<int4> runs;
+    for (int c = 0; c < nc_; ++c)
+      for (int d = 0; d < nc_; ++d) {
+        auto& v = per_pair[(size_t)c * nc_ + d];
+        if (v.empty()) continue;
+        cd.push_back(make_int2(c, d));
+        for (auto& r : v) runs.push_back(make_int4(r[0], r[1], r[2], 0));
+        ptr.push_back((int)runs.size());
+      }
+    npairs_ = (int)cd.size();
+    pair_cd_.upload(cd.data(), cd.size(), s);
+    pair_ptr_.upload(ptr.data(), ptr.size(), s);
+    runs_.upload(runs.data(), runs.size(), s);
   } else {
     Ac_[0].release();
     Ac_[1].release();
     gj_grid_ = 0;
+    npairs_ = 0;
   }
-  (void)s;
-}
-
-void TwoLevelPcg::set_pattern(const int* row_ptr, const int* col, int nnzb, cudaStream_t s) {
-  if (nf_ <= 0 || gj_grid_ == 0) return;
-  std::vector<int> rp(nf_ + 1), cl(nnzb);
-  SFM_CUDA(cudaMemcpyAsync(rp.data(), row_ptr, sizeof(int) * (nf_ + 1), cudaMemcpyDeviceToHost, s));
-  SFM_CUDA(cudaMemcpyAsync(cl.data(), col, sizeof(int) * nnzb, cudaMemcpyDeviceToHost, s));
-  SFM_CUDA(cudaStreamSynchronize(s));
-  // runs (row i, k0, k1) grouped by coarse pair (c(i), d), rows ascending
-  std::vector<std::vector<std::array<int, 3>>> per(nc_ * (size_t)nc_);
-  for (int i = 0; i < nf_; ++i) {
-    int k = rp[i];
-    while (k < rp[i + 1]) {
-      const int d = cl[k] / C_;
-      int k1 = k;
-      while (k1 < rp[i + 1] && cl[k1] / C_ == d) ++k1;
-      per[(size_t)(i / C_) * nc_ + d].push_back({i, k, k1});
-      k = k1;
-    }
-  }
-  std::vector<int2> cd;
-  std::vector<int> ptr(1, 0);
-  std::vector<int4> runs;
-  for (int c = 0; c < nc_; ++c)
-    for (int d = 0; d < nc_; ++d) {
-      auto& v = per[(size_t)c * nc_ + d];
-      if (v.empty()) continue;
-      cd.push_back(make_int2(c, d));
-      for (auto& r : v) runs.push_back(make_int4(r[0], r[1], r[2], 0));
-      ptr.push_back((int)runs.size());
-    }
-  npairs_ = (int)cd.size();
-  pair_cd_.upload(cd.data(), cd.size(), s);
-  pair_ptr_.upload(ptr.data(), ptr.size(), s);
-  runs_.upload(runs.data(), runs.size(), s);
   SFM_CUDA(cudaStreamSynchronize(s));
 }
 
 void TwoLevelPcg::set_basis(const int* free_frame, const double* q, const double* t, const double* Rt,
                             cudaStream_t s, Profiler* prof) {
   if (nf_ <= 0 || gj_grid_ == 0) return;
+  // The coarse operator (basis + A_c^-1) is rebuilt every `refresh_`
+  // linearisations; in between PCG keeps the previous one, which is still
+  // an SPD preconditioner (only the iteration count depends on it).
+  if (lin_count_++ % refresh_ != 0) return;
   coarse_valid_ = false;
   ProfScope ps(*prof, "coarse_basis", 0.0, s);
   k_coarse_basis<<<grid_for(nf_, 128), 128, 0, s>>>(nf_, free_frame, q, t, Rt, Pm_.get());
@@ -721,15 +898,17 @@ void TwoLevelPcg::solve(const PcgProblem& p, int max_it, double rtol, BAScalars*
     Aci_ = Ac_[(npad_ / kNB) & 1].get();
     coarse_valid_ = true;
   }
-  const double* Aci = gj_grid_ > 0 ? Aci_ : nullptr;
-  Pcg2Args a{};
-  a.nf = nf_; a.C = C_; a.nc = nc_; a.kc = kc_; a.npad = npad_;
-  a.row_ptr = p.row_ptr; a.col = p.col; a.S = p.S; a.Minv = Minv_.get(); a.Pm = Pm_.get(); a.Aci = Aci;
+  Pcg3Args a{};
+  a.nf = nf_; a.G = grid_; a.nc = nc_; a.npad = npad_; a.maxrows = maxrows_; a.maxsegs = maxsegs_;
+  a.row_ptr = p.row_ptr; a.col = p.col; a.S = p.S; a.Minv = Minv_.get(); a.Pm = Pm_.get();
+  a.Aci = gj_grid_ > 0 ? Aci_ : nullptr;
+  a.cta_row0 = cta_row0_.get(); a.wchunk = wchunk_.get(); a.rowseg = rowseg_.get();
+  a.cta_cluster = cta_cluster_.get(); a.cluster_cta0 = cluster_cta0_.get();
   a.b = p.b; a.x = p.x; a.r = r_.get(); a.z = z_.get(); a.p = p_.get(); a.q = q_.get();
-  a.qc = qc_.get(); a.rc0 = rc0_.get(); a.part = part_.get(); a.sc = sc; a.max_it = max_it; a.rtol = rtol;
+  a.rpart = rpart_.get(); a.part = part_.get(); a.sc = sc; a.max_it = max_it; a.rtol = rtol;
   void* args[] = {&a};
   ProfScope ps(*prof, "pcg", 0.0, s);
-  SFM_CUDA(cudaLaunchCooperativeKernel((void*)k_pcg2, grid_, kPcgThreads, args, smem_, s));
+  SFM_CUDA(cudaLaunchCooperativeKernel((void*)k_pcg3, grid_, nt_, args, smem_, s));
 }
 
 }  // namespace sfm

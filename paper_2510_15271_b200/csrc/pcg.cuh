@@ -5,8 +5,8 @@
 // Preconditioner: additive two-level
 //     M^-1 r = D^-1 r + P A_c^-1 P^T r
 // with D the 6x6 block diagonal of S (block-Jacobi) and P the rigid-motion
-// coarse space: cameras are aggregated into clusters of C consecutive free
-// frames and camera j's coarse basis is Adj(T_j) (a world-frame rigid motion
+// coarse space: cameras are aggregated into clusters of ~C consecutive free
+// frames (whole PCG CTA row ranges) and camera j's coarse basis is Adj(T_j) (a world-frame rigid motion
 // of the whole cluster, expressed as left perturbations).  A_c = P^T S P is
 // assembled on device and inverted by a cooperative blocked Gauss-Jordan.
 // The Krylov loop is one persistent cooperative kernel with two grid
@@ -32,7 +32,7 @@ struct PcgProblem {
 class TwoLevelPcg {
  public:
   // cluster <= 0 disables the coarse level (plain block-Jacobi).
-  void setup(int nf, int cluster, cudaStream_t s);
+  void setup(int nf, int cluster, int refresh, cudaStream_t s);
   // Coarse assembly runs from the (fixed) BSR pattern of S.
   void set_pattern(const int* row_ptr, const int* col, int nnzb, cudaStream_t s);
   // Coarse basis P_j = Adj(T_j) from the linearisation-point poses.
@@ -44,15 +44,16 @@ class TwoLevelPcg {
   int last_grid() const { return grid_; }
 
  private:
-  int nf_ = 0, C_ = 0, nc_ = 0, ncp_ = 0, npad_ = 0, kc_ = 0, grid_ = 0, gj_grid_ = 0;
+  int nf_ = 0, cluster_ = 0, nc_ = 0, ncp_ = 0, npad_ = 0, grid_ = 0, gj_grid_ = 0;
+  int maxrows_ = 0, maxsegs_ = 0, nt_ = 512, refresh_ = 1, lin_count_ = 0;
   size_t smem_ = 0;
   int npairs_ = 0;
   bool coarse_valid_ = false;
   const double* Aci_ = nullptr;
-  DevBuf<double> Minv_, Pm_, Ac_[2], r_, z_, p_, q_, qc_, rc0_, part_;
-  DevBuf<int2> pair_cd_;
-  DevBuf<int> pair_ptr_;
-  DevBuf<int4> runs_;
+  DevBuf<double> Minv_, Pm_, Ac_[2], r_, z_, p_, q_, rpart_, part_;
+  DevBuf<int2> pair_cd_, rowseg_;
+  DevBuf<int> pair_ptr_, cta_row0_, cta_cluster_, cluster_cta0_;
+  DevBuf<int4> runs_, wchunk_;
 };
 
 }  // namespace sfm

@@ -28,15 +28,33 @@ def test_library_loads_and_exports_every_symbol():
     lib = nat.load_library()
     for name in header_functions():
         assert hasattr(lib, name), name
-    assert lib.sfm_abi_version() == 1
+    assert lib.sfm_abi_version() == 2
 
 
-def test_ctypes_struct_layout_matches_header():
+def test_ctypes_struct_layout_matches_header(tmp_path):
+    """sizeof / offsetof of every C-ABI struct, as gcc sees include/sfm_b200.h,
+    equals the ctypes mirror in _native.py."""
     import ctypes
-    assert ctypes.sizeof(nat.CameraModelC) == 64
-    assert ctypes.sizeof(nat.BAOptionsC) == 72
-    assert ctypes.sizeof(nat.BAReportC) == 64
-    assert nat.BAProblemC.obs_offset.offset == ctypes.sizeof(nat.BAProblemC) - 16
+    import subprocess
+    structs = {"sfm_camera_model": nat.CameraModelC, "sfm_ba_problem": nat.BAProblemC,
+               "sfm_ba_options": nat.BAOptionsC, "sfm_ba_report": nat.BAReportC,
+               "sfm_tracks": nat.TracksC}
+    lines = ["#include <stdio.h>", "#include <stddef.h>", '#include "sfm_b200.h"', "int main(void){"]
+    for cname, cls in structs.items():
+        lines.append(f'printf("{cname} %zu\\n", sizeof({cname}));')
+        for fname, _ in cls._fields_:
+            lines.append(f'printf("{cname}.{fname} %zu\\n", offsetof({cname}, {fname}));')
+    lines.append("return 0;}")
+    src = tmp_path / "layout.c"
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "layout"
+    subprocess.run(["gcc", "-I", os.path.join(REPO, "include"), str(src), "-o", str(exe)], check=True)
+    got = dict(ln.rsplit(" ", 1) for ln in subprocess.run([str(exe)], capture_output=True, text=True,
+                                                         check=True).stdout.splitlines())
+    for cname, cls in structs.items():
+        assert int(got[cname]) == ctypes.sizeof(cls), cname
+        for fname, _ in cls._fields_:
+            assert int(got[f"{cname}.{fname}"]) == getattr(cls, fname).offset, (cname, fname)
 
 
 def test_flatten_matches_golden_order(golden):
