@@ -590,17 +590,33 @@ __global__ void __launch_bounds__(kBlock) k_point_lin(PointArgs a, double* __res
   if ((threadIdx.x & 31) == 0) atomicMax(&a.sc->gmax, m);
 }
 
-constexpr int kBlkWarps = 4;
+
+// fp64 tensor-core step D += A(8x4) B(4x8) (DMMA.8x8x4).  Fragments:
+// a = A[lane/4][lane%4], b = B[lane%4][lane/4], d = D[lane/4][2(lane%4)+{0,1}].
+__device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
 
 // One warp per off-diagonal S block (lo < hi), blocks in row-major order so
 // consecutive warps share cameras and points (L2 reuse).  The block's pairs
 // (observation a in camera lo, b in camera hi of the same point, sorted by
-// point) are taken 32 at a time, one per lane; each lane writes
-// -J~c_a^T (J~p_a V*^-1 J~p_b^T) J~c_b to a shared-memory row and lane l sums
-// column l over the rows -- fixed order, no partial buffers in HBM.  The
-// lambda_c edge block is added on rank 0 and both BSR triangles written.
-__global__ void __launch_bounds__(kBlkWarps * 32) k_offdiag_blocks(BlkArgs a) {
-  __shared__ double Tsm[kBlkWarps][32][37];
+// point) are taken 32 at a time, one per lane.  Each pair's contribution is
+// the rank-2 product -J~c_a^T (M J~c_b), M = J~p_a V*^-1 J~p_b^T (2x2), so
+// the block is S_ab = A^T B with A = [J~c_a] and B = [-M J~c_b] stacked over
+// pairs (K = 2 x pairs): lanes stage their 2x6 factors in shared memory and
+// the warp contracts them on the fp64 tensor cores (two pairs per
+// DMMA.8x8x4, fixed order, so the sum is bit-reproducible).  The lambda_c
+// edge block is added on rank 0 and both BSR triangles written.
+constexpr int kOffWarps = 4;
+constexpr int kOffLd = 13;  // padded row of the staged factors (bank spread)
+
+__global__ void __launch_bounds__(kOffWarps * 32, 5) k_offdiag_blocks(BlkArgs a) {
+  __shared__ double Ast[kOffWarps][32 * kOffLd];
+  __shared__ double Bst[kOffWarps][32 * kOffLd];
+  __shared__ Mat3 Rsm[kOffWarps][2];
+  __shared__ sfm_camera_model Csm[kOffWarps][2];
   const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (w >= a.n) return;
@@ -608,27 +624,43 @@ __global__ void __launch_bounds__(kBlkWarps * 32) k_offdiag_blocks(BlkArgs a) {
   const unsigned long long key = a.ub_key[u];
   const int lo = (int)(key / a.nf), hi = (int)(key % a.nf);
   const int pb = a.ub_pb[u];
-  double acc0 = 0.0, acc1 = 0.0;
+  double d0 = 0.0, d1 = 0.0, e0 = 0.0, e1 = 0.0;
+  const int fr = lane >> 2;          // fragment row (A) / column (B)
+  const int fk = lane & 3;           // fragment k: pair (fk >> 1), component (fk & 1)
   if (pb >= 0) {
+    // warp-uniform cameras staged in shared memory (keeps registers for
+    // the per-pair factors)
     const int fa = a.free_frame[lo], fb = a.free_frame[hi];
-    Mat3 Ra, Rb; Vec3 ta, tb;
-    load_cam(a.Rt, fa, Ra, ta);
-    load_cam(a.Rt, fb, Rb, tb);
-    const sfm_camera_model ca = a.models[a.frame_model[fa]];
-    const sfm_camera_model cb = a.models[a.frame_model[fb]];
+    if (lane < 9) {
+      Rsm[warp][0].m[lane] = __ldg(a.Rt + (int64_t)fa * 12 + lane);
+      Rsm[warp][1].m[lane] = __ldg(a.Rt + (int64_t)fb * 12 + lane);
+    }
+    if (lane == 0) {
+      Csm[warp][0] = a.models[a.frame_model[fa]];
+      Csm[warp][1] = a.models[a.frame_model[fb]];
+    }
+    __syncwarp();
+    const Mat3& Ra = Rsm[warp][0];
+    const Mat3& Rb = Rsm[warp][1];
+    const sfm_camera_model& ca = Csm[warp][0];
+    const sfm_camera_model& cb = Csm[warp][1];
     const int64_t k0 = a.pb_pair_ptr[pb], k1 = a.pb_pair_ptr[pb + 1];
-    double* row = &Tsm[warp][lane][0];
+    double* As = &Ast[warp][lane * kOffLd];
+    double* Bs = &Bst[warp][lane * kOffLd];
     for (int64_t kb = k0; kb < k1; kb += 32) {
       const int64_t k = kb + lane;
-      const int nv = (int)min((int64_t)32, k1 - kb);
       if (k < k1) {
         const unsigned long long pr = a.pairs[k];
         const int64_t oa = (int64_t)(pr >> 32), ob = (int64_t)(uint32_t)pr;
         const double* pv = a.pv + (int64_t)a.pair_pt[k] * 12;
-        double Jca[12], Jpa[6], Jcb[12], Jpb[6];
-        geo_jacobians(ca, Ra, a.geo[oa], Jca, Jpa);
-        geo_jacobians(cb, Rb, a.geo[ob], Jcb, Jpb);
+        const double4 ga = a.geo[oa], gb = a.geo[ob];
         const double v0 = pv[0], v1 = pv[1], v2 = pv[2], v3_ = pv[3], v4 = pv[4], v5 = pv[5];
+        double Jca[12], Jpa[6];
+        geo_jacobians(ca, Ra, ga, Jca, Jpa);
+#pragma unroll
+        for (int i = 0; i < 12; ++i) As[i] = Jca[i];
+        double Jcb[12], Jpb[6];
+        geo_jacobians(cb, Rb, gb, Jcb, Jpb);
         const double P00 = v0 * Jpb[0] + v1 * Jpb[1] + v2 * Jpb[2];
         const double P01 = v1 * Jpb[0] + v3_ * Jpb[1] + v4 * Jpb[2];
         const double P02 = v2 * Jpb[0] + v4 * Jpb[1] + v5 * Jpb[2];
@@ -639,36 +671,49 @@ __global__ void __launch_bounds__(kBlkWarps * 32) k_offdiag_blocks(BlkArgs a) {
         const double m01 = Jpa[0] * P10 + Jpa[1] * P11 + Jpa[2] * P12;
         const double m10 = Jpa[3] * P00 + Jpa[4] * P01 + Jpa[5] * P02;
         const double m11 = Jpa[3] * P10 + Jpa[4] * P11 + Jpa[5] * P12;
-        double MJ[12];
 #pragma unroll
         for (int c = 0; c < 6; ++c) {
-          MJ[c] = m00 * Jcb[c] + m01 * Jcb[6 + c];
-          MJ[6 + c] = m10 * Jcb[c] + m11 * Jcb[6 + c];
+          Bs[c] = -(m00 * Jcb[c] + m01 * Jcb[6 + c]);
+          Bs[6 + c] = -(m10 * Jcb[c] + m11 * Jcb[6 + c]);
         }
+      } else {
 #pragma unroll
-        for (int r = 0; r < 6; ++r)
-#pragma unroll
-          for (int c = 0; c < 6; ++c) row[r * 6 + c] = -(Jca[r] * MJ[c] + Jca[6 + r] * MJ[6 + c]);
+        for (int i = 0; i < 12; ++i) { As[i] = 0.0; Bs[i] = 0.0; }
       }
       __syncwarp();
-      for (int l = 0; l < nv; ++l) {
-        acc0 += Tsm[warp][l][lane];
-        if (lane < 4) acc1 += Tsm[warp][l][32 + lane];
+      const int nch = (int)((min((int64_t)32, k1 - kb) + 1) >> 1);
+      const int slot = (fk & 1) * 6 + fr;
+      for (int ch = 0; ch < nch; ch += 2) {
+        const int p0 = 2 * ch + (fk >> 1);
+        const double a0 = fr < 6 ? Ast[warp][p0 * kOffLd + slot] : 0.0;
+        const double b0 = fr < 6 ? Bst[warp][p0 * kOffLd + slot] : 0.0;
+        dmma_8x8x4(d0, d1, a0, b0);
+        if (ch + 1 < nch) {
+          const int p1 = p0 + 2;
+          const double a1 = fr < 6 ? Ast[warp][p1 * kOffLd + slot] : 0.0;
+          const double b1 = fr < 6 ? Bst[warp][p1 * kOffLd + slot] : 0.0;
+          dmma_8x8x4(e0, e1, a1, b1);
+        }
       }
       __syncwarp();
     }
   }
-  if (a.rank == 0 && a.ub_edge[u] >= 0) {
-    const double* H = a.edge_H + (int64_t)a.ub_edge[u] * 36;
-    acc0 += H[lane];
-    if (lane < 4) acc1 += H[32 + lane];
+  d0 += e0;
+  d1 += e1;
+  const int c0 = 2 * fk;
+  if (fr < 6 && c0 < 6) {
+    if (a.rank == 0 && a.ub_edge[u] >= 0) {
+      const double* H = a.edge_H + (int64_t)a.ub_edge[u] * 36;
+      d0 += H[fr * 6 + c0];
+      d1 += H[fr * 6 + c0 + 1];
+    }
+    double* up = a.S + (int64_t)a.pos_up[u] * 36;
+    up[fr * 6 + c0] = d0;
+    up[fr * 6 + c0 + 1] = d1;
+    double* dn = a.S + (int64_t)a.pos_lo[u] * 36;
+    dn[c0 * 6 + fr] = d0;
+    dn[(c0 + 1) * 6 + fr] = d1;
   }
-  double* up = a.S + (int64_t)a.pos_up[u] * 36;
-  up[lane] = acc0;
-  if (lane < 4) up[32 + lane] = acc1;
-  double* dn = a.S + (int64_t)a.pos_lo[u] * 36;
-  dn[(lane % 6) * 6 + lane / 6] = acc0;
-  if (lane < 4) dn[((32 + lane) % 6) * 6 + (32 + lane) / 6] = acc1;
 }
 
 constexpr int kCamWarps = 4;
@@ -1664,7 +1709,7 @@ void BASolver::build_schur(double lam) {
     // observation records, point V*^-1 once; both triangles of S out
     ProfScope ps(*prof_, "schur_offdiag",
                  12.0 * (n_pairs_ - n_cm_) + 32.0 * N_ + 48.0 * P_ + 288.0 * (n_full_ - nfree_), s);
-    k_offdiag_blocks<<<grid_for((int64_t)n_off_ * 32, kBlkWarps * 32), kBlkWarps * 32, 0, s>>>(ba);
+    k_offdiag_blocks<<<grid_for((int64_t)n_off_ * 32, kOffWarps * 32), kOffWarps * 32, 0, s>>>(ba);
   }
   if (comm_ && comm_->active()) {
     comm_->sum(S_.get(), (size_t)n_full_ * 36, s);
