@@ -84,6 +84,35 @@ constexpr int kBlock = 128;
 // small helpers
 // ---------------------------------------------------------------------------
 
+// 256-bit read-only load (LDG.E.ENL2.256 on sm_100a): one L1 wavefront per
+// 32-byte record instead of four 64-bit loads.  p must be 32-byte aligned and
+// not written during the kernel.
+__device__ __forceinline__ double4 ldg256(const void* p) {
+  double4 v;
+  asm("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(v.x), "=d"(v.y), "=d"(v.z), "=d"(v.w) : "l"(p));
+  return v;
+}
+
+// Camera record R (row-major) | t: 96 bytes = three 256-bit loads.
+__device__ __forceinline__ void load_cam256(const double* __restrict__ Rt, int f, Mat3& R, Vec3& t) {
+  const double* p = Rt + (int64_t)f * 12;
+  const double4 a = ldg256(p), b = ldg256(p + 4), c = ldg256(p + 8);
+  R.m[0] = a.x; R.m[1] = a.y; R.m[2] = a.z; R.m[3] = a.w;
+  R.m[4] = b.x; R.m[5] = b.y; R.m[6] = b.z; R.m[7] = b.w;
+  R.m[8] = c.x; t = v3(c.y, c.z, c.w);
+}
+
+// Camera models staged in shared memory when the table is small (the usual
+// case is one model for the whole map).
+constexpr int kSmemModels = 8;
+__device__ __forceinline__ const sfm_camera_model* stage_models(const sfm_camera_model* g, int n,
+                                                                 sfm_camera_model* sm) {
+  if (n > kSmemModels) return g;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) sm[i] = g[i];
+  __syncthreads();
+  return sm;
+}
+
 __device__ __forceinline__ void load_cam(const double* __restrict__ Rt, int f, Mat3& R, Vec3& t) {
   const double* p = Rt + (int64_t)f * 12;
 #pragma unroll
@@ -388,6 +417,7 @@ struct PointArgs {
   const double* uv;
   const int* frame_model;
   const sfm_camera_model* models;
+  int nmodels;
   const int* free_idx;
   const double* Rt;       // linearization state cameras
   const double* X;        // linearization state points
@@ -410,6 +440,8 @@ struct PointArgs {
 template <bool TRIAL>
 __global__ void __launch_bounds__(kBlock) k_point_cost(PointArgs a) {
   __shared__ double red[kBlock / 32];
+  __shared__ sfm_camera_model smod[kSmemModels];
+  const sfm_camera_model* models = stage_models(a.models, a.nmodels, smod);
   const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   double cost = 0.0, dp2 = 0.0;
   bool nonfinite = false;
@@ -424,10 +456,10 @@ __global__ void __launch_bounds__(kBlock) k_point_cost(PointArgs a) {
         const int j = a.free_idx[f];
         if (j < 0) continue;
         Mat3 R; Vec3 t;
-        load_cam(a.Rt, f, R, t);
-        const sfm_camera_model cm = a.models[a.frame_model[f]];
+        load_cam256(a.Rt, f, R, t);
+        const sfm_camera_model& cm = models[a.frame_model[f]];
         double Jc[12], Jp[6];
-        geo_jacobians(cm, R, a.geo[o], Jc, Jp);
+        geo_jacobians(cm, R, ldg256(a.geo + o), Jc, Jp);
         const double* d = a.dc + (int64_t)j * 6;
         double y0 = 0.0, y1 = 0.0;
 #pragma unroll
@@ -436,11 +468,12 @@ __global__ void __launch_bounds__(kBlock) k_point_cost(PointArgs a) {
         acc1 += Jp[1] * y0 + Jp[4] * y1;
         acc2 += Jp[2] * y0 + Jp[5] * y1;
       }
-      const double* Vi = a.pv + p * 12;  // xx xy xz yy yz zz | e
-      const double* ei = Vi + 6;
-      double d0 = -ei[0] - (Vi[0] * acc0 + Vi[1] * acc1 + Vi[2] * acc2);
-      double d1 = -ei[1] - (Vi[1] * acc0 + Vi[3] * acc1 + Vi[4] * acc2);
-      double d2 = -ei[2] - (Vi[2] * acc0 + Vi[4] * acc1 + Vi[5] * acc2);
+      // packed point record: V*^-1 (xx xy xz yy yz zz) | e | pad
+      const double4 pa = ldg256(a.pv + p * 12), pb = ldg256(a.pv + p * 12 + 4);
+      const double e0 = pb.z, e1 = pb.w, e2 = __ldg(a.pv + p * 12 + 8);
+      double d0 = -e0 - (pa.x * acc0 + pa.y * acc1 + pa.z * acc2);
+      double d1 = -e1 - (pa.y * acc0 + pa.w * acc1 + pb.x * acc2);
+      double d2 = -e2 - (pa.z * acc0 + pb.x * acc1 + pb.y * acc2);
       if (!(isfinite(d0) && isfinite(d1) && isfinite(d2))) nonfinite = true;
       dp2 = d0 * d0 + d1 * d1 + d2 * d2;
       X = v3(X.x + d0, X.y + d1, X.z + d2);
@@ -452,8 +485,8 @@ __global__ void __launch_bounds__(kBlock) k_point_cost(PointArgs a) {
       for (int64_t o = b0; o < b1; ++o) {
         const int f = a.of[o];
         Mat3 R; Vec3 t;
-        load_cam(a.Rt_eval, f, R, t);
-        const sfm_camera_model cm = a.models[a.frame_model[f]];
+        load_cam256(a.Rt_eval, f, R, t);
+        const sfm_camera_model& cm = models[a.frame_model[f]];
         Vec3 pc = add(mul(R, X), t);
         double u, v;
         if (project_point(cm, pc, u, v) != PROJ_OK) {
@@ -542,6 +575,8 @@ __global__ void k_finalize(const double* __restrict__ pa, int na, const double* 
 // V_i = sum Jp^T Jp, g_i = sum Jp^T r over ALL observations of the point.
 __global__ void __launch_bounds__(kBlock) k_point_lin(PointArgs a, double* __restrict__ V,
                                                       double* __restrict__ gp) {
+  __shared__ sfm_camera_model smod[kSmemModels];
+  const sfm_camera_model* models = stage_models(a.models, a.nmodels, smod);
   const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   double gm = 0.0;
   if (p < a.P) {
@@ -551,8 +586,8 @@ __global__ void __launch_bounds__(kBlock) k_point_lin(PointArgs a, double* __res
     for (int64_t o = a.ptr[p]; o < a.ptr[p + 1]; ++o) {
       const int f = a.of[o];
       Mat3 R; Vec3 t;
-      load_cam(a.Rt, f, R, t);
-      const sfm_camera_model cm = a.models[a.frame_model[f]];
+      load_cam256(a.Rt, f, R, t);
+      const sfm_camera_model& cm = models[a.frame_model[f]];
       const double2 uv = reinterpret_cast<const double2*>(a.uv)[o];
       const Vec3 pc = add(mul(R, X), t);
       double u, vv;
@@ -653,8 +688,9 @@ __global__ void __launch_bounds__(kOffWarps * 32, 5) k_offdiag_blocks(BlkArgs a)
         const unsigned long long pr = a.pairs[k];
         const int64_t oa = (int64_t)(pr >> 32), ob = (int64_t)(uint32_t)pr;
         const double* pv = a.pv + (int64_t)a.pair_pt[k] * 12;
-        const double4 ga = a.geo[oa], gb = a.geo[ob];
-        const double v0 = pv[0], v1 = pv[1], v2 = pv[2], v3_ = pv[3], v4 = pv[4], v5 = pv[5];
+        const double4 ga = ldg256(a.geo + oa), gb = ldg256(a.geo + ob);
+        const double4 pva = ldg256(pv), pvb = ldg256(pv + 4);
+        const double v0 = pva.x, v1 = pva.y, v2 = pva.z, v3_ = pva.w, v4 = pvb.x, v5 = pvb.y;
         double Jca[12], Jpa[6];
         geo_jacobians(ca, Ra, ga, Jca, Jpa);
 #pragma unroll
@@ -744,7 +780,7 @@ __global__ void __launch_bounds__(kCamWarps * 32) k_cam_blocks(BlkArgs a) {
     const int64_t k = kb + lane;
     const int nv = (int)min((int64_t)32, k1 - kb);
     if (k < k1) {
-      const double4 g = a.geo_cm[k];
+      const double4 g = ldg256(a.geo_cm + k);
       double Jc[12], Jp[6];
       geo_jacobians(cm, R, g, Jc, Jp);
       if (MODE == 0) {
@@ -765,7 +801,9 @@ __global__ void __launch_bounds__(kCamWarps * 32) k_cam_blocks(BlkArgs a) {
         }
       } else {
         const double* pv = a.pv + (int64_t)a.cm_pt[k] * 12;
-        const double v0 = pv[0], v1 = pv[1], v2 = pv[2], v3_ = pv[3], v4 = pv[4], v5 = pv[5];
+        const double4 pva = ldg256(pv), pvb = ldg256(pv + 4);
+        const double v0 = pva.x, v1 = pva.y, v2 = pva.z, v3_ = pva.w, v4 = pvb.x, v5 = pvb.y;
+        const double pe0 = pvb.z, pe1 = pvb.w, pe2 = __ldg(pv + 8);
         const double P00 = v0 * Jp[0] + v1 * Jp[1] + v2 * Jp[2];
         const double P01 = v1 * Jp[0] + v3_ * Jp[1] + v4 * Jp[2];
         const double P02 = v2 * Jp[0] + v4 * Jp[1] + v5 * Jp[2];
@@ -789,8 +827,8 @@ __global__ void __launch_bounds__(kCamWarps * 32) k_cam_blocks(BlkArgs a) {
             row[r * 6 + c] = v;
             row[c * 6 + r] = v;
           }
-        const double y0 = Jp[0] * pv[6] + Jp[1] * pv[7] + Jp[2] * pv[8];
-        const double y1 = Jp[3] * pv[6] + Jp[4] * pv[7] + Jp[5] * pv[8];
+        const double y0 = Jp[0] * pe0 + Jp[1] * pe1 + Jp[2] * pe2;
+        const double y1 = Jp[3] * pe0 + Jp[4] * pe1 + Jp[5] * pe2;
 #pragma unroll
         for (int r = 0; r < 6; ++r) row[36 + r] = Jc[r] * y0 + Jc[6 + r] * y1;
       }
@@ -1592,7 +1630,8 @@ double BASolver::eval_cost_current() {
   PointArgs pa{};
   pa.P = P_; pa.lk = opt_.loss_kind; pa.lp = opt_.loss_param;
   pa.ptr = pt_ptr_.get(); pa.of = obs_frame_.get(); pa.uv = obs_uv_.get();
-  pa.frame_model = frame_model_.get(); pa.models = models_.get(); pa.free_idx = free_idx_.get();
+  pa.frame_model = frame_model_.get(); pa.models = models_.get(); pa.nmodels = nmodels_;
+  pa.free_idx = free_idx_.get();
   pa.Rt = Rt_[cur_].get(); pa.X = X_[cur_].get(); pa.Rt_eval = Rt_[cur_].get();
   pa.obs_offset = obs_offset_; pa.part_cost = part_a_.get(); pa.part_dp2 = part_b_.get(); pa.sc = sc_.get();
   const unsigned gp = grid_for(std::max<int64_t>(P_, 1), kBlock);
@@ -1626,7 +1665,8 @@ void BASolver::linearize() {
   PointArgs pa{};
   pa.P = P_; pa.lk = opt_.loss_kind; pa.lp = opt_.loss_param;
   pa.ptr = pt_ptr_.get(); pa.of = obs_frame_.get(); pa.uv = obs_uv_.get();
-  pa.frame_model = frame_model_.get(); pa.models = models_.get(); pa.free_idx = free_idx_.get();
+  pa.frame_model = frame_model_.get(); pa.models = models_.get(); pa.nmodels = nmodels_;
+  pa.free_idx = free_idx_.get();
   pa.Rt = Rt_[cur_].get(); pa.X = X_[cur_].get(); pa.sc = sc_.get(); pa.geo = geo_.get();
   pa.cm_pos = cm_pos_.get(); pa.geo_cm = geo_cm_.get();
   if (P_) {
@@ -1753,7 +1793,8 @@ bool BASolver::trial(double lam, double* new_cost, double* step_norm) {
   PointArgs pa{};
   pa.P = P_; pa.lk = opt_.loss_kind; pa.lp = opt_.loss_param;
   pa.ptr = pt_ptr_.get(); pa.of = obs_frame_.get(); pa.uv = obs_uv_.get();
-  pa.frame_model = frame_model_.get(); pa.models = models_.get(); pa.free_idx = free_idx_.get();
+  pa.frame_model = frame_model_.get(); pa.models = models_.get(); pa.nmodels = nmodels_;
+  pa.free_idx = free_idx_.get();
   pa.Rt = Rt_[cur_].get(); pa.X = X_[cur_].get(); pa.Rt_eval = Rt_[o].get(); pa.X_out = X_[o].get();
   pa.pv = pv_.get(); pa.dc = dc_.get(); pa.geo = geo_.get();
   pa.obs_offset = obs_offset_; pa.part_cost = part_a_.get(); pa.part_dp2 = part_b_.get(); pa.sc = sc_.get();
