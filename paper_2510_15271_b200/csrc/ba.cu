@@ -753,20 +753,23 @@ __global__ void __launch_bounds__(kOffWarps * 32, 5) k_offdiag_blocks(BlkArgs a)
 }
 
 constexpr int kCamWarps = 4;
+constexpr int kCamLd = 29;  // staged factors per observation: A (12) | B (16), padded
 
 // One CTA per free camera j over its observations in camera-major order
 // (contiguous linearisation records, point ids and pixels): the diagonal
-// S block and the camera half of the normal equations.  Warps take 32-
-// observation batches round-robin; each lane writes its contribution row to
-// shared memory, lane l sums column l over the rows, then the warp sums
-// are added in warp order -- a fixed order, independent of timing.
-//   MODE 0: U_j = sum J~c^T J~c, g_j = sum J~c^T r~              (linearise)
-//   MODE 1: S_jj = U*_j - sum J~c^T (J~p V*^-1 J~p^T) J~c,
-//           b_j = -g_j + sum J~c^T J~p e_i                        (each trial)
+// S block and the camera half of the normal equations.  Each observation
+// contributes a rank-2 term A^T B with A = J~c (2x6) and
+//   MODE 0: B = [J~c | r~ | 0]                U_j = sum J~c^T J~c, g_j = sum J~c^T r~
+//   MODE 1: B = [-M J~c | J~p e | 0],  M = J~p V*^-1 J~p^T
+//           S_jj = U*_j - sum J~c^T M J~c,  b_j = -g_j + sum J~c^T J~p e
+// so the camera's [6 x 8] result is one long K = 2 x observations
+// contraction: lanes stage their factors in shared memory, each warp runs
+// DMMA.8x8x4 over its 32-observation batches (two observations per step)
+// and the four warp results are added in warp order -- fixed order.
 template <int MODE>
-__global__ void __launch_bounds__(kCamWarps * 32) k_cam_blocks(BlkArgs a) {
-  __shared__ double Tsm[kCamWarps][32][43];
-  __shared__ double Wsum[kCamWarps][42];
+__global__ void __launch_bounds__(kCamWarps * 32, 5) k_cam_blocks(BlkArgs a) {
+  __shared__ double St[kCamWarps][32 * kCamLd];
+  __shared__ double Wsum[kCamWarps][64];
   const int j = blockIdx.x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int f = a.free_frame[j];
@@ -774,15 +777,18 @@ __global__ void __launch_bounds__(kCamWarps * 32) k_cam_blocks(BlkArgs a) {
   load_cam(a.Rt, f, R, t);
   const sfm_camera_model cm = a.models[a.frame_model[f]];
   const int64_t k0 = a.cm_ptr[j], k1 = a.cm_ptr[j + 1];
-  double acc0 = 0.0, acc1 = 0.0;
-  double* row = &Tsm[warp][lane][0];
+  double d0 = 0.0, d1 = 0.0, e0 = 0.0, e1 = 0.0;
+  double* As = &St[warp][lane * kCamLd];
+  double* Bs = As + 12;
+  const int fr = lane >> 2, fk = lane & 3;
   for (int64_t kb = k0 + (int64_t)warp * 32; kb < k1; kb += kCamWarps * 32) {
     const int64_t k = kb + lane;
-    const int nv = (int)min((int64_t)32, k1 - kb);
     if (k < k1) {
       const double4 g = ldg256(a.geo_cm + k);
       double Jc[12], Jp[6];
       geo_jacobians(cm, R, g, Jc, Jp);
+#pragma unroll
+      for (int i = 0; i < 12; ++i) As[i] = Jc[i];
       if (MODE == 0) {
         const double2 uv = reinterpret_cast<const double2*>(a.cm_uv)[k];
         double xd, yd;
@@ -790,15 +796,8 @@ __global__ void __launch_bounds__(kCamWarps * 32) k_cam_blocks(BlkArgs a) {
         const double r0 = g.w * (cm.fx * xd + cm.cx - uv.x);
         const double r1 = g.w * (cm.fy * yd + cm.cy - uv.y);
 #pragma unroll
-        for (int r = 0; r < 6; ++r) {
-#pragma unroll
-          for (int c = r; c < 6; ++c) {
-            const double v = Jc[r] * Jc[c] + Jc[6 + r] * Jc[6 + c];
-            row[r * 6 + c] = v;
-            row[c * 6 + r] = v;
-          }
-          row[36 + r] = Jc[r] * r0 + Jc[6 + r] * r1;
-        }
+        for (int c = 0; c < 6; ++c) { Bs[c] = Jc[c]; Bs[8 + c] = Jc[6 + c]; }
+        Bs[6] = r0; Bs[14] = r1;
       } else {
         const double* pv = a.pv + (int64_t)a.cm_pt[k] * 12;
         const double4 pva = ldg256(pv), pvb = ldg256(pv + 4);
@@ -813,42 +812,63 @@ __global__ void __launch_bounds__(kCamWarps * 32) k_cam_blocks(BlkArgs a) {
         const double m00 = Jp[0] * P00 + Jp[1] * P01 + Jp[2] * P02;
         const double m01 = Jp[0] * P10 + Jp[1] * P11 + Jp[2] * P12;
         const double m11 = Jp[3] * P10 + Jp[4] * P11 + Jp[5] * P12;
-        double MJ[12];
 #pragma unroll
         for (int c = 0; c < 6; ++c) {
-          MJ[c] = m00 * Jc[c] + m01 * Jc[6 + c];
-          MJ[6 + c] = m01 * Jc[c] + m11 * Jc[6 + c];
+          Bs[c] = -(m00 * Jc[c] + m01 * Jc[6 + c]);
+          Bs[8 + c] = -(m01 * Jc[c] + m11 * Jc[6 + c]);
         }
+        Bs[6] = Jp[0] * pe0 + Jp[1] * pe1 + Jp[2] * pe2;
+        Bs[14] = Jp[3] * pe0 + Jp[4] * pe1 + Jp[5] * pe2;
+      }
+      Bs[7] = 0.0;
+      Bs[15] = 0.0;
+    } else {
 #pragma unroll
-        for (int r = 0; r < 6; ++r)
-#pragma unroll
-          for (int c = r; c < 6; ++c) {
-            const double v = -(Jc[r] * MJ[c] + Jc[6 + r] * MJ[6 + c]);
-            row[r * 6 + c] = v;
-            row[c * 6 + r] = v;
-          }
-        const double y0 = Jp[0] * pe0 + Jp[1] * pe1 + Jp[2] * pe2;
-        const double y1 = Jp[3] * pe0 + Jp[4] * pe1 + Jp[5] * pe2;
-#pragma unroll
-        for (int r = 0; r < 6; ++r) row[36 + r] = Jc[r] * y0 + Jc[6 + r] * y1;
+      for (int i = 0; i < 28; ++i) As[i] = 0.0;
+    }
+    __syncwarp();
+    const int nch = (int)((min((int64_t)32, k1 - kb) + 1) >> 1);
+    const double* Sw = &St[warp][0];
+    const int comp = fk & 1;
+    for (int ch = 0; ch < nch; ch += 2) {
+      const int o0 = 2 * ch + (fk >> 1);
+      const double a0 = fr < 6 ? Sw[o0 * kCamLd + comp * 6 + fr] : 0.0;
+      const double b0 = Sw[o0 * kCamLd + 12 + comp * 8 + fr];
+      dmma_8x8x4(d0, d1, a0, b0);
+      if (ch + 1 < nch) {
+        const int o1 = o0 + 2;
+        const double a1 = fr < 6 ? Sw[o1 * kCamLd + comp * 6 + fr] : 0.0;
+        const double b1 = Sw[o1 * kCamLd + 12 + comp * 8 + fr];
+        dmma_8x8x4(e0, e1, a1, b1);
       }
     }
     __syncwarp();
-    for (int l = 0; l < nv; ++l) {
-      acc0 += Tsm[warp][l][lane];
-      if (lane < 10) acc1 += Tsm[warp][l][32 + lane];
-    }
-    __syncwarp();
   }
-  Wsum[warp][lane] = acc0;
-  if (lane < 10) Wsum[warp][32 + lane] = acc1;
+  // warp result C[fr][2fk + {0,1}] -> smem, then warp 0 adds the warps in order
+  Wsum[warp][fr * 8 + 2 * fk] = d0 + e0;
+  Wsum[warp][fr * 8 + 2 * fk + 1] = d1 + e1;
   __syncthreads();
   if (warp != 0) return;
-  double s0 = 0.0, s1 = 0.0;
+  // lane l < 36: block entry (l/6, l%6); lanes 36.. handled below via l2
+  const int r0 = lane / 6, c0 = lane % 6;
+  // MODE 1's -J~c^T M J~c is symmetric only up to rounding: average the two
+  // triangles so S stays exactly symmetric (MODE 0 is symmetric as computed)
+  auto ent = [&](int w, int r, int c) {
+    return MODE == 0 ? Wsum[w][r * 8 + c] : 0.5 * (Wsum[w][r * 8 + c] + Wsum[w][c * 8 + r]);
+  };
+  double s0 = 0.0;
 #pragma unroll
-  for (int w = 0; w < kCamWarps; ++w) {
-    s0 += Wsum[w][lane];
-    if (lane < 10) s1 += Wsum[w][32 + lane];
+  for (int w = 0; w < kCamWarps; ++w) s0 += ent(w, r0, c0);
+  // second value per lane: entries 32..35 of the block (lanes 0..3), the
+  // 6-vector column 6 (lanes 4..9)
+  double s1 = 0.0;
+  if (lane < 4) {
+    const int e = 32 + lane;
+#pragma unroll
+    for (int w = 0; w < kCamWarps; ++w) s1 += ent(w, e / 6, e % 6);
+  } else if (lane < 10) {
+#pragma unroll
+    for (int w = 0; w < kCamWarps; ++w) s1 += Wsum[w][(lane - 4) * 8 + 6];
   }
   if (MODE == 0) {
     a.Uout[(int64_t)j * 36 + lane] = s0;
