@@ -335,6 +335,12 @@ struct Pcg3Args {
   const double* Aci;       // coarse inverse [npad x npad] (nullptr: one level)
   const int* cta_row0;     // [G+1]
   const int4* wchunk;      // [G*kPcgWarps] (k_begin, k_end, first row, first segment)
+  const int2* wres;        // [G*kPcgWarps] (resident blocks at the chunk head, smem slot)
+  int resblocks;           // smem capacity for resident S blocks
+  const int* lcol;         // [nnzb] column of each block as an index into its CTA's z list
+  const int* zl_ptr;       // [G+1] per-CTA distinct columns
+  const int* zl;           // distinct frame ids, CTA by CTA
+  int maxblk, maxdist;     // per-CTA maxima (shared-memory sizing)
   const int2* rowseg;      // [nf] (first segment local to the CTA, count)
   const int* cta_cluster;  // [G]
   const int* cluster_cta0; // [nc+1]
@@ -360,10 +366,25 @@ __device__ __forceinline__ double warp_sum(double v) {
 __device__ __forceinline__ double2 ldg2(const double* p) { return __ldg(reinterpret_cast<const double2*>(p)); }
 __device__ __forceinline__ double2 ldcg2(const double* p) { return __ldcg(reinterpret_cast<const double2*>(p)); }
 
-// dot of S block row (6 doubles at s) with the 6-vector at v
-__device__ __forceinline__ double dot6(const double* s, const double* v) {
+__device__ __forceinline__ double dot6_sg(const double* s, const double* v) {  // S global, z smem
   const double2 s0 = ldg2(s), s1 = ldg2(s + 2), s2 = ldg2(s + 4);
-  const double2 v0 = ldcg2(v), v1 = ldcg2(v + 2), v2 = ldcg2(v + 4);
+  const double2 v0 = *reinterpret_cast<const double2*>(v);
+  const double2 v1 = *reinterpret_cast<const double2*>(v + 2);
+  const double2 v2 = *reinterpret_cast<const double2*>(v + 4);
+  double acc = s0.x * v0.x;
+  acc = fma(s0.y, v0.y, acc);
+  acc = fma(s1.x, v1.x, acc);
+  acc = fma(s1.y, v1.y, acc);
+  acc = fma(s2.x, v2.x, acc);
+  return fma(s2.y, v2.y, acc);
+}
+__device__ __forceinline__ double dot6_ss(const double* s, const double* v) {  // both smem
+  const double2 s0 = *reinterpret_cast<const double2*>(s);
+  const double2 s1 = *reinterpret_cast<const double2*>(s + 2);
+  const double2 s2 = *reinterpret_cast<const double2*>(s + 4);
+  const double2 v0 = *reinterpret_cast<const double2*>(v);
+  const double2 v1 = *reinterpret_cast<const double2*>(v + 2);
+  const double2 v2 = *reinterpret_cast<const double2*>(v + 4);
   double acc = s0.x * v0.x;
   acc = fma(s0.y, v0.y, acc);
   acc = fma(s1.x, v1.x, acc);
@@ -373,28 +394,46 @@ __device__ __forceinline__ double dot6(const double* s, const double* v) {
 }
 
 // w = S z over the CTA's rows; writes one 6-vector per segment to seg[].
-__device__ __forceinline__ void spmv_segments(const Pcg3Args& a, const double* __restrict__ zv, double* seg) {
+// z is read from the CTA's shared-memory z cache (zc, the distinct columns
+// of its rows, gathered once per iteration) through the block's local
+// column index (lc, staged once per solve), so the only global traffic in
+// the loop is the S stream itself: independent loads, no index -> z chain.
+// The head of every warp's chunk (wres.x blocks) is resident in shared
+// memory for the whole solve (Ssm).
+__device__ __forceinline__ void spmv_segments(const Pcg3Args& a, const double* zc, const int* lc, int kc0,
+                                              double* seg, const double* Ssm) {
   const unsigned full = 0xffffffffu;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int grp = lane / 6, comp = lane % 6;
   const int4 ch = a.wchunk[blockIdx.x * kPcgWarps + warp];
+  const int2 wr = a.wres[blockIdx.x * kPcgWarps + warp];
   int kb = ch.x, r = ch.z, sidx = ch.w;
   const int ke = ch.y;
+  const int kres = ch.x + wr.x;                    // first non-resident block
+  const double* Sres = Ssm + ((int64_t)wr.y - ch.x) * 36 + comp * 6;  // Sres + k*36 for resident k
+  const int* lcb = lc - kc0;                       // lcb[k] for global block k
   while (kb < ke) {
     const int re = min(ke, __ldg(a.row_ptr + r + 1));
     double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, acc3 = 0.0;
     if (lane < 30) {
       int k = kb + grp;
-      for (; k + 15 < re; k += 20) {
-        const int c0 = __ldg(a.col + k), c1 = __ldg(a.col + k + 5);
-        const int c2 = __ldg(a.col + k + 10), c3 = __ldg(a.col + k + 15);
-        const double* s0 = a.S + (int64_t)k * 36 + comp * 6;
-        acc0 += dot6(s0, zv + c0 * 6);
-        acc1 += dot6(s0 + 5 * 36, zv + c1 * 6);
-        acc2 += dot6(s0 + 10 * 36, zv + c2 * 6);
-        acc3 += dot6(s0 + 15 * 36, zv + c3 * 6);
+      const int rs = min(re, kres);
+      for (; k + 15 < rs; k += 20) {
+        const double* s0 = Sres + (int64_t)k * 36;
+        acc0 += dot6_ss(s0, zc + lcb[k] * 6);
+        acc1 += dot6_ss(s0 + 5 * 36, zc + lcb[k + 5] * 6);
+        acc2 += dot6_ss(s0 + 10 * 36, zc + lcb[k + 10] * 6);
+        acc3 += dot6_ss(s0 + 15 * 36, zc + lcb[k + 15] * 6);
       }
-      for (; k < re; k += 5) acc0 += dot6(a.S + (int64_t)k * 36 + comp * 6, zv + __ldg(a.col + k) * 6);
+      for (; k < rs; k += 5) acc0 += dot6_ss(Sres + (int64_t)k * 36, zc + lcb[k] * 6);
+      for (; k + 15 < re; k += 20) {
+        const double* s0 = a.S + (int64_t)k * 36 + comp * 6;
+        acc0 += dot6_sg(s0, zc + lcb[k] * 6);
+        acc1 += dot6_sg(s0 + 5 * 36, zc + lcb[k + 5] * 6);
+        acc2 += dot6_sg(s0 + 10 * 36, zc + lcb[k + 10] * 6);
+        acc3 += dot6_sg(s0 + 15 * 36, zc + lcb[k + 15] * 6);
+      }
+      for (; k < re; k += 5) acc0 += dot6_sg(a.S + (int64_t)k * 36 + comp * 6, zc + lcb[k] * 6);
     }
     double acc = (acc0 + acc1) + (acc2 + acc3);
     const double v1 = __shfl_sync(full, acc, comp + 6);
@@ -424,6 +463,9 @@ struct PcgSmem {
   double* z;
   double* Mi;   // [maxrows*36]
   double* Pc;   // [maxrows*36]
+  double* Ssm;  // [resblocks*36] resident S blocks
+  double* zc;   // [maxdist*6] z cache (distinct columns of the CTA's rows)
+  int* lc;      // [maxblk] local column index of each of the CTA's blocks
 };
 
 // z_i = D_i^-1 r_i (+ P_i e) for lanes 0..5 of the warp owning local row i
@@ -553,6 +595,9 @@ __global__ void __launch_bounds__(kPcgMaxThreads, 1) k_pcg3(Pcg3Args a) {
   m.z = m.q + 6 * MR;
   m.Mi = m.z + 6 * MR;
   m.Pc = m.Mi + 36 * MR;
+  m.Ssm = m.Pc + 36 * MR;
+  m.zc = m.Ssm + 36 * a.resblocks;
+  m.lc = reinterpret_cast<int*>(m.zc + 6 * a.maxdist);
   __shared__ double2 red[32];
   __shared__ double tmp[16];
   __shared__ double e[6];
@@ -561,6 +606,16 @@ __global__ void __launch_bounds__(kPcgMaxThreads, 1) k_pcg3(Pcg3Args a) {
   const int G = gridDim.x;
   const int row0 = a.cta_row0[blockIdx.x], row1 = a.cta_row0[blockIdx.x + 1];
   const int nrows = row1 - row0;
+  const int kc0 = __ldg(a.row_ptr + row0);
+  const int nblk = __ldg(a.row_ptr + row1) - kc0;
+  const int zl0 = a.zl_ptr[blockIdx.x], ndist = a.zl_ptr[blockIdx.x + 1] - zl0;
+  // z cache fill: 3 double2 per distinct column, straight from L2
+  auto fill_zc = [&]() {
+    for (int t = threadIdx.x; t < 3 * ndist; t += kPcgThreads) {
+      const int c = __ldg(a.zl + zl0 + t / 3);
+      reinterpret_cast<double2*>(m.zc)[t] = ldcg2(a.z + c * 6 + 2 * (t % 3));
+    }
+  };
   double* part_pq = a.part;          // [G]
   double* part_rz = a.part + G;      // [G] followed by part_rr [G]
   double* part_bb = a.part + 3 * G;  // [G]
@@ -575,6 +630,15 @@ __global__ void __launch_bounds__(kPcgMaxThreads, 1) k_pcg3(Pcg3Args a) {
     const int k = a.cta_cluster[blockIdx.x];
     for (int t = threadIdx.x; t < 6 * n6; t += kPcgThreads)
       m.Ae[t] = a.Aci[(int64_t)(6 * k + t / n6) * a.npad + t % n6];
+  }
+  for (int t = threadIdx.x; t < nblk; t += kPcgThreads) m.lc[t] = __ldg(a.lcol + kc0 + t);
+  // resident S blocks: the head of every warp's chunk (18 double2 per block)
+  for (int w = 0; w < kPcgWarps; ++w) {
+    const int4 ch = a.wchunk[blockIdx.x * kPcgWarps + w];
+    const int2 wr = a.wres[blockIdx.x * kPcgWarps + w];
+    const double2* src = reinterpret_cast<const double2*>(a.S + (int64_t)ch.x * 36);
+    double2* dst = reinterpret_cast<double2*>(m.Ssm + (int64_t)wr.y * 36);
+    for (int t = threadIdx.x; t < wr.x * 18; t += kPcgThreads) dst[t] = __ldg(src + t);
   }
   __syncthreads();
 
@@ -633,7 +697,9 @@ __global__ void __launch_bounds__(kPcgMaxThreads, 1) k_pcg3(Pcg3Args a) {
   } else {
     for (it = 0; it < a.max_it;) {
       // ---- phase 1: w = S z; p = z + beta p; q = w + beta q; P^T q --------
-      spmv_segments(a, a.z, m.seg);
+      fill_zc();
+      __syncthreads();
+      spmv_segments(a, m.zc, m.lc, kc0, m.seg, m.Ssm);
       __syncthreads();
       double pq_l = 0.0;
       for (int i = warp; i < nrows; i += kPcgWarps) {
@@ -777,6 +843,26 @@ void TwoLevelPcg::set_pattern(const int* row_ptr, const int* col, int nnzb, cuda
     }
     maxsegs = std::max(maxsegs, sidx);
   }
+  // ---- per-CTA z cache: distinct columns and the local index of each block --
+  std::vector<int> zl_ptr(G + 1, 0), zl, lcol(nnzb);
+  maxdist_ = 1;
+  maxblk_ = 1;
+  {
+    std::vector<int> mark(nf_, -1);
+    for (int c = 0; c < G; ++c) {
+      const int k0 = rp[row0[c]], k1 = rp[row0[c + 1]];
+      std::vector<int> d;
+      for (int k = k0; k < k1; ++k)
+        if (mark[cl[k]] != c) { mark[cl[k]] = c; d.push_back(cl[k]); }
+      std::sort(d.begin(), d.end());
+      for (size_t i = 0; i < d.size(); ++i) mark[d[i]] = c, zl.push_back(d[i]);
+      for (int k = k0; k < k1; ++k)
+        lcol[k] = (int)(std::lower_bound(d.begin(), d.end(), cl[k]) - d.begin());
+      zl_ptr[c + 1] = (int)zl.size();
+      maxdist_ = std::max(maxdist_, (int)d.size());
+      maxblk_ = std::max(maxblk_, k1 - k0);
+    }
+  }
   // ---- coarse clusters = groups of consecutive CTAs -------------------------
   const bool two = cluster_ > 0;
   nc_ = two ? std::min(G, std::max(1, (nf_ + cluster_ - 1) / cluster_)) : 1;
@@ -794,12 +880,47 @@ void TwoLevelPcg::set_pattern(const int* row_ptr, const int* col, int nnzb, cuda
   maxsegs_ = maxsegs;
   smem_ = sizeof(double) * (size_t)(6 * maxsegs + 108 * maxrows + 42 * nc_);
   SFM_REQUIRE(smem_ <= 200 * 1024, "PCG partition needs too much shared memory");
+  // ---- S blocks kept resident in shared memory for the whole solve ---------
+  // (the head of each warp's chunk, the same fraction in every warp)
+  int max_smem = 0;
+  SFM_CUDA(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+  const size_t per_cta_avail = (size_t)max_smem / (1024 / nt_) - 2048;  // static smem margin
+  const size_t zbytes = sizeof(double) * 6 * (size_t)maxdist_ + sizeof(int) * (size_t)maxblk_ + 16;
+  SFM_REQUIRE(smem_ + zbytes <= per_cta_avail, "PCG z cache does not fit in shared memory");
+  // Measured on config 3: keeping S blocks resident costs the L1 capacity
+  // the rest of the loop relies on and is slower (20.5 vs 18.2 us/iteration),
+  // so it is off unless SFM_PCG_RESIDENT=<blocks> asks for it.
+  int resblocks = 0;
+  if (const char* e = std::getenv("SFM_PCG_RESIDENT"))
+    resblocks = std::min((int)((per_cta_avail - smem_ - zbytes) / 288), std::max(0, std::atoi(e)));
+  std::vector<int2> wres((size_t)G * nwarps);
+  int maxres = 0;
+  for (int c = 0; c < G; ++c) {
+    const int64_t nb = rp[row0[c + 1]] - rp[row0[c]];
+    const int64_t R = std::min<int64_t>(resblocks, nb);
+    int base = 0;
+    for (int w = 0; w < nwarps; ++w) {
+      const int4 ch = wchunk[(size_t)c * nwarps + w];
+      const int len = ch.y - ch.x;
+      const int rw = nb > 0 ? (int)((int64_t)len * R / nb) : 0;
+      wres[(size_t)c * nwarps + w] = make_int2(rw, base);
+      base += rw;
+    }
+    maxres = std::max(maxres, base);
+  }
+  resblocks_ = maxres;
+  smem_ += sizeof(double) * 36 * (size_t)maxres;
+  smem_ += sizeof(double) * 6 * (size_t)maxdist_ + sizeof(int) * (size_t)maxblk_ + 16;
   SFM_CUDA(cudaFuncSetAttribute(k_pcg3, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_));
   int per_sm = 0;
   SFM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pcg3, nt_, smem_));
   SFM_REQUIRE(per_sm > 0 && G <= per_sm * nsm, "PCG grid cannot be made co-resident");
   cta_row0_.upload(row0.data(), row0.size(), s);
   wchunk_.upload(wchunk.data(), wchunk.size(), s);
+  wres_.upload(wres.data(), wres.size(), s);
+  zl_ptr_.upload(zl_ptr.data(), zl_ptr.size(), s);
+  zl_.upload(zl.data(), zl.size(), s);
+  lcol_.upload(lcol.data(), lcol.size(), s);
   rowseg_.upload(rowseg.data(), rowseg.size(), s);
   cta_cluster_.upload(cta_cluster.data(), cta_cluster.size(), s);
   cluster_cta0_.upload(cluster_cta0.data(), cluster_cta0.size(), s);
@@ -902,7 +1023,9 @@ void TwoLevelPcg::solve(const PcgProblem& p, int max_it, double rtol, BAScalars*
   a.nf = nf_; a.G = grid_; a.nc = nc_; a.npad = npad_; a.maxrows = maxrows_; a.maxsegs = maxsegs_;
   a.row_ptr = p.row_ptr; a.col = p.col; a.S = p.S; a.Minv = Minv_.get(); a.Pm = Pm_.get();
   a.Aci = gj_grid_ > 0 ? Aci_ : nullptr;
-  a.cta_row0 = cta_row0_.get(); a.wchunk = wchunk_.get(); a.rowseg = rowseg_.get();
+  a.cta_row0 = cta_row0_.get(); a.wchunk = wchunk_.get();
+  a.wres = wres_.get(); a.resblocks = resblocks_;
+  a.lcol = lcol_.get(); a.zl_ptr = zl_ptr_.get(); a.zl = zl_.get(); a.maxblk = maxblk_; a.maxdist = maxdist_; a.rowseg = rowseg_.get();
   a.cta_cluster = cta_cluster_.get(); a.cluster_cta0 = cluster_cta0_.get();
   a.b = p.b; a.x = p.x; a.r = r_.get(); a.z = z_.get(); a.p = p_.get(); a.q = q_.get();
   a.rpart = rpart_.get(); a.part = part_.get(); a.sc = sc; a.max_it = max_it; a.rtol = rtol;

@@ -45,14 +45,14 @@ class TwoLevelPcg {
 
  private:
   int nf_ = 0, cluster_ = 0, nc_ = 0, ncp_ = 0, npad_ = 0, grid_ = 0, gj_grid_ = 0;
-  int maxrows_ = 0, maxsegs_ = 0, nt_ = 512, refresh_ = 1, lin_count_ = 0;
+  int maxrows_ = 0, maxsegs_ = 0, nt_ = 512, refresh_ = 1, lin_count_ = 0, resblocks_ = 0, maxdist_ = 1, maxblk_ = 1;
   size_t smem_ = 0;
   int npairs_ = 0;
   bool coarse_valid_ = false;
   const double* Aci_ = nullptr;
   DevBuf<double> Minv_, Pm_, Ac_[2], r_, z_, p_, q_, rpart_, part_;
-  DevBuf<int2> pair_cd_, rowseg_;
-  DevBuf<int> pair_ptr_, cta_row0_, cta_cluster_, cluster_cta0_;
+  DevBuf<int2> pair_cd_, rowseg_, wres_;
+  DevBuf<int> pair_ptr_, cta_row0_, cta_cluster_, cluster_cta0_, zl_ptr_, zl_, lcol_;
   DevBuf<int4> runs_, wchunk_;
 };
 
