@@ -355,6 +355,7 @@ struct Pcg3Args {
   BAScalars* sc;
   int max_it;
   double rtol;
+  int fuse_zc;
 };
 
 __device__ __forceinline__ double warp_sum(double v) {
@@ -610,10 +611,27 @@ __global__ void __launch_bounds__(kPcgMaxThreads, 1) k_pcg3(Pcg3Args a) {
   const int nblk = __ldg(a.row_ptr + row1) - kc0;
   const int zl0 = a.zl_ptr[blockIdx.x], ndist = a.zl_ptr[blockIdx.x + 1] - zl0;
   // z cache fill: 3 double2 per distinct column, straight from L2
-  auto fill_zc = [&]() {
-    for (int t = threadIdx.x; t < 3 * ndist; t += kPcgThreads) {
+  // (threads from `first` on; the first warps are busy with the scalar sums)
+  auto fill_zc = [&](int first) {
+    for (int t = threadIdx.x - first; t < 3 * ndist && t >= 0; t += kPcgThreads - first) {
       const int c = __ldg(a.zl + zl0 + t / 3);
       reinterpret_cast<double2*>(m.zc)[t] = ldcg2(a.z + c * 6 + 2 * (t % 3));
+    }
+  };
+  // After the r.z / r.r barrier: the scalar sums (warps 0..nsum-1) and the
+  // next SpMV's z cache (the other warps) in one L2 round trip.
+  auto sums_and_zc = [&](const double* part, int nsum) {
+    if (warp < nsum) {
+      double sacc = 0.0;
+      for (int i = lane; i < G; i += 32) sacc += __ldcg(part + warp * G + i);
+      sacc = warp_sum(sacc);
+      if (lane == 0) sums[warp] = sacc;
+    }
+    if (a.fuse_zc) fill_zc(32 * nsum);
+    __syncthreads();
+    if (!a.fuse_zc) {
+      fill_zc(0);
+      __syncthreads();
     }
   };
   double* part_pq = a.part;          // [G]
@@ -688,7 +706,7 @@ __global__ void __launch_bounds__(kPcgMaxThreads, 1) k_pcg3(Pcg3Args a) {
   double2 s1 = block_sum2(rz_l, 0.0, red);
   if (threadIdx.x == 0) part_rz[blockIdx.x] = s1.x;
   grid.sync();
-  gather_after_sync(a, part_rz, sums, 1, m.rc, false, true, nullptr, nullptr);
+  sums_and_zc(part_rz, 1);
   double rz_old = sums[0];
   int it = 0, fail = 0;
   double beta = 0.0;
@@ -697,8 +715,6 @@ __global__ void __launch_bounds__(kPcgMaxThreads, 1) k_pcg3(Pcg3Args a) {
   } else {
     for (it = 0; it < a.max_it;) {
       // ---- phase 1: w = S z; p = z + beta p; q = w + beta q; P^T q --------
-      fill_zc();
-      __syncthreads();
       spmv_segments(a, m.zc, m.lc, kc0, m.seg, m.Ssm);
       __syncthreads();
       double pq_l = 0.0;
@@ -748,7 +764,7 @@ __global__ void __launch_bounds__(kPcgMaxThreads, 1) k_pcg3(Pcg3Args a) {
       const double2 t = block_sum2(rz_n, rr_n, red);
       if (threadIdx.x == 0) { part_rz[blockIdx.x] = t.x; part_rz[G + blockIdx.x] = t.y; }
       grid.sync();
-      gather_after_sync(a, part_rz, sums, 2, m.rc, false, true, nullptr, nullptr);
+      sums_and_zc(part_rz, 2);
       const double rz_new = sums[0], rr = sums[1];
       ++it;
       if (!isfinite(rr) || !isfinite(rz_new)) { fail = 1; break; }
@@ -1029,6 +1045,8 @@ void TwoLevelPcg::solve(const PcgProblem& p, int max_it, double rtol, BAScalars*
   a.cta_cluster = cta_cluster_.get(); a.cluster_cta0 = cluster_cta0_.get();
   a.b = p.b; a.x = p.x; a.r = r_.get(); a.z = z_.get(); a.p = p_.get(); a.q = q_.get();
   a.rpart = rpart_.get(); a.part = part_.get(); a.sc = sc; a.max_it = max_it; a.rtol = rtol;
+  a.fuse_zc = 1;
+  if (const char* e = std::getenv("SFM_PCG_FUSEZC")) a.fuse_zc = std::atoi(e);
   void* args[] = {&a};
   ProfScope ps(*prof, "pcg", 0.0, s);
   SFM_CUDA(cudaLaunchCooperativeKernel((void*)k_pcg3, grid_, nt_, args, smem_, s));
