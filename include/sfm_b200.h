@@ -134,7 +134,7 @@ typedef struct {
   int32_t coarse_cluster;     /* PCG coarse level: frames per cluster (0 =
                                  default 8, < 0 = block-Jacobi only)       */
   int32_t coarse_refresh;     /* rebuild the coarse operator every this many
-                                 linearisations (0 = default 4)            */
+                                 linearisations (0 = default 8)            */
 } sfm_ba_options;
 
 /* SolverReport (solver.py:90-95) + device-side statistics. */

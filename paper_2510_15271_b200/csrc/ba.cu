@@ -1582,7 +1582,7 @@ void BASolver::setup(const sfm_ba_problem& pr, const sfm_ba_options& opt) {
   }
   if (!use_dense_ && nfree_ > 0) {
     const int cl = opt_.coarse_cluster == 0 ? 8 : opt_.coarse_cluster;
-    pcg_.setup(nfree_, cl, opt_.coarse_refresh > 0 ? opt_.coarse_refresh : 4, s);
+    pcg_.setup(nfree_, cl, opt_.coarse_refresh > 0 ? opt_.coarse_refresh : 8, s);
     pcg_.set_pattern(row_ptr_.get(), col_idx_.get(), n_full_, s);
   }
 

@@ -58,7 +58,7 @@ class DeviceOptions:
     pcg_max_iters: int = 2000
     dense_max_dim: int = 210
     coarse_cluster: int = 8      # frames per coarse cluster; < 0 = block-Jacobi only
-    coarse_refresh: int = 4      # rebuild the coarse operator every N linearisations
+    coarse_refresh: int = 8      # rebuild the coarse operator every N linearisations
 
 
 DEFAULT_DEVICE_OPTIONS = DeviceOptions()

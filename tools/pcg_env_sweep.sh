@@ -5,6 +5,6 @@ OUT=gpurun_out/$1; mkdir -p $OUT
 for envs in $2; do
   for v in $3; do
     echo "env=$envs" >> $OUT/env_sweep.log
-    env $(echo $envs | tr ',' ' ') timeout 300 python tools/pcg_sweep.py 3 6 $v >> $OUT/env_sweep.log 2>&1
+    env $(echo $envs | tr "," " ") timeout 300 python tools/pcg_sweep.py 3 ${ITERS:-6} $v >> $OUT/env_sweep.log 2>&1
   done
 done
