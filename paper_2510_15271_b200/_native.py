@@ -115,7 +115,8 @@ def load_library(path: str = None):
     with _lib_lock:
         if _lib is not None:
             return _lib
-        path = path or LIB_PATH
+        # SFM_B200_LIB: an alternative in-tree build (A/B experiments)
+        path = path or os.environ.get("SFM_B200_LIB") or LIB_PATH
         if not os.path.exists(path):
             raise NativeLibraryMissing(
                 f"{path} not built: run `python -c 'import __graft_entry__ as g; g.build()'` "
