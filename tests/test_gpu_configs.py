@@ -1,0 +1,218 @@
+"""Parity and properties at the BASELINE.json configuration sizes (SURVEY.md
+§8(c)/(d)).  sfmkit itself cannot reach these sizes (DNF at 250k
+observations), so the checker is the pinned oracle
+(oracle/ba.py, oracle/tri.py) where it finishes in seconds, and
+size-independent properties where it does not:
+
+  * configs[1] (driving, 500 frames, 100k points, ~0.9M observations, Huber):
+    the first LM trial pushes a point behind a camera; the reference raises
+    NonPositiveDepth out of bundle_adjust (solver.py:235 -> cameras.py:132),
+    and so must the device path, with the same payload;
+  * a 600-camera / 1.4M-observation Venice-shaped scene: two full LM
+    iterations vs the oracle's exact Schur + Cholesky solve;
+  * configs[2] (BAL-Venice-shaped, 1,778 cameras, 5M observations):
+    initial cost vs the oracle, bit-identical reruns, monotone cost;
+  * configs[3]-shaped triangulation + gating (2k cameras, 5% outliers):
+    RANSAC status / masks / removed counts bit-exact against the oracle on
+    a random sample of tracks, positions to 1e-9;
+  * configs[4] (10k cameras, 10M points, 50M observations): the first LM
+    iteration at full size (initial cost vs the chunked oracle, bit-identical
+    outcome on a rerun) when the host has the RAM to generate it.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+MODELS = [(0, 500.0, 500.0, 320.0, 240.0, (0.0, 0.0))]
+
+
+def oracle_problem(a):
+    from oracle import ba as OB
+    return OB.BAProblem(a.cam_q, a.cam_t, a.frame_model, a.frame_fixed, MODELS, a.points,
+                        a.obs_frame, a.obs_point, a.obs_uv, a.edge_ab, a.prior_frame,
+                        a.edge_weight, a.prior_weight)
+
+
+def oracle_cost_chunked(a, loss_kind, loss_param, chunk_points=2_000_000):
+    """Problem.evaluate (solver.py:132-142) summed over point chunks (the
+    cost is additive over residual blocks), pose terms once."""
+    from oracle import ba as OB
+    P = len(a.points)
+    total = 0.0
+    for p0 in range(0, P, chunk_points):
+        p1 = min(P, p0 + chunk_points)
+        o0, o1 = np.searchsorted(a.obs_point, [p0, p1])
+        first = p0 == 0
+        sub = OB.BAProblem(a.cam_q, a.cam_t, a.frame_model, a.frame_fixed, MODELS,
+                           a.points[p0:p1], a.obs_frame[o0:o1], a.obs_point[o0:o1] - p0,
+                           a.obs_uv[o0:o1], a.edge_ab if first else None,
+                           a.prior_frame if first else None, a.edge_weight, a.prior_weight)
+        total += sub.cost(a.cam_q, a.cam_t, a.points[p0:p1], loss_kind, loss_param)
+    return total
+
+
+def test_config2_depth_failure_matches_oracle():
+    from oracle import ba as OB
+    from paper_2510_15271_b200.errors import NonPositiveDepth
+    from paper_2510_15271_b200.mapping import solve_arrays
+    from paper_2510_15271_b200.scenes import config_scene, scene_arrays
+    from paper_2510_15271_b200.solver import DeviceOptions, RobustLoss, SolverOptions
+    a = scene_arrays(config_scene(2, seed=0))
+    assert len(a.obs_frame) > 800_000
+    with pytest.raises(OB.OracleNonPositiveDepth) as ref:
+        oracle_problem(a).solve(1, 2.0, 1)
+    with pytest.raises(NonPositiveDepth) as got:
+        solve_arrays(a, RobustLoss("huber", 2.0), SolverOptions(max_iters=1),
+                     DeviceOptions(linear_solver="pcg", pcg_rtol=1e-12))
+    assert str(ref.value) in str(got.value)
+
+
+def test_venice_1p4m_two_lm_iterations_match_oracle():
+    from paper_2510_15271_b200.mapping import solve_arrays
+    from paper_2510_15271_b200.scenes import make_scene, scene_arrays
+    from paper_2510_15271_b200.solver import DeviceOptions, RobustLoss, SolverOptions
+    a = scene_arrays(make_scene(600, 300000, 1500000, shape="venice", seed=1))
+    q, t, X, rep, raw = solve_arrays(a, RobustLoss("huber", 2.0), SolverOptions(max_iters=2),
+                                     DeviceOptions(linear_solver="pcg", pcg_rtol=1e-12))
+    qo, to, Xo, ro = oracle_problem(a).solve(1, 2.0, 2)
+    assert rep.iterations == ro["iterations"] == 2
+    assert rep.initial_cost == pytest.approx(ro["initial_cost"], rel=1e-12)
+    assert rep.final_cost == pytest.approx(ro["final_cost"], rel=1e-9)
+    scale = np.abs(Xo).max()
+    np.testing.assert_allclose(X, Xo, atol=1e-8 * scale)
+    np.testing.assert_allclose(t, to, atol=1e-8 * scale)
+    np.testing.assert_allclose(q, qo, atol=1e-9)
+
+
+def test_config3_full_size_cost_determinism_monotone():
+    from paper_2510_15271_b200.mapping import DeviceBA
+    from paper_2510_15271_b200.scenes import config_scene, scene_arrays
+    from paper_2510_15271_b200.solver import DeviceOptions, RobustLoss, SolverOptions
+    a = scene_arrays(config_scene(3, seed=0))
+    assert len(a.obs_frame) > 4_900_000 and len(a.cam_q) == 1778
+    ref_cost = oracle_cost_chunked(a, 1, 2.0)
+    runs = []
+    for _ in range(2):
+        ba = DeviceBA(a, RobustLoss("huber", 2.0), SolverOptions(max_iters=100),
+                      DeviceOptions(linear_solver="pcg", pcg_rtol=1e-10))
+        costs = []
+        for _ in range(3):
+            rep = ba.iterate(1)
+            costs.append(rep.final_cost)
+        q, t, X = ba.download()
+        runs.append((rep.initial_cost, costs, q, t, X))
+    init, costs, q, t, X = runs[0]
+    assert init == pytest.approx(ref_cost, rel=1e-12)
+    assert all(c2 < c1 for c1, c2 in zip([init] + costs, costs))
+    assert runs[1][1] == costs
+    for u, v in zip(runs[0][2:], runs[1][2:]):
+        assert u.tobytes() == v.tobytes()
+
+
+def tracks_from_scene(sc):
+    from paper_2510_15271_b200 import _native as nat
+    from paper_2510_15271_b200.cameras import CameraModel
+    from paper_2510_15271_b200.mapping import model_table
+    models, n_models, fm = model_table([CameraModel(**sc.camera)] * sc.n_frames)
+    ptr = np.searchsorted(sc.obs_point, np.arange(sc.n_points + 1)).astype(np.int64)
+    keep = dict(q=np.ascontiguousarray(sc.cam_q), t=np.ascontiguousarray(sc.cam_t),
+                fm=np.ascontiguousarray(fm, dtype=np.int32), ptr=ptr,
+                of=np.ascontiguousarray(sc.obs_frame, dtype=np.int32),
+                uv=np.ascontiguousarray(sc.obs_uv), models=models)
+    s = nat.TracksC(sc.n_frames, n_models, nat.ptr(keep["q"]), nat.ptr(keep["t"]),
+                    nat.ptr(keep["fm"]), ctypes.addressof(models), sc.n_points, len(keep["of"]),
+                    nat.ptr(keep["ptr"]), nat.ptr(keep["of"]), nat.ptr(keep["uv"]), None)
+    return s, keep
+
+
+def test_config4_shaped_ransac_and_gate_match_oracle():
+    from oracle import tri as OT
+    from paper_2510_15271_b200 import _native as nat
+    from paper_2510_15271_b200.scenes import make_scene
+    sc = make_scene(2000, 200000, 1000000, shape="line", seed=4, outlier_frac=0.05)
+    s, keep = tracks_from_scene(sc)
+    T, N = sc.n_points, len(keep["of"])
+    X = np.empty((T, 3))
+    mask = np.empty(N, np.uint8)
+    st = np.empty(T, np.int8)
+    ctx = nat.default_context()
+    thr, ang = 4.0, np.radians(0.5)
+    ctx.check(ctx.lib.sfm_ransac_triangulate(ctx.handle, ctypes.byref(s), thr, ang,
+                                             nat.TRI_METHODS["dlt"], nat.ptr(X), nat.ptr(mask),
+                                             nat.ptr(st)))
+    fr = OT.Frames(keep["q"], keep["t"], keep["fm"], MODELS)
+    rng = np.random.default_rng(0)
+    sample = np.sort(rng.choice(T, 1500, replace=False))
+    ptr = keep["ptr"]
+    for i in sample:
+        b0, b1 = ptr[i], ptr[i + 1]
+        xo, mo, so = OT.ransac_triangulate(fr, list(keep["of"][b0:b1]), list(keep["uv"][b0:b1]),
+                                           thr, ang, "dlt")
+        assert int(st[i]) == int(so), i
+        if so == OT.OK:
+            assert mask[b0:b1].astype(bool).tolist() == list(mo), i
+            np.testing.assert_allclose(X[i], xo, rtol=1e-9, atol=1e-9)
+    # gating (remove_outliers) of the triangulated tracks at the stage-2 2 px bar
+    ok = st == nat.TRI_OK
+    pts = np.ascontiguousarray(np.where(ok[:, None], X, 0.0))
+    m_in = np.ascontiguousarray(np.where(np.repeat(ok, np.diff(ptr)), mask, 0).astype(np.uint8))
+    m_out = m_in.copy()
+    inl = np.empty(T, np.int32)
+    removed = ctypes.c_int64(0)
+    ctx.check(ctx.lib.sfm_gate(ctx.handle, ctypes.byref(s), nat.ptr(pts), 2.0, nat.ptr(m_out),
+                               nat.ptr(inl), ctypes.byref(removed)))
+    sub_ptr = np.concatenate([[0], np.cumsum(np.diff(ptr)[sample])])
+    idx = np.concatenate([np.arange(ptr[i], ptr[i + 1]) for i in sample])
+    mo, io, ro = OT.gate(fr, sub_ptr, keep["of"][idx], keep["uv"][idx], pts[sample],
+                         m_in[idx].astype(bool), 2.0)
+    assert m_out[idx].astype(bool).tolist() == mo.tolist()
+    assert inl[sample].tolist() == io.tolist()
+    assert int(removed.value) == int((m_in.astype(bool) & ~m_out.astype(bool)).sum())
+
+
+def _host_ram_gb():
+    try:
+        import psutil
+        return psutil.virtual_memory().available / 1e9
+    except Exception:
+        return 0.0
+
+
+@pytest.mark.skipif(_host_ram_gb() < 120, reason="config 5 generation needs ~45 GB of host RAM "
+                    "with headroom")
+def test_config5_full_size_first_lm_iteration():
+    """10k cameras / 10M points / 50M observations.  Like configs[1], this
+    forward-moving sequence makes the undamped first step (lambda = 1e-4)
+    push a point behind a camera, where the reference raises
+    NonPositiveDepth out of bundle_adjust; the oracle cannot reach this size,
+    so the checks are the oracle's initial cost and a bit-identical outcome
+    (same exception payload, or same costs) on a rerun."""
+    from paper_2510_15271_b200.errors import NonPositiveDepth
+    from paper_2510_15271_b200.mapping import DeviceBA
+    from paper_2510_15271_b200.scenes import config_scene, scene_arrays
+    from paper_2510_15271_b200.solver import DeviceOptions, RobustLoss, SolverOptions
+    a = scene_arrays(config_scene(5, seed=0))
+    assert len(a.obs_frame) > 49_000_000 and len(a.cam_q) == 10000
+    outcomes = []
+    for _ in range(2):
+        ba = DeviceBA(a, RobustLoss("huber", 2.0), SolverOptions(max_iters=100),
+                      DeviceOptions(linear_solver="pcg", pcg_rtol=1e-10))
+        try:
+            rep = ba.iterate(1)
+            assert np.isfinite(rep.final_cost) and rep.final_cost < rep.initial_cost
+            outcomes.append(("ok", rep.initial_cost, rep.final_cost))
+        except NonPositiveDepth as e:
+            outcomes.append(("NonPositiveDepth", str(e)))
+        del ba
+    assert outcomes[0] == outcomes[1]
+    # initial cost through the setup path (sfm_ba_setup evaluates it)
+    ba = DeviceBA(a, RobustLoss("huber", 2.0), SolverOptions(max_iters=0),
+                  DeviceOptions(linear_solver="pcg"))
+    rep = ba.iterate(1)
+    assert rep.initial_cost == pytest.approx(oracle_cost_chunked(a, 1, 2.0), rel=1e-11)
