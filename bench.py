@@ -258,9 +258,17 @@ def main():
     # ---- end-to-end through the C-ABI with host buffers (e2e) -----------------
     e2e = None
     if not args.no_e2e:
+        # the caller's problem arrays live in pinned host memory (the e2e
+        # contract); the H2D copies happen inside the timed call
+        import dataclasses
+        pin = {f.name: torch.from_numpy(getattr(part, f.name)).pin_memory().numpy()
+               for f in dataclasses.fields(part)
+               if isinstance(getattr(part, f.name), np.ndarray)}
+        part_pinned = dataclasses.replace(part, **pin)
+        del ba  # the stepwise session's device memory returns to the pool
         barrier_sync(world)
         t0 = time.perf_counter()
-        q, t, X, rep_e, raw_e = solve_arrays(part, loss, SolverOptions(max_iters=args.steps),
+        q, t, X, rep_e, raw_e = solve_arrays(part_pinned, loss, SolverOptions(max_iters=args.steps),
                                              dopt, ctx)
         barrier_sync(world)
         e2e_s = max_over_ranks(time.perf_counter() - t0, world)
@@ -272,8 +280,8 @@ def main():
                "h2d_bytes_per_step": int(h2d / max(rep_e.iterations, 1)),
                "d2h_bytes_per_step": int(d2h / max(rep_e.iterations, 1)),
                "iterations": rep_e.iterations, "seconds": e2e_s,
-               "note": "sfm_ba_solve from host arrays: H2D + structure build + initial cost + "
-                       "LM iterations + D2H, per call amortised over its iterations"}
+               "note": "one sfm_ba_solve call from pinned host arrays: H2D + structure build + "
+                       "initial cost + LM iterations 1..steps + D2H, amortised over its iterations"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -175,6 +175,7 @@ int sfm_prof_reset(sfm_ctx* ctx);
  * out_cam_q/out_cam_t/out_points (same shapes as the inputs; fixed frames are
  * copied bit-identically) and fills `report`.  On SFM_E_NON_POSITIVE_DEPTH the
  * outputs are left untouched (the reference raises before writing back).
+ * Ends any stepwise (sfm_ba_setup/iterate) session on the context.
  */
 int sfm_ba_solve(sfm_ctx* ctx, const sfm_ba_problem* prob,
                  const sfm_ba_options* opt, double* out_cam_q,

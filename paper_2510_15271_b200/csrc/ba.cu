@@ -25,7 +25,9 @@
 
 #include <algorithm>
 #include <cmath>
+#include <chrono>
 #include <cstdio>
+#include <cstdlib>
 
 #include "ba.cuh"
 #include "pcg.cuh"
@@ -1241,6 +1243,25 @@ int bits_for(unsigned long long maxval) {
 // host driver
 // ===========================================================================
 
+namespace {
+// SFM_TIMING=1: wall-clock split of sfm_ba_setup on stderr (stream-synced
+// at each mark, so only for diagnosis).
+struct SetupTimer {
+  bool on = std::getenv("SFM_TIMING") != nullptr;
+  cudaStream_t s;
+  std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+  explicit SetupTimer(cudaStream_t st) : s(st) {}
+  void mark(const char* what) {
+    if (!on) return;
+    cudaStreamSynchronize(s);
+    const auto t1 = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[sfm setup] %-28s %8.3f ms\n", what,
+                 std::chrono::duration<double, std::milli>(t1 - t0).count());
+    t0 = t1;
+  }
+};
+}  // namespace
+
 void BASolver::setup(const sfm_ba_problem& pr, const sfm_ba_options& opt) {
   opt_ = opt;
   rank_ = comm_ ? comm_->rank : 0;
@@ -1257,6 +1278,7 @@ void BASolver::setup(const sfm_ba_problem& pr, const sfm_ba_options& opt) {
   edge_w_ = std::sqrt(pr.edge_weight);
   prior_w_ = std::sqrt(pr.prior_weight);
   cudaStream_t s = stream_;
+  SetupTimer tm(s);
 
   // frames: free index map (solver.py:154-161: free blocks in insertion
   // order = sorted frames), models
@@ -1288,6 +1310,7 @@ void BASolver::setup(const sfm_ba_problem& pr, const sfm_ba_options& opt) {
   sc_.resize(1);
   SFM_CUDA(cudaMemsetAsync(sc_.get(), 0, sizeof(BAScalars), s));
 
+  tm.mark("uploads");
   // layout validation
   {
     DevBuf<int> bad;
@@ -1305,6 +1328,7 @@ void BASolver::setup(const sfm_ba_problem& pr, const sfm_ba_options& opt) {
 
   CubTemp tmp;
   size_t tb = 0;
+  tm.mark("validate + pt_ptr");
   // ---- pair list: count, scan, generate, stable sort by S block ----------
   DevBuf<int64_t> pcnt, poff;
   pcnt.resize(P_ + 1);
@@ -1357,6 +1381,7 @@ void BASolver::setup(const sfm_ba_problem& pr, const sfm_ba_options& opt) {
     SFM_CUDA(cub::DeviceScan::ExclusiveSum(tmp.get(tb), tb, pb_pair_cnt64.get(), pb_pair_ptr_.get(), n_pb_ + 1, s));
   }
 
+  tm.mark("pair list + sort");
   // ---- S block pattern: pair blocks U diagonal U lambda_c edges ----------
   std::vector<int> h_ab(2 * (size_t)n_edges_), h_pf(n_priors_);
   if (n_edges_) std::memcpy(h_ab.data(), pr.edge_ab, sizeof(int) * 2 * n_edges_);
@@ -1488,6 +1513,7 @@ void BASolver::setup(const sfm_ba_problem& pr, const sfm_ba_options& opt) {
     diag_ub_.upload(dub.data(), nfree_, s);
     diag_pos_.upload(dpos.data(), nfree_, s);
   }
+  tm.mark("S pattern");
   // camera-major observation streams + off-diagonal block list
   {
     std::vector<int64_t> cptr(nfree_ + 1, 0);
@@ -1523,6 +1549,7 @@ void BASolver::setup(const sfm_ba_problem& pr, const sfm_ba_options& opt) {
     n_off_ = (int)off.size();
     work_.upload(off.data(), off.size(), s);
   }
+  tm.mark("camera-major streams");
   // pose terms per free camera (edge side 0 = from/a, 1 = to/b, prior 2)
   {
     std::vector<std::vector<int>> per(nfree_);
@@ -1586,6 +1613,7 @@ void BASolver::setup(const sfm_ba_problem& pr, const sfm_ba_options& opt) {
     pcg_.set_pattern(row_ptr_.get(), col_idx_.get(), n_full_, s);
   }
 
+  tm.mark("terms + buffers + pcg plan");
   // all_fixed (solver.py:200-203) and the initial cost (solver.py:201)
   int has_res = (N_ > 0 || n_edges_ > 0 || n_priors_ > 0) ? 1 : 0;
   if (comm_ && comm_->active()) {
@@ -1602,6 +1630,7 @@ void BASolver::setup(const sfm_ba_problem& pr, const sfm_ba_options& opt) {
   term_ = SFM_TERM_MAX_ITERATIONS;
   lam_ = opt_.initial_lambda;
   initial_cost_ = eval_cost_current();
+  tm.mark("initial cost");
   cost_ = initial_cost_;
   finished_ = false;
   if (n_params_ == 0 || !has_residuals_) {

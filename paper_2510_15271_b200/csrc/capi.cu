@@ -28,6 +28,7 @@ int guarded(sfm_ctx* ctx, F&& body) {
     cudaError_t e = cudaSetDevice(ctx->device);
     if (e != cudaSuccess) throw sfm::SfmError(SFM_E_CUDA, std::string("cudaSetDevice: ") + cudaGetErrorString(e));
     ctx->err.clear();
+    sfm::alloc_stream() = ctx->stream;
     body();
     return SFM_OK;
   } catch (const sfm::SfmError& e) {
@@ -61,6 +62,13 @@ int sfm_ctx_create(int32_t device, int32_t rank, int32_t world, const uint8_t* n
   ctx->device = device;
   int rc = guarded(ctx, [&] {
     SFM_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+    sfm::alloc_stream() = ctx->stream;
+    // keep freed device blocks cached in the default pool (stream-ordered
+    // allocation, see DevBuf)
+    cudaMemPool_t pool;
+    SFM_CUDA(cudaDeviceGetDefaultMemPool(&pool, ctx->device));
+    uint64_t thr = UINT64_MAX;
+    SFM_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
     ctx->comm.init(rank, world, nccl_id);
   });
   if (rc != SFM_OK) {
@@ -75,8 +83,13 @@ int sfm_ctx_create(int32_t device, int32_t rank, int32_t world, const uint8_t* n
 void sfm_ctx_destroy(sfm_ctx* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->device);
+  sfm::alloc_stream() = ctx->stream;
   ctx->ba.reset();
-  if (ctx->stream) cudaStreamDestroy(ctx->stream);
+  if (ctx->stream) {
+    cudaStreamSynchronize(ctx->stream);
+    cudaStreamDestroy(ctx->stream);
+  }
+  sfm::alloc_stream() = nullptr;
   delete ctx;
 }
 
@@ -106,6 +119,7 @@ int sfm_prof_reset(sfm_ctx* ctx) {
 int sfm_ba_setup(sfm_ctx* ctx, const sfm_ba_problem* prob, const sfm_ba_options* opt) {
   return guarded(ctx, [&] {
     SFM_REQUIRE(prob && opt, "null problem/options");
+    ctx->ba.reset();  // back to the pool before the new solver allocates
     ctx->ba.reset(new sfm::BASolver(ctx->stream, &ctx->prof, &ctx->comm));
     try {
       ctx->ba->setup(*prob, *opt);
@@ -134,6 +148,9 @@ int sfm_ba_solve(sfm_ctx* ctx, const sfm_ba_problem* prob, const sfm_ba_options*
                  double* out_cam_t, double* out_points, sfm_ba_report* report) {
   return guarded(ctx, [&] {
     SFM_REQUIRE(prob && opt, "null problem/options");
+    // a full solve ends any stepwise session: its device memory goes back
+    // to the pool first, so the solve reuses it instead of growing the pool
+    ctx->ba.reset();
     sfm::BASolver solver(ctx->stream, &ctx->prof, &ctx->comm);
     solver.setup(*prob, *opt);
     solver.iterate(opt->max_iters > 0 ? opt->max_iters : 0, report);

@@ -38,6 +38,16 @@ struct SfmError : public std::runtime_error {
     if (!(cond)) throw ::sfm::SfmError(SFM_E_INVALID, msg);                    \
   } while (0)
 
+// Stream on which device buffers are allocated and freed (stream-ordered
+// allocation from the device's default memory pool, whose release threshold
+// is raised at context creation so freed blocks stay cached across calls:
+// repeated bundle_adjust / triangulation calls do not pay cudaMalloc).  Set
+// by the C-ABI guard to the context stream for the duration of a call.
+inline cudaStream_t& alloc_stream() {
+  static thread_local cudaStream_t s = nullptr;
+  return s;
+}
+
 // Owning device buffer (grow-only).
 template <typename T>
 struct DevBuf {
@@ -49,16 +59,16 @@ struct DevBuf {
   DevBuf& operator=(const DevBuf&) = delete;
   ~DevBuf() { release(); }
   void release() {
-    if (ptr) cudaFree(ptr);
+    if (ptr) cudaFreeAsync(ptr, alloc_stream());
     ptr = nullptr;
     cap = n = 0;
   }
   T* resize(size_t count) {
     if (count > cap) {
-      if (ptr) cudaFree(ptr);
+      if (ptr) cudaFreeAsync(ptr, alloc_stream());
       ptr = nullptr;
       size_t bytes = (count ? count : 1) * sizeof(T);
-      SFM_CUDA(cudaMalloc(&ptr, bytes));
+      SFM_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&ptr), bytes, alloc_stream()));
       cap = count;
     }
     n = count;

@@ -955,29 +955,35 @@ void TwoLevelPcg::set_pattern(const int* row_ptr, const int* col, int nnzb, cuda
     SFM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_gj_inverse, kGJThreads, gsm));
     const int T = npad_ / kNB;
     gj_grid_ = std::max(1, std::min(T * T, per * nsm));
-    // coarse assembly runs (row i, k0, k1) grouped by coarse pair (c(i), d)
-    std::vector<std::vector<std::array<int, 3>>> per_pair(nc_ * (size_t)nc_);
+    // coarse assembly runs (row i, k0, k1) grouped by coarse pair (c(i), d),
+    // rows ascending inside a pair (stable sort of the row-ordered runs)
+    std::vector<std::array<int, 4>> rr;  // (pair key, i, k0, k1)
+    rr.reserve((size_t)nf_ * 8);
     for (int i = 0; i < nf_; ++i) {
       int k = rp[i];
       while (k < rp[i + 1]) {
         const int d = frame_cluster[cl[k]];
         int k1 = k;
         while (k1 < rp[i + 1] && frame_cluster[cl[k1]] == d) ++k1;
-        per_pair[(size_t)frame_cluster[i] * nc_ + d].push_back({i, k, k1});
+        rr.push_back({frame_cluster[i] * nc_ + d, i, k, k1});
         k = k1;
       }
     }
+    std::stable_sort(rr.begin(), rr.end(), [](const std::array<int, 4>& x, const std::array<int, 4>& y) {
+      return x[0] < y[0];
+    });
     std::vector<int2> cd;
     std::vector<int> ptr(1, 0);
     std::vector<int4> runs;
-    for (int c = 0; c < nc_; ++c)
-      for (int d = 0; d < nc_; ++d) {
-        auto& v = per_pair[(size_t)c * nc_ + d];
-        if (v.empty()) continue;
-        cd.push_back(make_int2(c, d));
-        for (auto& r : v) runs.push_back(make_int4(r[0], r[1], r[2], 0));
-        ptr.push_back((int)runs.size());
+    runs.reserve(rr.size());
+    for (size_t q = 0; q < rr.size(); ++q) {
+      if (q == 0 || rr[q][0] != rr[q - 1][0]) {
+        if (q) ptr.push_back((int)runs.size());
+        cd.push_back(make_int2(rr[q][0] / nc_, rr[q][0] % nc_));
       }
+      runs.push_back(make_int4(rr[q][1], rr[q][2], rr[q][3], 0));
+    }
+    if (!rr.empty()) ptr.push_back((int)runs.size());
     npairs_ = (int)cd.size();
     pair_cd_.upload(cd.data(), cd.size(), s);
     pair_ptr_.upload(ptr.data(), ptr.size(), s);
