@@ -223,7 +223,8 @@ def _with_provenance(smap):
 
 # --- triangulation / gating fixtures ----------------------------------------------
 
-def track_fixture(name, tracks, poses, thr, min_angle, method):
+def track_fixture(name, tracks, poses, thr, min_angle, method, cams_of=None, models=None):
+    """cams_of: frame -> (model index, CameraModel); default all frames CAM."""
     frames = sorted(poses)
     fidx = {f: i for i, f in enumerate(frames)}
     ptr = np.zeros(len(tracks) + 1, np.int64)
@@ -232,7 +233,10 @@ def track_fixture(name, tracks, poses, thr, min_angle, method):
     uv = np.array([o.pixel for t in tracks for o in t.observations]).reshape(-1, 2)
     q = np.array([poses[f].quat for f in frames])
     t = np.array([poses[f].t for f in frames])
-    cams = {f: CAM for f in frames}
+    cams = {f: (cams_of[f][1] if cams_of else CAM) for f in frames}
+    frame_model = np.array([cams_of[f][0] if cams_of else 0 for f in frames], np.int32)
+    if models is None:
+        models = np.array([[0, 500.0, 500.0, 320.0, 240.0, 0.0, 0.0]])
     X = np.full((len(tracks), 3), np.nan)
     mask = np.zeros(len(of), np.uint8)
     status = np.zeros(len(tracks), np.int8)
@@ -257,8 +261,7 @@ def track_fixture(name, tracks, poses, thr, min_angle, method):
         except Exception as e:  # noqa: BLE001
             dstat[i] = codes.get(type(e).__name__, 9)
     np.savez_compressed(os.path.join(HERE, f"tri_{name}.npz"), cam_q=q, cam_t=t,
-                        frame_model=np.zeros(len(frames), np.int32),
-                        models=np.array([[0, 500.0, 500.0, 320.0, 240.0, 0.0, 0.0]]),
+                        frame_model=frame_model, models=models,
                         track_ptr=ptr, obs_frame=of, obs_uv=uv, threshold_px=thr,
                         min_angle=min_angle, method=method, ref_X=X, ref_mask=mask,
                         ref_status=status, ref_direct_X=dX, ref_direct_status=dstat)
@@ -326,8 +329,7 @@ def gate_fixture():
     mask_out = np.concatenate([lm.inlier_mask for lm in tri]).astype(np.uint8)
     status = np.array([1 if lm.track.status == M.TRIANGULATED else 0 for lm in tri], np.int8)
     np.savez_compressed(os.path.join(HERE, "gate.npz"), cam_q=q, cam_t=t,
-                        frame_model=np.zeros(len(frames), np.int32),
-                        models=np.array([[0, 500.0, 500.0, 320.0, 240.0, 0.0, 0.0]]),
+                        frame_model=frame_model, models=models,
                         track_ptr=ptr, obs_frame=of, obs_uv=uv, points=P, mask_in=mask_in,
                         threshold_px=2.0, ref_mask=mask_out, ref_removed=removed,
                         ref_triangulated=status)
@@ -373,6 +375,70 @@ def iterative_map_fixture():
     print(f"iterative_map: tracks={len(tracks)} landmarks={len(smap.landmarks)} rounds={len(rs)}")
 
 
+# --- radial / fisheye camera kinds (cameras.py:57-125) ------
+
+RAD = CameraModel("pinhole_radial", 480.0, 470.0, 318.0, 242.0, 640, 480, (-0.08, 0.02))
+FISH = CameraModel("equidistant_fisheye", 320.0, 320.0, 320.0, 240.0, 640, 480)
+KIND_MODELS = np.array([[1, 480.0, 470.0, 318.0, 242.0, -0.08, 0.02],
+                        [2, 320.0, 320.0, 320.0, 240.0, 0.0, 0.0]])
+
+
+def observations_cams(point, poses, cam_of, noise=0.0, rng=None):
+    obs = []
+    for f in sorted(poses):
+        cam = cam_of[f]
+        try:
+            pix = project(cam, poses[f], point)
+        except Exception:  # noqa: BLE001 -- outside the model domain: not observed
+            continue
+        if not (0 <= pix[0] < cam.width and 0 <= pix[1] < cam.height):
+            continue
+        if noise and rng is not None:
+            pix = pix + rng.normal(0, noise, 2)
+        obs.append(M.Observation(f, 0, pix))
+    return obs
+
+
+def camera_kinds_fixtures():
+    rng = np.random.default_rng(31)
+    pts, poses = scene(rng, 8, 70)
+    cam_id = {f: f % 2 for f in poses}
+    cams = {0: RAD, 1: FISH}
+    cam_of = {f: cams[cam_id[f]] for f in poses}
+    kfs = {f: Keyframe(f, float(f), cam_id[f], poses[f]) for f in poses}
+    smap = M.SparseMap(kfs, cams, fixed_frames={0})
+    for p in pts:
+        obs = observations_cams(p, poses, cam_of, 0.3, rng)
+        if len(obs) < 2:
+            continue
+        smap.landmarks.append(M.Landmark(p.copy(), M.Track(obs, status=M.TRIANGULATED),
+                                         np.ones(len(obs), bool)))
+    for f in poses:
+        if f != 0:
+            kfs[f].cam_from_world = exp_map(rng.normal(0, 0.003, 6)) @ kfs[f].cam_from_world
+    for lm in smap.landmarks:
+        lm.position = lm.position + rng.normal(0, 0.015, 3)
+    run_ba("camera_kinds", smap, M.MappingConfig(max_solver_iters=30), stage=1)
+    # RANSAC triangulation with the same two camera kinds
+    for method in ("dlt", "midpoint"):
+        rng = np.random.default_rng(37)
+        pts, poses = scene(rng, 8, 90, spacing=0.6)
+        cam_of = {f: (RAD if f % 2 == 0 else FISH) for f in poses}
+        tracks = []
+        for i, p in enumerate(pts):
+            obs = observations_cams(p, poses, cam_of, 0.4, rng)
+            if len(obs) < 2:
+                continue
+            if i % 4 == 0 and len(obs) >= 3:
+                k = int(rng.integers(len(obs)))
+                obs[k] = M.Observation(obs[k].frame_id, 0,
+                                       obs[k].pixel + rng.uniform(15, 60, 2) * rng.choice([-1, 1], 2))
+            tracks.append(M.Track(obs))
+        track_fixture("kinds_" + method, tracks, poses, 4.0, np.radians(0.5), method,
+                      cams_of={f: ((0, RAD) if f % 2 == 0 else (1, FISH)) for f in poses},
+                      models=KIND_MODELS)
+
+
 # --- known-answer vectors for the geometry --------------------------------------
 
 def kat_fixture():
@@ -412,9 +478,11 @@ def kat_fixture():
 
 
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["kat", "tri", "gate", "imap", "ba"]
+    which = sys.argv[1:] or ["kat", "tri", "gate", "imap", "ba", "kinds"]
     if "kat" in which:
         kat_fixture()
+    if "kinds" in which:
+        camera_kinds_fixtures()
     if "tri" in which:
         tri_fixtures()
     if "gate" in which:

@@ -9,7 +9,7 @@ import pytest
 pytestmark = pytest.mark.gpu
 
 BA_CASES = ["plain_stage2", "huber_outliers", "cauchy_pose_terms", "localization_fixed",
-            "localization_adjust", "prior_gauge", "pure_provenance_lc", "config1"]
+            "localization_adjust", "prior_gauge", "pure_provenance_lc", "config1", "camera_kinds"]
 LOSS_NAMES = {0: "trivial", 1: "huber", 2: "cauchy"}
 
 
@@ -145,10 +145,11 @@ def tracks_struct(d):
     return s, keep
 
 
-@pytest.mark.parametrize("method", ["dlt", "midpoint"])
-def test_ransac_matches_reference(golden, method):
+@pytest.mark.parametrize("case", ["dlt", "midpoint", "kinds_dlt", "kinds_midpoint"])
+def test_ransac_matches_reference(golden, case):
     from paper_2510_15271_b200 import _native as nat
-    d = golden("tri_" + method)
+    method = case.split("_")[-1]
+    d = golden("tri_" + case)
     s, keep = tracks_struct(d)
     T = len(keep["ptr"]) - 1
     X = np.empty((T, 3))

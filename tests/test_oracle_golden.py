@@ -9,7 +9,7 @@ from oracle import geometry as G
 from oracle import tri as OT
 
 BA_CASES = ["plain_stage2", "huber_outliers", "cauchy_pose_terms", "localization_fixed",
-            "localization_adjust", "prior_gauge", "pure_provenance_lc", "config1"]
+            "localization_adjust", "prior_gauge", "pure_provenance_lc", "config1", "camera_kinds"]
 
 
 def models_of(d):
@@ -122,9 +122,10 @@ def test_oracle_geometry_kat(golden):
         np.testing.assert_allclose(w * G.se3_jl_inv(rr), Jp, rtol=1e-11, atol=1e-12)
 
 
-@pytest.mark.parametrize("method", ["dlt", "midpoint"])
-def test_oracle_triangulation_matches_reference(golden, method):
-    d = golden("tri_" + method)
+@pytest.mark.parametrize("case", ["dlt", "midpoint", "kinds_dlt", "kinds_midpoint"])
+def test_oracle_triangulation_matches_reference(golden, case):
+    method = case.split("_")[-1]
+    d = golden("tri_" + case)
     fr = OT.Frames(d["cam_q"], d["cam_t"], d["frame_model"], models_of(d))
     X, mask, st = OT.ransac_batch(fr, d["track_ptr"], d["obs_frame"], d["obs_uv"],
                                   float(d["threshold_px"]), float(d["min_angle"]), method)

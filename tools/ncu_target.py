@@ -1,5 +1,7 @@
-"""Small driver for ncu captures: a few LM iterations on a config scene with
-the bench's solver options (bench.py).  usage: ncu_target.py [CFG] [ITERS]"""
+"""Small driver for ncu captures: LM iterations on a config scene with the
+bench's solver options (bench.py), one iterate() call per LM iteration so
+the per-iteration PCG counts can be matched to captured launches.
+usage: ncu_target.py [CFG] [ITERS]"""
 import sys
 sys.path.insert(0, ".")
 from paper_2510_15271_b200.scenes import config_scene, scene_arrays
@@ -10,5 +12,9 @@ iters = int(sys.argv[2]) if len(sys.argv) > 2 else 2
 a = scene_arrays(config_scene(cfg, seed=0))
 ba = DeviceBA(a, RobustLoss("huber", 2.0), SolverOptions(max_iters=100),
               DeviceOptions(linear_solver="pcg", pcg_rtol=1e-10, pcg_max_iters=500))
-r = ba.iterate(iters)
-print("iters", r.iterations, "trials", r.n_trials, "pcg", r.pcg_iterations, "ms", r.device_ms)
+prev = 0
+for i in range(iters):
+    r = ba.iterate(1)
+    print(f"LM iteration {r.iterations}: trials {r.n_trials} pcg iterations {r.pcg_iterations - prev} "
+          f"device {r.device_ms:.3f} ms", flush=True)
+    prev = r.pcg_iterations
