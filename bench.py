@@ -18,7 +18,6 @@ from __future__ import annotations
 import argparse
 import json
 import os
-import subprocess
 import sys
 import time
 
@@ -63,54 +62,54 @@ def max_over_ranks(x, world):
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clocks and throttle reasons sampled DURING the timed region: NVML
+    (nvidia-ml-py) polled from a thread every 2 ms (the timed region is tens
+    of milliseconds, too short for `nvidia-smi -lms`), nvidia-smi fallback."""
 
-    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+               "sw_power_cap": 0x4}
 
     def __init__(self, device):
         self.device = device
-        self.proc = None
+        self.samples = []
+        self.reasons = set()
+        self.smax = None
 
     def __enter__(self):
+        import threading
+        self.stop = threading.Event()
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-        except OSError:
-            self.proc = None
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.device)
+            self.smax = float(pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM))
+
+            def poll():
+                while not self.stop.is_set():
+                    try:
+                        self.samples.append(float(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)))
+                        bits = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                        for n, m in self.REASONS.items():
+                            if bits & m:
+                                self.reasons.add(n)
+                    except Exception:
+                        pass
+                    self.stop.wait(0.002)
+            self.th = threading.Thread(target=poll, daemon=True)
+            self.th.start()
+        except Exception:
+            self.th = None
         return self
 
     def __exit__(self, *exc):
-        self.lines = []
-        if self.proc:
-            self.proc.terminate()
-            try:
-                out, _ = self.proc.communicate(timeout=5)
-            except subprocess.TimeoutExpired:
-                self.proc.kill()
-                out, _ = self.proc.communicate()
-            self.lines = [ln for ln in out.splitlines() if ln.strip()]
+        self.stop.set()
+        if self.th:
+            self.th.join()
 
     def summary(self):
-        sm, smax, reasons = [], 0.0, set()
-        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
-        for ln in getattr(self, "lines", []):
-            parts = [p.strip() for p in ln.split(",")]
-            if len(parts) < 8:
-                continue
-            try:
-                sm.append(float(parts[0]))
-                smax = max(smax, float(parts[1]))
-            except ValueError:
-                continue
-            for n, v in zip(names, parts[4:8]):
-                if v.lower().startswith("active"):
-                    reasons.add(n)
-        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": smax or None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+        return {"sm_mhz": float(np.median(self.samples)) if self.samples else None,
+                "sm_max_mhz": self.smax, "reasons": sorted(self.reasons),
+                "samples": len(self.samples), "source": "NVML, 2 ms polling during the timed region"}
 
 
 def build_workload(seed):
@@ -174,6 +173,33 @@ def run_reference(args, rank, world):
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+# profiler entry -> kernel symbol in the committed ncu capture (profiles/traffic.json)
+PROF_KERNEL = {"pcg": "k_pcg3", "schur_offdiag": "k_offdiag_blocks", "schur_diag": "k_cam_blocks<1>",
+               "cam_lin": "k_cam_blocks<0>", "point_lin": "k_point_lin", "point_trial": "k_point_cost<1>",
+               "point_prep": "k_point_prep"}
+
+
+def measured_traffic(prof_name, ent, pcg_iters_timed):
+    """DRAM bytes (read + write) per launch of the dominant kernel from the
+    committed `ncu --set full` capture.  The PCG launch runs a data-dependent
+    number of iterations, so its capture is normalised per PCG iteration and
+    scaled to this run's mean iterations per launch."""
+    path = os.path.join(REPO, "profiles", "traffic.json")
+    k = PROF_KERNEL.get(prof_name)
+    if not k or not os.path.exists(path):
+        return None, None
+    t = json.load(open(path))
+    e = t["kernels"].get(k)
+    if e is None:
+        return None, None
+    if "dram_bytes_per_pcg_iteration" in e:
+        per_launch_its = pcg_iters_timed / max(ent["launches"], 1)
+        return e["dram_bytes_per_pcg_iteration"] * per_launch_its, (
+            f"{t['source']}: {e['dram_bytes_per_pcg_iteration'] / 1e6:.2f} MB DRAM per PCG iteration "
+            f"x {per_launch_its:.1f} iterations per launch in this run")
+    return e["dram_bytes_per_launch"], t["source"]
 
 
 def workload_config(sc, world):
@@ -254,6 +280,7 @@ def main():
         if os.path.exists(os.path.join(REPO, "MEASURED_PEAKS.json")) else {"hbm_gbs": 6650.0}
     peak = float(peaks.get("hbm_gbs", 6650.0))
     achieved = bytes_per_launch / (avg_ms / 1000.0) / 1e9 if avg_ms > 0 else 0.0
+    traffic, traffic_src = measured_traffic(name, ent, rep1.pcg_iterations - rep.pcg_iterations)
 
     # ---- end-to-end through the C-ABI with host buffers (e2e) -----------------
     e2e = None
@@ -308,7 +335,8 @@ def main():
             "n_blocks_S": int(rep1.n_blocks_S),
             "roofline": {"kernel": name, "bound": "hbm", "achieved": achieved, "peak": peak,
                          "unit": "GB/s", "frac": achieved / peak if peak else None,
-                         "traffic": None, "avg_ms": avg_ms, "bytes_per_launch": bytes_per_launch,
+                         "traffic": traffic, "traffic_source": traffic_src,
+                         "avg_ms": avg_ms, "bytes_per_launch": bytes_per_launch,
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)"},
             "kernels": {k: {"launches": v["launches"], "ms": round(v["ms"], 4),
                             "GBps": (v["bytes"] / (v["ms"] / 1000.0) / 1e9) if v["ms"] > 0 and v["bytes"] else None}
