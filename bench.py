@@ -29,6 +29,7 @@ sys.path.insert(0, REPO)
 METRIC = "BA LM iterations/s and residual+Jacobian obs/s at 1/2/4/8 B200 vs CPU ref"
 UNIT = "LM iterations/s"
 CPU_SAMPLE_FRAC = 0.10   # oracle runs on all cameras + the first 10% of the points
+PCG_RTOL = 1e-8
 
 
 def dist_init(args):
@@ -206,6 +207,7 @@ def workload_config(sc, world):
     return {"workload": "config 3: synthetic BAL-Venice-shaped BA (ring of cameras around a "
                         "plaza, random co-visible subsets), 1 LM iteration per step",
             "cameras": sc.n_frames, "points": sc.n_points, "observations": sc.n_obs,
+            "pcg_rtol": PCG_RTOL,
             "loss": "huber(2.0)", "lambda_c": 1.0, "lambda_a": 1.0, "seed": sc.seed,
             "parallelism": f"point-shard x{world}" if world > 1 else "single GPU",
             "l2": "inputs larger than L2 (observation + pair streams >> 126 MB per iteration)"}
@@ -244,7 +246,10 @@ def main():
     loss = RobustLoss("huber", 2.0)
     total = args.warmup + args.steps
     sopt = SolverOptions(max_iters=total + 1000)
-    dopt = DeviceOptions(linear_solver="pcg", pcg_rtol=1e-10, pcg_max_iters=500)
+    # PCG relative tolerance 1e-8: after several LM iterations the poses /
+    # points deviate from the exact-solve oracle by ~1e-10 (tools/rtol_check.py,
+    # tests/test_gpu_configs.py), four orders inside the 1e-6 parity bar
+    dopt = DeviceOptions(linear_solver="pcg", pcg_rtol=PCG_RTOL, pcg_max_iters=500)
 
     # ---- device-resident LM iterations (value) -------------------------------
     ba = DeviceBA(part, loss, sopt, dopt, ctx)

@@ -11,7 +11,7 @@ cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 3
 iters = int(sys.argv[2]) if len(sys.argv) > 2 else 2
 a = scene_arrays(config_scene(cfg, seed=0))
 ba = DeviceBA(a, RobustLoss("huber", 2.0), SolverOptions(max_iters=100),
-              DeviceOptions(linear_solver="pcg", pcg_rtol=1e-10, pcg_max_iters=500))
+              DeviceOptions(linear_solver="pcg", pcg_rtol=1e-8, pcg_max_iters=500))
 prev = 0
 for i in range(iters):
     r = ba.iterate(1)
