@@ -25,7 +25,7 @@
 extern "C" {
 #endif
 
-#define SFM_ABI_VERSION 2
+#define SFM_ABI_VERSION 3
 
 /* ---- error codes (mapped to sfmkit.errors classes by the Python layer) --- */
 #define SFM_OK 0
@@ -264,6 +264,82 @@ int sfm_gate(sfm_ctx* ctx, const sfm_tracks* tracks, const double* points,
  */
 int sfm_reprojection_errors(sfm_ctx* ctx, const sfm_tracks* tracks,
                             const double* points, double* out_err);
+
+/* ---- device-resident iterative mapping ---------------------------------- */
+/* Track status (Track.status, mapping.py:48-52): in/out of sfm_iterative_map */
+#define SFM_TRACK_PENDING 0
+#define SFM_TRACK_TRIANGULATED 1
+#define SFM_TRACK_FAILED 2
+
+/*
+ * The inputs of iterative_map (mapping.py:569-571) flattened: frames (sorted
+ * keyframe ids) with the fixed set already resolved (anchor frame,
+ * mapping.py:583-593), the pose terms every bundle_adjust call of the loop
+ * builds (lambda_c consecutive-frame edges, lambda_a priors; mapping.py:477-
+ * 509), and the tracks as CSR in track order.
+ */
+typedef struct {
+  int32_t n_frames;
+  int32_t n_models;
+  const double* cam_q;          /* [n_frames,4] initial poses              */
+  const double* cam_t;          /* [n_frames,3]                            */
+  const int32_t* frame_model;   /* [n_frames]                              */
+  const uint8_t* frame_fixed;   /* [n_frames]                              */
+  const sfm_camera_model* models;
+  int64_t n_tracks;
+  int64_t n_obs;
+  const int64_t* track_ptr;     /* [n_tracks+1]                            */
+  const int32_t* obs_frame;     /* [n_obs]                                 */
+  const double* obs_uv;         /* [n_obs,2]                               */
+  const int8_t* track_status;   /* [n_tracks] SFM_TRACK_* (NULL = pending) */
+  int32_t n_edges;
+  int32_t n_priors;
+  const int32_t* edge_ab;       /* [n_edges,2]                             */
+  const int32_t* prior_frame;   /* [n_priors]                              */
+  double edge_weight;           /* lambda_c                                */
+  double prior_weight;          /* lambda_a                                */
+} sfm_map_problem;
+
+/* MappingConfig (mapping.py:84-108) + the B200 solver knobs of each BA. */
+typedef struct {
+  int32_t max_outer_iters;
+  int32_t max_solver_iters;
+  int32_t stage1_loss_kind;
+  int32_t stage2_loss_kind;
+  double stage1_loss_param;
+  double stage2_loss_param;
+  double stage1_outlier_px;
+  double stage2_outlier_px;
+  double min_angle;             /* min_triangulation_angle (radians)       */
+  int32_t method;               /* SFM_TRI_DLT / SFM_TRI_MIDPOINT          */
+  int32_t _pad;
+  sfm_ba_options solver;        /* loss / max_iters fields ignored         */
+} sfm_map_options;
+
+typedef struct {
+  int32_t round;                /* -1 = the final stage-2 pass             */
+  int32_t _pad;
+  int64_t added;
+  int64_t removed;
+  int64_t landmarks;
+} sfm_round_stat;
+
+/*
+ * Replaces iterative_map (mapping.py:569-624) with the whole loop on the
+ * device: rounds of {RANSAC-triangulate PENDING tracks -> stage-1 BA over
+ * the landmarks -> stage-1 outlier gate (demoted tracks back to PENDING)}
+ * until a round neither adds nor removes (cap max_outer_iters), then stage-2
+ * BA + gate.  Tracks, masks, landmark positions and the landmark order stay
+ * on the device between rounds.  Outputs: final poses, per-track position
+ * ([n_tracks,3], NaN if not a landmark), per-observation inlier mask, per-
+ * track status, the landmarks as track ids in map order (out_lm_track
+ * [n_tracks], *out_n_landmarks of them) and the round statistics
+ * (out_stats [max_outer_iters+1], *out_n_stats).
+ */
+int sfm_iterative_map(sfm_ctx* ctx, const sfm_map_problem* prob, const sfm_map_options* opt,
+                      double* out_cam_q, double* out_cam_t, double* out_X, uint8_t* out_mask,
+                      int8_t* out_status, int64_t* out_lm_track, int64_t* out_n_landmarks,
+                      sfm_round_stat* out_stats, int32_t* out_n_stats);
 
 #ifdef __cplusplus
 }

@@ -17,7 +17,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libsfm_b200.so")
 
 # ---- constants (mirror include/sfm_b200.h) ---------------------------------
-ABI_VERSION = 2
+ABI_VERSION = 3
 SFM_OK = 0
 SFM_E_INVALID = -1
 SFM_E_NON_POSITIVE_DEPTH = -2
@@ -49,8 +49,10 @@ EXPORTED_SYMBOLS = (
     "sfm_last_error", "sfm_set_profiling", "sfm_prof_count", "sfm_prof_get",
     "sfm_prof_reset", "sfm_ba_solve", "sfm_ba_setup", "sfm_ba_iterate",
     "sfm_ba_download", "sfm_ba_eval", "sfm_ransac_triangulate", "sfm_triangulate",
-    "sfm_gate", "sfm_reprojection_errors",
+    "sfm_gate", "sfm_reprojection_errors", "sfm_iterative_map",
 )
+
+TRACK_PENDING, TRACK_TRIANGULATED, TRACK_FAILED = 0, 1, 2
 
 _p = ctypes.c_void_p
 
@@ -101,6 +103,31 @@ class TracksC(ctypes.Structure):
                 ("track_ptr", _p), ("obs_frame", _p), ("obs_uv", _p), ("active", _p)]
 
 
+class MapProblemC(ctypes.Structure):
+    _fields_ = [("n_frames", ctypes.c_int32), ("n_models", ctypes.c_int32),
+                ("cam_q", _p), ("cam_t", _p), ("frame_model", _p), ("frame_fixed", _p),
+                ("models", _p), ("n_tracks", ctypes.c_int64), ("n_obs", ctypes.c_int64),
+                ("track_ptr", _p), ("obs_frame", _p), ("obs_uv", _p), ("track_status", _p),
+                ("n_edges", ctypes.c_int32), ("n_priors", ctypes.c_int32),
+                ("edge_ab", _p), ("prior_frame", _p),
+                ("edge_weight", ctypes.c_double), ("prior_weight", ctypes.c_double)]
+
+
+class MapOptionsC(ctypes.Structure):
+    _fields_ = [("max_outer_iters", ctypes.c_int32), ("max_solver_iters", ctypes.c_int32),
+                ("stage1_loss_kind", ctypes.c_int32), ("stage2_loss_kind", ctypes.c_int32),
+                ("stage1_loss_param", ctypes.c_double), ("stage2_loss_param", ctypes.c_double),
+                ("stage1_outlier_px", ctypes.c_double), ("stage2_outlier_px", ctypes.c_double),
+                ("min_angle", ctypes.c_double), ("method", ctypes.c_int32),
+                ("_pad", ctypes.c_int32), ("solver", BAOptionsC)]
+
+
+class RoundStatC(ctypes.Structure):
+    _fields_ = [("round", ctypes.c_int32), ("_pad", ctypes.c_int32),
+                ("added", ctypes.c_int64), ("removed", ctypes.c_int64),
+                ("landmarks", ctypes.c_int64)]
+
+
 _lib = None
 _lib_lock = threading.Lock()
 
@@ -144,6 +171,8 @@ def load_library(path: str = None):
         lib.sfm_triangulate.argtypes = [_p, P(TracksC), c_d, c_i32, _p, _p]
         lib.sfm_gate.argtypes = [_p, P(TracksC), _p, c_d, _p, _p, P(c_i64)]
         lib.sfm_reprojection_errors.argtypes = [_p, P(TracksC), _p, _p]
+        lib.sfm_iterative_map.argtypes = [_p, P(MapProblemC), P(MapOptionsC), _p, _p, _p, _p, _p,
+                                          _p, P(c_i64), _p, P(c_i32)]
         for name in EXPORTED_SYMBOLS:
             if name not in ("sfm_ctx_destroy", "sfm_last_error"):
                 getattr(lib, name).restype = c_int

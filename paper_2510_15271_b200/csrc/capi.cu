@@ -8,6 +8,7 @@
 
 #include "ba.cuh"
 #include "comm.cuh"
+#include "imap.cuh"
 #include "tri.cuh"
 
 struct sfm_ctx {
@@ -164,6 +165,20 @@ int sfm_ba_eval(sfm_ctx* ctx, const sfm_ba_problem* prob, int32_t loss_kind, dou
     SFM_REQUIRE(prob != nullptr, "null problem");
     sfm::BASolver::eval(ctx->stream, &ctx->prof, *prob, loss_kind, loss_param, out_cost_per_obs, out_res,
                         out_jc, out_jp);
+  });
+}
+
+int sfm_iterative_map(sfm_ctx* ctx, const sfm_map_problem* prob, const sfm_map_options* opt,
+                      double* out_cam_q, double* out_cam_t, double* out_X, uint8_t* out_mask,
+                      int8_t* out_status, int64_t* out_lm_track, int64_t* out_n_landmarks,
+                      sfm_round_stat* out_stats, int32_t* out_n_stats) {
+  return guarded(ctx, [&] {
+    SFM_REQUIRE(prob && opt && out_cam_q && out_cam_t && out_X && out_mask && out_status && out_lm_track &&
+                    out_n_landmarks && out_stats && out_n_stats,
+                "null argument");
+    ctx->ba.reset();  // device memory back to the pool
+    sfm::iterative_map(ctx->stream, &ctx->prof, *prob, *opt, out_cam_q, out_cam_t, out_X, out_mask, out_status,
+                       out_lm_track, out_n_landmarks, out_stats, out_n_stats);
   });
 }
 

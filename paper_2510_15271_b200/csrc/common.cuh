@@ -76,12 +76,14 @@ struct DevBuf {
   }
   T* get() const { return ptr; }
   size_t bytes() const { return n * sizeof(T); }
-  void upload(const T* host, size_t count, cudaStream_t s) {
+  // `src` / `dst` may be host or device memory (unified addressing): the
+  // C-ABI passes host arrays, the device-resident mapping loop device arrays.
+  void upload(const T* src, size_t count, cudaStream_t s) {
     resize(count);
-    if (count) SFM_CUDA(cudaMemcpyAsync(ptr, host, count * sizeof(T), cudaMemcpyHostToDevice, s));
+    if (count) SFM_CUDA(cudaMemcpyAsync(ptr, src, count * sizeof(T), cudaMemcpyDefault, s));
   }
-  void download(T* host, size_t count, cudaStream_t s) const {
-    if (count) SFM_CUDA(cudaMemcpyAsync(host, ptr, count * sizeof(T), cudaMemcpyDeviceToHost, s));
+  void download(T* dst, size_t count, cudaStream_t s) const {
+    if (count) SFM_CUDA(cudaMemcpyAsync(dst, ptr, count * sizeof(T), cudaMemcpyDefault, s));
   }
   void zero(cudaStream_t s) {
     if (n) SFM_CUDA(cudaMemsetAsync(ptr, 0, n * sizeof(T), s));

@@ -1,0 +1,11 @@
+// imap.cuh -- device-resident iterative_map (mapping.py:569-624).
+#pragma once
+#include "common.cuh"
+
+namespace sfm {
+
+void iterative_map(cudaStream_t s, Profiler* prof, const sfm_map_problem& prob, const sfm_map_options& opt,
+                   double* out_q, double* out_t, double* out_X, uint8_t* out_mask, int8_t* out_status,
+                   int64_t* out_lm, int64_t* out_nlm, sfm_round_stat* out_stats, int32_t* out_nstats);
+
+}  // namespace sfm

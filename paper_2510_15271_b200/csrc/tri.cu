@@ -607,6 +607,44 @@ void tri_gate(cudaStream_t s, Profiler* prof, const sfm_tracks& tr, const double
   if (out_removed) *out_removed = (int64_t)h;
 }
 
+namespace {
+TriData tri_data(const TriDeviceTracks& tr) {
+  TriData d{};
+  d.of = tr.obs_frame; d.uv = tr.obs_uv; d.ray = tr.ray; d.ray_st = tr.ray_st; d.Rt = tr.Rt;
+  d.fm = tr.frame_model; d.models = tr.models;
+  return d;
+}
+}  // namespace
+
+void tri_rt_device(cudaStream_t s, int F, const double* q, const double* t, double* Rt) {
+  if (F) k_rt<<<grid_for(F, 128), 128, 0, s>>>(F, q, t, Rt);
+  SFM_CHECK_LAUNCH();
+}
+
+void tri_rays_device(cudaStream_t s, Profiler* prof, const TriDeviceTracks& tr, double* ray, int* ray_st) {
+  if (!tr.n_obs) return;
+  ProfScope ps(*prof, "tri_rays", 48.0 * tr.n_obs, s);
+  k_rays<<<grid_for(tr.n_obs, 128), 128, 0, s>>>(tr.n_obs, tri_data(tr), ray, ray_st);
+}
+
+void tri_ransac_device(cudaStream_t s, Profiler* prof, const TriDeviceTracks& tr, const uint8_t* active,
+                       double thr, double min_angle, int method, double* X, uint8_t* mask, int8_t* status) {
+  if (!tr.n_tracks) return;
+  TrackArgs a{};
+  a.T = tr.n_tracks; a.ptr = tr.ptr; a.active = active; a.d = tri_data(tr);
+  a.thr = thr; a.min_angle = min_angle; a.method = method; a.X = X; a.mask = mask; a.status = status;
+  ProfScope ps(*prof, "tri_ransac", 24.0 * tr.n_obs + 24.0 * tr.n_tracks + tr.n_obs, s);
+  k_ransac<<<grid_for(tr.n_tracks * 32, 128), 128, 0, s>>>(a);
+}
+
+void tri_gate_device(cudaStream_t s, Profiler* prof, const TriDeviceTracks& tr, const double* P, double thr,
+                     uint8_t* mask, int* inliers, unsigned long long* removed) {
+  if (!tr.n_tracks) return;
+  ProfScope ps(*prof, "gate", 24.0 * tr.n_obs + 24.0 * tr.n_tracks + 2.0 * tr.n_obs, s);
+  k_gate<<<grid_for(tr.n_tracks, 128), 128, 0, s>>>(tr.n_tracks, tr.ptr, tri_data(tr), P, thr, mask, inliers,
+                                                     removed);
+}
+
 void tri_reproj_errors(cudaStream_t s, Profiler* prof, const sfm_tracks& tr, const double* points,
                        double* out_err) {
   validate(tr);

@@ -493,12 +493,116 @@ def remove_outliers(sparse_map, threshold_px: float, ctx=None):
     return sparse_map, removed
 
 
+@dataclass
+class MapResult:
+    """Output of iterative_map_arrays (sfm_iterative_map)."""
+
+    cam_q: np.ndarray          # [F,4] final poses (frame order of the inputs)
+    cam_t: np.ndarray          # [F,3]
+    points: np.ndarray         # [T,3] per track, NaN unless a landmark
+    inlier_mask: np.ndarray    # [N] bool per observation
+    status: np.ndarray         # [T] int8 nat.TRACK_*
+    lm_track: np.ndarray       # [L] landmarks as track ids, in map order
+    round_stats: list
+
+
+def _map_options(config: MappingConfig, device: DeviceOptions) -> nat.MapOptionsC:
+    dev = device or DEFAULT_DEVICE_OPTIONS
+    return nat.MapOptionsC(
+        int(config.max_outer_iters), int(config.max_solver_iters),
+        nat.LOSS_KINDS[config.stage1.loss.kind], nat.LOSS_KINDS[config.stage2.loss.kind],
+        float(config.stage1.loss.param), float(config.stage2.loss.param),
+        float(config.stage1.outlier_px), float(config.stage2.outlier_px),
+        float(config.min_triangulation_angle), nat.TRI_METHODS[config.triangulation], 0,
+        _options(TRIVIAL_LOSS, SolverOptions(max_iters=config.max_solver_iters), dev))
+
+
+def iterative_map_arrays(cam_q, cam_t, frame_model, frame_fixed, models, n_models, track_ptr,
+                         obs_frame, obs_uv, edge_ab=None, prior_frame=None,
+                         config: MappingConfig = None, track_status=None,
+                         device: DeviceOptions = None, ctx=None) -> MapResult:
+    """iterative_map (mapping.py:569-624) on flattened arrays, the whole loop
+    device-resident (sfm_iterative_map): frames with the fixed set resolved,
+    tracks as CSR in track order, the pose terms each bundle_adjust builds
+    (lambda_c / lambda_a weights from `config`)."""
+    config = config or MappingConfig()
+    ctx = ctx or nat.default_context()
+    keep = dict(q=np.ascontiguousarray(cam_q, dtype=np.float64),
+                t=np.ascontiguousarray(cam_t, dtype=np.float64),
+                fm=np.ascontiguousarray(frame_model, dtype=np.int32),
+                fx=np.ascontiguousarray(frame_fixed, dtype=np.uint8),
+                ptr=np.ascontiguousarray(track_ptr, dtype=np.int64),
+                of=np.ascontiguousarray(obs_frame, dtype=np.int32),
+                uv=np.ascontiguousarray(obs_uv, dtype=np.float64).reshape(-1, 2),
+                ab=np.ascontiguousarray(edge_ab if edge_ab is not None else np.zeros((0, 2)),
+                                        dtype=np.int32).reshape(-1, 2),
+                pf=np.ascontiguousarray(prior_frame if prior_frame is not None else np.zeros(0),
+                                        dtype=np.int32))
+    F, T, N = len(keep["fm"]), len(keep["ptr"]) - 1, len(keep["of"])
+    st_in = None
+    if track_status is not None:
+        st_in = np.ascontiguousarray(track_status, dtype=np.int8)
+    prob = nat.MapProblemC(
+        F, n_models, nat.ptr(keep["q"]), nat.ptr(keep["t"]), nat.ptr(keep["fm"]),
+        nat.ptr(keep["fx"]), ctypes.addressof(models), T, N, nat.ptr(keep["ptr"]),
+        nat.ptr(keep["of"]), nat.ptr(keep["uv"]), nat.ptr(st_in), len(keep["ab"]), len(keep["pf"]),
+        nat.ptr(keep["ab"]), nat.ptr(keep["pf"]),
+        float(config.lambda_c) if len(keep["ab"]) else 0.0,
+        float(config.lambda_a) if len(keep["pf"]) else 0.0)
+    opt = _map_options(config, device)
+    q = np.empty((F, 4))
+    t = np.empty((F, 3))
+    X = np.empty((T, 3))
+    mask = np.empty(N, np.uint8)
+    status = np.empty(T, np.int8)
+    lm = np.empty(max(T, 1), np.int64)
+    nlm = ctypes.c_int64()
+    stats = (nat.RoundStatC * (int(config.max_outer_iters) + 1))()
+    nst = ctypes.c_int32()
+    ctx.check(ctx.lib.sfm_iterative_map(ctx.handle, ctypes.byref(prob), ctypes.byref(opt),
+                                        nat.ptr(q), nat.ptr(t), nat.ptr(X), nat.ptr(mask),
+                                        nat.ptr(status), nat.ptr(lm), ctypes.byref(nlm),
+                                        ctypes.addressof(stats), ctypes.byref(nst)))
+    rs = [{"round": (stats[i].round if stats[i].round >= 0 else "final"),
+           "added": int(stats[i].added), "removed": int(stats[i].removed),
+           "landmarks": int(stats[i].landmarks)} for i in range(nst.value)]
+    return MapResult(q, t, X, mask.astype(bool), status, lm[:nlm.value].copy(), rs)
+
+
+def _pose_terms(frames, fidx, sparse_map, config, fixed, mode):
+    """The lambda_c edges / lambda_a priors bundle_adjust builds
+    (mapping.py:477-509), as frame-index arrays (same as flatten_ba)."""
+    edges = []
+    if config.lambda_c > 0:
+        by_cam = {}
+        for f in frames:
+            by_cam.setdefault(sparse_map.keyframes[f].camera_id, []).append(f)
+        for seq in by_cam.values():
+            edges.extend((fidx[a], fidx[b]) for a, b in zip(seq, seq[1:]))
+    priors = []
+    if config.lambda_a > 0:
+        for f in frames:
+            if f in fixed:
+                continue
+            if mode == PURE and sparse_map.provenance.get(f) == "prior":
+                continue
+            priors.append(fidx[f])
+    return (np.asarray(edges, dtype=np.int32).reshape(-1, 2), np.asarray(priors, dtype=np.int32))
+
+
+_STATUS_CODE = {PENDING: nat.TRACK_PENDING, TRIANGULATED: nat.TRACK_TRIANGULATED,
+                FAILED: nat.TRACK_FAILED}
+_STATUS_NAME = {v: k for k, v in _STATUS_CODE.items()}
+
+
 def iterative_map(keyframes, tracks, cameras, config: MappingConfig = None, rig=None,
                   mode: str = PURE, provenance=None, fixed_frames=None, device=None,
                   ctx=None) -> SparseMap:
-    """mapping.py:569-624: rounds of {batched RANSAC triangulation of pending
-    tracks -> stage-1 BA -> 4 px gate} until a round neither adds nor
-    removes, then stage-2 BA and the 2 px gate."""
+    """mapping.py:569-624: rounds of {RANSAC triangulation of pending tracks
+    -> stage-1 BA -> 4 px gate} until a round neither adds nor removes, then
+    stage-2 BA and the 2 px gate -- one device-resident call
+    (iterative_map_arrays / sfm_iterative_map); the object model is read
+    once and written back once."""
     if config is None:
         config = MappingConfig()
     kf_map = {kf.frame_id: kf for kf in keyframes}
@@ -509,32 +613,41 @@ def iterative_map(keyframes, tracks, cameras, config: MappingConfig = None, rig=
     if not sparse_map.fixed_frames and kf_map and needs_anchor:
         new = [f for f in kf_map if sparse_map.provenance.get(f) != "prior"]
         sparse_map.fixed_frames = {min(new) if new else min(kf_map)}
-    stats = []
-    for round_idx in range(config.max_outer_iters):
-        poses = {f: kf.cam_from_world for f, kf in kf_map.items()}
-        cams = {f: sparse_map.camera_of(f) for f in kf_map}
-        pending = [t for t in tracks if t.status == PENDING]
-        results = ransac_triangulate_batch(
-            pending, poses, cams, threshold_px=config.stage1.outlier_px,
-            min_angle=config.min_triangulation_angle, method=config.triangulation, ctx=ctx)
-        added = 0
-        for lm in results:
-            if lm is not None:
-                sparse_map.landmarks.append(lm)
-                added += 1
-        if sparse_map.landmarks:
-            bundle_adjust(sparse_map, config, stage=1, mode=mode, device=device, ctx=ctx)
-        _, removed = remove_outliers(sparse_map, config.stage1.outlier_px, ctx=ctx)
-        stats.append({"round": round_idx, "added": added, "removed": removed,
-                      "landmarks": len(sparse_map.landmarks)})
-        if added == 0 and removed == 0:
-            break
-    if sparse_map.landmarks:
-        bundle_adjust(sparse_map, config, stage=2, mode=mode, device=device, ctx=ctx)
-        _, removed = remove_outliers(sparse_map, config.stage2.outlier_px, ctx=ctx)
-        stats.append({"round": "final", "added": 0, "removed": removed,
-                      "landmarks": len(sparse_map.landmarks)})
-    sparse_map.round_stats = stats
+    frames = sorted(kf_map)
+    fixed = set(sparse_map.fixed_frames)
+    if mode == LOCALIZATION_FIXED:
+        fixed |= {f for f in frames if sparse_map.provenance.get(f) == "prior"}
+    _check_supported(sparse_map, frames, mode)
+    if mode != RIG_EXTRINSIC and not fixed and config.lambda_a <= 0:
+        raise NoGauge("no fixed pose and no absolute prior")
+    fidx = {f: i for i, f in enumerate(frames)}
+    cam_q = np.array([kf_map[f].cam_from_world.quat for f in frames]).reshape(-1, 4)
+    cam_t = np.array([kf_map[f].cam_from_world.t for f in frames]).reshape(-1, 3)
+    models, n_models, fm = model_table([sparse_map.camera_of(f) for f in frames])
+    fixed_arr = np.array([1 if f in fixed else 0 for f in frames], dtype=np.uint8)
+    edges, priors = _pose_terms(frames, fidx, sparse_map, config, fixed, mode)
+    counts = np.fromiter((len(t.observations) for t in tracks), dtype=np.int64, count=len(tracks))
+    ptr = np.zeros(len(tracks) + 1, dtype=np.int64)
+    np.cumsum(counts, out=ptr[1:])
+    of = np.fromiter((fidx[o.frame_id] for t in tracks for o in t.observations), dtype=np.int32,
+                     count=int(ptr[-1]))
+    uv = np.array([o.pixel for t in tracks for o in t.observations], dtype=np.float64).reshape(-1, 2)
+    st_in = np.array([_STATUS_CODE[t.status] for t in tracks], dtype=np.int8)
+    res = iterative_map_arrays(cam_q, cam_t, fm, fixed_arr, models, n_models, ptr, of, uv, edges,
+                               priors, config, st_in, device, ctx)
+    for i, f in enumerate(frames):
+        if fixed_arr[i]:
+            continue
+        if np.array_equal(res.cam_q[i], cam_q[i]) and np.array_equal(res.cam_t[i], cam_t[i]):
+            continue
+        kf = kf_map[f]
+        kf.cam_from_world = type(kf.cam_from_world)(res.cam_q[i], res.cam_t[i])
+    for i, tr in enumerate(tracks):
+        tr.status = _STATUS_NAME[int(res.status[i])]
+    sparse_map.landmarks = [Landmark(res.points[i].copy(), tracks[i],
+                                     res.inlier_mask[ptr[i]:ptr[i + 1]].copy())
+                            for i in res.lm_track]
+    sparse_map.round_stats = res.round_stats
     return sparse_map
 
 
@@ -555,7 +668,8 @@ __all__ = [
     "RIG_EXTRINSIC", "Observation", "Track", "Landmark", "SparseMap", "StageConfig",
     "MappingConfig", "BAArrays", "flatten_ba", "solve_arrays", "shard_ranges", "bundle_adjust",
     "triangulate_dlt", "triangulate_midpoint", "reprojection_error", "ransac_triangulate",
-    "ransac_triangulate_batch", "remove_outliers", "iterative_map", "mean_reprojection_error",
+    "ransac_triangulate_batch", "remove_outliers", "iterative_map", "iterative_map_arrays",
+    "MapResult", "mean_reprojection_error",
     "CameraModel", "Keyframe",
 ]
 

@@ -336,17 +336,24 @@ def gate_fixture():
     print(f"gate: L={len(tri)} removed={removed} demoted={int((status == 0).sum())}")
 
 
-def iterative_map_fixture():
-    rng = np.random.default_rng(42)
-    pts, poses = scene(rng, 6, 30)
+def iterative_map_fixture(name="iterative_map", seed=42, n_frames=6, n_points=30, config=None,
+                          noise=0.3, mild_every=0):
+    rng = np.random.default_rng(seed)
+    pts, poses = scene(rng, n_frames, n_points)
     kfs = [Keyframe(f, float(f), 0, poses[f]) for f in sorted(poses)]
     tracks = []
     for k, p in enumerate(pts):
-        obs = observations(p, poses, 0.3, rng)
+        obs = observations(p, poses, noise, rng)
         if len(obs) < 3:
             continue
         if k % 5 == 0:
             obs[1] = M.Observation(obs[1].frame_id, 0, obs[1].pixel + np.array([40.0, 30.0]))
+        if mild_every and k % mild_every == 1:
+            # 2-4 px errors: inside RANSAC's 4 px bar, gated by the 2 px stage-2 gate
+            # (and, on short tracks, demoted and re-triangulated)
+            j = len(obs) - 1
+            obs[j] = M.Observation(obs[j].frame_id, 0, obs[j].pixel + rng.uniform(2.5, 3.8, 2) *
+                                   rng.choice([-1, 1], 2) / np.sqrt(2))
         tracks.append(M.Track(obs))
     # perturb the non-anchor initial poses
     for kf in kfs[1:]:
@@ -357,12 +364,12 @@ def iterative_map_fixture():
     ptr[1:] = np.cumsum([len(t.observations) for t in tracks])
     of = np.array([o.frame_id for t in tracks for o in t.observations], np.int32)
     uv = np.array([o.pixel for t in tracks for o in t.observations])
-    smap = M.iterative_map(kfs, tracks, {0: CAM})
+    smap = M.iterative_map(kfs, tracks, {0: CAM}, config=config)
     lm_track = np.array([next(i for i, t in enumerate(tracks) if t is lm.track)
                          for lm in smap.landmarks], np.int64)
     rs = smap.round_stats
     np.savez_compressed(
-        os.path.join(HERE, "iterative_map.npz"), cam_q=q0, cam_t=t0, track_ptr=ptr, obs_frame=of,
+        os.path.join(HERE, f"{name}.npz"), cam_q=q0, cam_t=t0, track_ptr=ptr, obs_frame=of,
         obs_uv=uv, ref_cam_q=np.array([smap.keyframes[f].cam_from_world.quat for f in sorted(poses)]),
         ref_cam_t=np.array([smap.keyframes[f].cam_from_world.t for f in sorted(poses)]),
         ref_lm_track=lm_track, ref_lm_X=np.array([lm.position for lm in smap.landmarks]),
@@ -372,7 +379,8 @@ def iterative_map_fixture():
         ref_round_removed=np.array([r["removed"] for r in rs]),
         ref_round_landmarks=np.array([r["landmarks"] for r in rs]),
         ref_mean_err=M.mean_reprojection_error(smap))
-    print(f"iterative_map: tracks={len(tracks)} landmarks={len(smap.landmarks)} rounds={len(rs)}")
+    print(f"{name}: tracks={len(tracks)} landmarks={len(smap.landmarks)} rounds={len(rs)} "
+          f"added={[r['added'] for r in rs]} removed={[r['removed'] for r in rs]}")
 
 
 # --- radial / fisheye camera kinds (cameras.py:57-125) ------
@@ -489,5 +497,10 @@ if __name__ == "__main__":
         gate_fixture()
     if "imap" in which:
         iterative_map_fixture()
+        # larger: 12 frames, outliers re-gated across rounds, Cauchy stage 1
+        iterative_map_fixture("iterative_map_large", seed=77, n_frames=12, n_points=160,
+                              config=M.MappingConfig(stage1=M.StageConfig(4.0, SV.RobustLoss("cauchy", 1.0)),
+                                                     lambda_c=0.5, lambda_a=2.0, max_solver_iters=25),
+                              noise=0.8, mild_every=3)
     if "ba" in which:
         ba_fixtures()

@@ -28,7 +28,7 @@ def test_library_loads_and_exports_every_symbol():
     lib = nat.load_library()
     for name in header_functions():
         assert hasattr(lib, name), name
-    assert lib.sfm_abi_version() == 2
+    assert lib.sfm_abi_version() == 3
 
 
 def test_ctypes_struct_layout_matches_header(tmp_path):
@@ -38,7 +38,8 @@ def test_ctypes_struct_layout_matches_header(tmp_path):
     import subprocess
     structs = {"sfm_camera_model": nat.CameraModelC, "sfm_ba_problem": nat.BAProblemC,
                "sfm_ba_options": nat.BAOptionsC, "sfm_ba_report": nat.BAReportC,
-               "sfm_tracks": nat.TracksC}
+               "sfm_tracks": nat.TracksC, "sfm_map_problem": nat.MapProblemC,
+               "sfm_map_options": nat.MapOptionsC, "sfm_round_stat": nat.RoundStatC}
     lines = ["#include <stdio.h>", "#include <stddef.h>", '#include "sfm_b200.h"', "int main(void){"]
     for cname, cls in structs.items():
         lines.append(f'printf("{cname} %zu\\n", sizeof({cname}));')

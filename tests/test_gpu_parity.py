@@ -189,16 +189,29 @@ def test_gate_matches_reference(golden):
     np.testing.assert_array_equal((inl >= 2).astype(np.int8), d["ref_triangulated"])
 
 
-def test_iterative_map_matches_reference(golden):
+def imap_config(case):
+    from paper_2510_15271_b200 import MappingConfig, StageConfig
+    from paper_2510_15271_b200.solver import RobustLoss
+    if case == "iterative_map_large":  # tests/golden/make_golden.py
+        return MappingConfig(stage1=StageConfig(4.0, RobustLoss("cauchy", 1.0)), lambda_c=0.5,
+                             lambda_a=2.0, max_solver_iters=25)
+    return MappingConfig()
+
+
+@pytest.mark.parametrize("case", ["iterative_map", "iterative_map_large"])
+def test_iterative_map_matches_reference(golden, case):
+    """The device-resident loop (sfm_iterative_map) through the object-level
+    drop-in: track status, landmark order, masks, positions, poses and
+    round statistics of sfmkit's iterative_map."""
     from paper_2510_15271_b200 import (CameraModel, Keyframe, Observation, Pose, Track,
                                        iterative_map, mean_reprojection_error)
-    d = golden("iterative_map")
+    d = golden(case)
     cam = CameraModel("pinhole", 500.0, 500.0, 320.0, 240.0, 640, 480)
     kfs = [Keyframe(f, float(f), 0, Pose(d["cam_q"][f], d["cam_t"][f])) for f in range(len(d["cam_q"]))]
     ptr = d["track_ptr"]
     tracks = [Track([Observation(int(d["obs_frame"][o]), 0, d["obs_uv"][o])
                      for o in range(ptr[i], ptr[i + 1])]) for i in range(len(ptr) - 1)]
-    smap = iterative_map(kfs, tracks, {0: cam})
+    smap = iterative_map(kfs, tracks, {0: cam}, config=imap_config(case))
     stat = np.array([{"pending": 0, "triangulated": 1, "failed": 2}[t.status] for t in tracks])
     np.testing.assert_array_equal(stat, d["ref_status"])
     np.testing.assert_array_equal([r["added"] for r in smap.round_stats], d["ref_round_added"])
