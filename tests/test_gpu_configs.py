@@ -16,6 +16,9 @@ size-independent properties where it does not:
   * configs[3]-shaped triangulation + gating (2k cameras, 5% outliers):
     RANSAC status / masks / removed counts bit-exact against the oracle on
     a random sample of tracks, positions to 1e-9;
+  * configs[1] through the device-resident iterative_map (RANSAC + BA +
+    gating rounds): deterministic, RANSAC agrees with the oracle, the final
+    map satisfies the final gate's invariants under the oracle;
   * configs[4] (10k cameras, 10M points, 50M observations): the first LM
     iteration at full size (initial cost vs the chunked oracle, bit-identical
     outcome on a rerun) when the host has the RAM to generate it.
@@ -224,3 +227,57 @@ def test_config5_full_size_first_lm_iteration():
                   DeviceOptions(linear_solver="pcg"))
     rep = ba.iterate(1)
     assert rep.initial_cost == pytest.approx(oracle_cost_chunked(a, 1, 2.0), rel=1e-11)
+
+
+def test_config2_iterative_map_device_resident():
+    """configs[1] (driving, 500 frames, 100k tracks, ~0.9M observations, 5%
+    outliers) through the device-resident iterative_map: bit-identical
+    reruns; round 0's RANSAC statuses/masks equal the oracle's on sampled
+    tracks (same initial poses); the final map satisfies the final gate's
+    invariants under the oracle's reprojection error (every inlier <= 2 px,
+    every landmark >= 2 inliers, non-landmark tracks have no inliers)."""
+    from oracle import tri as OT
+    from paper_2510_15271_b200.cameras import CameraModel
+    from paper_2510_15271_b200.mapping import MappingConfig, iterative_map_arrays, model_table
+    from paper_2510_15271_b200.scenes import config_scene
+    from paper_2510_15271_b200.solver import DeviceOptions
+    sc = config_scene(2, seed=0)
+    models, n_models, fm = model_table([CameraModel(**sc.camera)] * sc.n_frames)
+    ptr = np.searchsorted(sc.obs_point, np.arange(sc.n_points + 1)).astype(np.int64)
+    F = sc.n_frames
+    edges = np.stack([np.arange(F - 1), np.arange(1, F)], 1).astype(np.int32)
+    priors = np.flatnonzero(sc.frame_fixed == 0).astype(np.int32)
+    dev = DeviceOptions(linear_solver="pcg", pcg_rtol=1e-8)
+    cfg = MappingConfig()
+    runs = [iterative_map_arrays(sc.cam_q, sc.cam_t, fm, sc.frame_fixed, models, n_models, ptr,
+                                 sc.obs_frame, sc.obs_uv, edges, priors, cfg, device=dev)
+            for _ in range(2)]
+    r = runs[0]
+    for name in ("cam_q", "cam_t", "points", "inlier_mask", "status", "lm_track"):
+        assert getattr(r, name).tobytes() == getattr(runs[1], name).tobytes(), name
+    assert r.round_stats == runs[1].round_stats
+    assert len(r.lm_track) > 0.99 * sc.n_points
+    assert r.round_stats[0]["added"] >= len(r.lm_track)
+    # round 0 RANSAC vs the oracle at the initial poses
+    fr0 = OT.Frames(sc.cam_q, sc.cam_t, fm, MODELS)
+    rng = np.random.default_rng(1)
+    sample = np.sort(rng.choice(sc.n_points, 400, replace=False))
+    for i in sample:
+        b0, b1 = ptr[i], ptr[i + 1]
+        xo, mo, so = OT.ransac_triangulate(fr0, list(sc.obs_frame[b0:b1]), list(sc.obs_uv[b0:b1]),
+                                           cfg.stage1.outlier_px, cfg.min_triangulation_angle, "dlt")
+        if so != OT.OK:
+            assert r.status[i] == 2, i   # FAILED, never retried
+    # final-gate invariants with the oracle's reprojection error
+    fr = OT.Frames(r.cam_q, r.cam_t, fm, MODELS)
+    lm_set = set(int(x) for x in r.lm_track)
+    for i in sample:
+        b0, b1 = ptr[i], ptr[i + 1]
+        m = r.inlier_mask[b0:b1]
+        if i in lm_set:
+            assert r.status[i] == 1 and m.sum() >= 2
+            for o in range(b0, b1):
+                if m[o - b0]:
+                    assert OT.reprojection_error(fr, sc.obs_frame[o], sc.obs_uv[o], r.points[i]) <= 2.0
+        else:
+            assert not m.any()
