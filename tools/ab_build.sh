@@ -7,7 +7,7 @@ NAME=$1; FLAGS=$2
 CS=paper_2510_15271_b200/csrc
 OUT=paper_2510_15271_b200/variants; mkdir -p $OUT /tmp/ab_$NAME
 NCCL=$(python -c "import nvidia.nccl,os;print(list(nvidia.nccl.__path__)[0])")
-for f in ba pcg tri capi; do
+for f in $(cd $CS && ls *.cu | sed "s/\.cu$//"); do
   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -I$NCCL/include \
        --expt-relaxed-constexpr $FLAGS -c $CS/$f.cu -o /tmp/ab_$NAME/$f.o &
 done
