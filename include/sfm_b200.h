@@ -192,6 +192,20 @@ int sfm_ba_download(sfm_ctx* ctx, double* out_cam_q, double* out_cam_t,
                     double* out_points);
 
 /*
+ * Test path for the point-sharded multi-GPU solve on ONE
+ * device: n_shards logical ranks (host threads, one stream each) run the
+ * exact per-rank control flow of the NCCL path on their shard
+ * (shards[r] = what rank r would pass to sfm_ba_solve: its contiguous
+ * points and their observations, obs_offset, n_params_global; pose terms on
+ * shard 0 only), with every collective executed as a fixed-rank-order
+ * device reduction.  Writes the (replicated) poses and each shard's points
+ * into out_points[r].
+ */
+int sfm_ba_solve_emulated(sfm_ctx* ctx, int32_t n_shards, const sfm_ba_problem* shards,
+                          const sfm_ba_options* opt, double* out_cam_q, double* out_cam_t,
+                          double* const* out_points, sfm_ba_report* report);
+
+/*
  * Parity/debug: Problem.evaluate (solver.py:132-142) + _assemble
  * (solver.py:164-191) restricted to the reprojection residuals: robust cost
  * per observation, weighted residual r~ [n_obs,2], weighted pose Jacobian

@@ -8,6 +8,7 @@
 
 #include "ba.cuh"
 #include "comm.cuh"
+#include "emu.cuh"
 #include "imap.cuh"
 #include "tri.cuh"
 
@@ -156,6 +157,16 @@ int sfm_ba_solve(sfm_ctx* ctx, const sfm_ba_problem* prob, const sfm_ba_options*
     solver.setup(*prob, *opt);
     solver.iterate(opt->max_iters > 0 ? opt->max_iters : 0, report);
     solver.download(out_cam_q, out_cam_t, out_points);
+  });
+}
+
+int sfm_ba_solve_emulated(sfm_ctx* ctx, int32_t n_shards, const sfm_ba_problem* shards,
+                          const sfm_ba_options* opt, double* out_cam_q, double* out_cam_t,
+                          double* const* out_points, sfm_ba_report* report) {
+  return guarded(ctx, [&] {
+    SFM_REQUIRE(shards && opt && out_cam_q && out_cam_t && out_points, "null argument");
+    ctx->ba.reset();
+    sfm::ba_solve_emulated(ctx->device, n_shards, shards, *opt, out_cam_q, out_cam_t, out_points, report);
   });
 }
 

@@ -8,6 +8,10 @@
 #pragma once
 #include <nccl.h>
 
+#include <condition_variable>
+#include <mutex>
+#include <vector>
+
 #include "common.cuh"
 
 namespace sfm {
@@ -19,10 +23,53 @@ namespace sfm {
       throw ::sfm::SfmError(SFM_E_NCCL, std::string(#call) + ": " + ncclGetErrorString(r_)); \
   } while (0)
 
+// Shard emulation (test path): R logical ranks as R host
+// threads on ONE device, each driving its own BASolver on its own stream.
+// The collectives are the same calls the NCCL path makes (same points in
+// the LM control flow, same buffers), executed as a fixed-rank-order
+// reduction kernel over the ranks' device buffers plus host barriers, so
+// the partitioned math (point shards, partial Schur complements, replicated
+// PCG, scalar reductions) runs exactly as across GPUs.  NCCL itself rejects
+// a communicator with the same device twice, hence this path.
+struct EmuGroup {
+  int world = 1;
+  std::mutex mu;
+  std::condition_variable cv;
+  int arrived = 0;
+  unsigned long long gen = 0;
+  bool aborted = false;
+  std::vector<void*> ptr_a, ptr_b;
+  explicit EmuGroup(int w) : world(w), ptr_a(w), ptr_b(w) {}
+  void barrier() {
+    std::unique_lock<std::mutex> lk(mu);
+    if (aborted) throw SfmError(SFM_E_INVALID, "shard emulation aborted by another rank");
+    const unsigned long long g = gen;
+    if (++arrived == world) {
+      arrived = 0;
+      ++gen;
+      cv.notify_all();
+    } else {
+      cv.wait(lk, [&] { return gen != g || aborted; });
+      if (aborted) throw SfmError(SFM_E_INVALID, "shard emulation aborted by another rank");
+    }
+  }
+  void abort() {
+    std::lock_guard<std::mutex> lk(mu);
+    aborted = true;
+    cv.notify_all();
+  }
+  // op: 0 sum, 1 max, 2 min
+  template <typename T>
+  void reduce(int rank, T* d, size_t n, cudaStream_t s, int op);
+  void allgather_u64(int rank, const unsigned long long* send, unsigned long long* recv, size_t n,
+                     cudaStream_t s);
+};
+
 struct Comm {
   int rank = 0;
   int world = 1;
   ncclComm_t comm = nullptr;
+  EmuGroup* emu = nullptr;
 
   void init(int r, int w, const uint8_t* id_bytes) {
     rank = r;
@@ -39,23 +86,28 @@ struct Comm {
   bool active() const { return world > 1; }
   void sum(double* d, size_t n, cudaStream_t s) {
     if (world <= 1 || n == 0) return;
+    if (emu) return emu->reduce(rank, d, n, s, 0);
     SFM_NCCL(ncclAllReduce(d, d, n, ncclFloat64, ncclSum, comm, s));
   }
   void max_u64(unsigned long long* d, size_t n, cudaStream_t s) {
     if (world <= 1 || n == 0) return;
+    if (emu) return emu->reduce(rank, d, n, s, 1);
     SFM_NCCL(ncclAllReduce(d, d, n, ncclUint64, ncclMax, comm, s));
   }
   void min_u64(unsigned long long* d, size_t n, cudaStream_t s) {
     if (world <= 1 || n == 0) return;
+    if (emu) return emu->reduce(rank, d, n, s, 2);
     SFM_NCCL(ncclAllReduce(d, d, n, ncclUint64, ncclMin, comm, s));
   }
   void max_i32(int* d, size_t n, cudaStream_t s) {
     if (world <= 1 || n == 0) return;
+    if (emu) return emu->reduce(rank, d, n, s, 1);
     SFM_NCCL(ncclAllReduce(d, d, n, ncclInt32, ncclMax, comm, s));
   }
   void allgather_u64(const unsigned long long* send, unsigned long long* recv, size_t n_per_rank,
                      cudaStream_t s) {
     if (world <= 1) return;
+    if (emu) return emu->allgather_u64(rank, send, recv, n_per_rank, s);
     SFM_NCCL(ncclAllGather(send, recv, n_per_rank, ncclUint64, comm, s));
   }
 };

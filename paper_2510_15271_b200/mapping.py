@@ -352,6 +352,32 @@ def _solve_sharded(arrays, loss, sopt, device, ctx):
     return q, t, np.concatenate(gathered, axis=0), report, rep
 
 
+def solve_sharded_emulated(arrays: BAArrays, loss: RobustLoss = TRIVIAL_LOSS,
+                           options: SolverOptions = None, device: DeviceOptions = None,
+                           n_shards: int = 2, ctx=None):
+    """The point-sharded multi-GPU solve with `n_shards` logical ranks on one
+    device (sfm_ba_solve_emulated): the same shards (BAArrays.shard) and the
+    same per-rank control flow and collectives as the NCCL path, the
+    collectives run as fixed-rank-order reductions.  -> (cam_q, cam_t,
+    points, report, raw)."""
+    ctx = ctx or nat.default_context()
+    options = options or SolverOptions()
+    parts = [arrays.shard(r, n_shards) for r in range(n_shards)]
+    structs = (nat.BAProblemC * n_shards)(*[p.struct() for p in parts])
+    Xs = [np.array(p.points, dtype=np.float64, copy=True) for p in parts]
+    ptrs = (ctypes.c_void_p * n_shards)(*[nat.ptr(x) for x in Xs])
+    q = np.array(arrays.cam_q, dtype=np.float64, copy=True)
+    t = np.array(arrays.cam_t, dtype=np.float64, copy=True)
+    rep = nat.BAReportC()
+    opt = _options(loss, options, device or DEFAULT_DEVICE_OPTIONS)
+    ctx.check(ctx.lib.sfm_ba_solve_emulated(ctx.handle, n_shards, ctypes.addressof(structs),
+                                            ctypes.byref(opt), nat.ptr(q), nat.ptr(t),
+                                            ctypes.addressof(ptrs), ctypes.byref(rep)))
+    report = SolverReport(rep.initial_cost, rep.final_cost, rep.iterations,
+                          nat.TERMINATIONS[rep.termination])
+    return q, t, np.concatenate(Xs, axis=0), report, rep
+
+
 # --- tracks ------------------------------------------------------------------
 
 class TrackArrays:

@@ -252,3 +252,45 @@ def test_dropin_bundle_adjust_objects(golden):
         assert smap.keyframes[f].cam_from_world is fixed_before[f]
     X = np.array([lm.position for lm in smap.landmarks])
     np.testing.assert_allclose(X, d["ref_points"], atol=1e-8)
+
+
+@pytest.mark.parametrize("n_shards", [2, 3, 4])
+def test_point_sharded_solve_matches_single_rank(n_shards):
+    """SURVEY.md §8(e) on one B200: n logical ranks run the multi-GPU
+    control flow (point shards balanced by observation count, partial Schur
+    complements reduced, replicated PCG, reduced scalars); the result equals
+    the single-rank solve and the oracle's."""
+    from oracle import ba as OB
+    from paper_2510_15271_b200.mapping import solve_arrays, solve_sharded_emulated
+    from paper_2510_15271_b200.scenes import make_scene, scene_arrays
+    from paper_2510_15271_b200.solver import DeviceOptions, RobustLoss, SolverOptions
+    a = scene_arrays(make_scene(120, 12000, 60000, shape="venice", seed=8))
+    loss, sopt = RobustLoss("huber", 2.0), SolverOptions(max_iters=5)
+    dopt = DeviceOptions(linear_solver="pcg", pcg_rtol=1e-12)
+    q1, t1, X1, r1, _ = solve_arrays(a, loss, sopt, dopt)
+    qs, ts, Xs, rs, raw = solve_sharded_emulated(a, loss, sopt, dopt, n_shards)
+    assert raw.kernel_launches > 0
+    assert rs.iterations == r1.iterations
+    assert rs.initial_cost == pytest.approx(r1.initial_cost, rel=1e-13)
+    assert rs.final_cost == pytest.approx(r1.final_cost, rel=1e-10)
+    scale = np.abs(X1).max()
+    np.testing.assert_allclose(Xs, X1, atol=1e-9 * scale)
+    np.testing.assert_allclose(qs, q1, atol=1e-10)
+    p = OB.BAProblem(a.cam_q, a.cam_t, a.frame_model, a.frame_fixed,
+                     [(0, 500.0, 500.0, 320.0, 240.0, (0.0, 0.0))], a.points, a.obs_frame,
+                     a.obs_point, a.obs_uv, a.edge_ab, a.prior_frame, a.edge_weight, a.prior_weight)
+    qo, to, Xo, ro = p.solve(1, 2.0, 5)
+    assert rs.final_cost == pytest.approx(ro["final_cost"], rel=1e-9)
+    np.testing.assert_allclose(Xs, Xo, atol=1e-8 * np.abs(Xo).max())
+
+
+def test_point_sharded_depth_failure_matches_single_rank(golden):
+    """NonPositiveDepth raised inside a sharded trial surfaces with the same
+    exception class on the emulated multi-rank path."""
+    from paper_2510_15271_b200.errors import NonPositiveDepth
+    from paper_2510_15271_b200.mapping import solve_sharded_emulated
+    from paper_2510_15271_b200.solver import DeviceOptions, RobustLoss, SolverOptions
+    d = golden("ba_depth_error")
+    with pytest.raises(NonPositiveDepth):
+        solve_sharded_emulated(arrays_from_npz(d), RobustLoss("huber", 2.0), SolverOptions(max_iters=5),
+                               DeviceOptions(linear_solver="pcg"), 2)
