@@ -279,6 +279,22 @@ int sfm_gate(sfm_ctx* ctx, const sfm_tracks* tracks, const double* points,
 int sfm_reprojection_errors(sfm_ctx* ctx, const sfm_tracks* tracks,
                             const double* points, double* out_err);
 
+/* ---- track formation (host-native, no context) ------------------------- */
+/*
+ * Replaces build_tracks (mapping.py:113-161): connected components of the
+ * feature-match graph with the reference's conflict rule (a merge that would
+ * put two features of one frame into a track is skipped).  Pairs
+ * pair_frames [n_pairs,2] = (frame_a, frame_b) with their matches
+ * match_index [pair_ptr[p] .. pair_ptr[p+1]) as (index_a, index_b); any
+ * order (merges run in the reference's sorted order).  Outputs sized by the
+ * caller for the worst case (2 * matches observations, matches + 1 track
+ * pointers): tracks as CSR (out_track_ptr, out_obs_frame, out_obs_feature),
+ * in the reference's track and observation order.  Needs no GPU.
+ */
+int sfm_build_tracks(int64_t n_pairs, const int32_t* pair_frames, const int64_t* pair_ptr,
+                     const int32_t* match_index, int64_t* out_track_ptr, int32_t* out_obs_frame,
+                     int32_t* out_obs_feature, int64_t* out_n_tracks, int64_t* out_n_obs);
+
 /* ---- device-resident iterative mapping ---------------------------------- */
 /* Track status (Track.status, mapping.py:48-52): in/out of sfm_iterative_map */
 #define SFM_TRACK_PENDING 0

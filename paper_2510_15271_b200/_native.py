@@ -50,6 +50,7 @@ EXPORTED_SYMBOLS = (
     "sfm_prof_reset", "sfm_ba_solve", "sfm_ba_setup", "sfm_ba_iterate",
     "sfm_ba_download", "sfm_ba_eval", "sfm_ransac_triangulate", "sfm_triangulate",
     "sfm_gate", "sfm_reprojection_errors", "sfm_iterative_map", "sfm_ba_solve_emulated",
+    "sfm_build_tracks",
 )
 
 TRACK_PENDING, TRACK_TRIANGULATED, TRACK_FAILED = 0, 1, 2
@@ -171,6 +172,7 @@ def load_library(path: str = None):
         lib.sfm_triangulate.argtypes = [_p, P(TracksC), c_d, c_i32, _p, _p]
         lib.sfm_gate.argtypes = [_p, P(TracksC), _p, c_d, _p, _p, P(c_i64)]
         lib.sfm_reprojection_errors.argtypes = [_p, P(TracksC), _p, _p]
+        lib.sfm_build_tracks.argtypes = [c_i64, _p, _p, _p, _p, _p, _p, P(c_i64), P(c_i64)]
         lib.sfm_ba_solve_emulated.argtypes = [_p, c_i32, _p, P(BAOptionsC), _p, _p, _p,
                                               P(BAReportC)]
         lib.sfm_iterative_map.argtypes = [_p, P(MapProblemC), P(MapOptionsC), _p, _p, _p, _p, _p,

@@ -9,6 +9,7 @@
 #include "ba.cuh"
 #include "comm.cuh"
 #include "emu.cuh"
+#include "tracks.cuh"
 #include "imap.cuh"
 #include "tri.cuh"
 
@@ -191,6 +192,24 @@ int sfm_iterative_map(sfm_ctx* ctx, const sfm_map_problem* prob, const sfm_map_o
     sfm::iterative_map(ctx->stream, &ctx->prof, *prob, *opt, out_cam_q, out_cam_t, out_X, out_mask, out_status,
                        out_lm_track, out_n_landmarks, out_stats, out_n_stats);
   });
+}
+
+int sfm_build_tracks(int64_t n_pairs, const int32_t* pair_frames, const int64_t* pair_ptr,
+                     const int32_t* match_index, int64_t* out_track_ptr, int32_t* out_obs_frame,
+                     int32_t* out_obs_feature, int64_t* out_n_tracks, int64_t* out_n_obs) {
+  // host-only: no context (runs without a GPU)
+  try {
+    if (n_pairs < 0 || (n_pairs && (!pair_frames || !pair_ptr)) || !out_track_ptr || !out_n_tracks ||
+        !out_n_obs)
+      return SFM_E_INVALID;
+    sfm::build_tracks(n_pairs, pair_frames, pair_ptr, match_index, out_track_ptr, out_obs_frame, out_obs_feature,
+                      out_n_tracks, out_n_obs);
+    return SFM_OK;
+  } catch (const sfm::SfmError& e) {
+    return e.code;
+  } catch (...) {
+    return SFM_E_INVALID;
+  }
 }
 
 int sfm_ransac_triangulate(sfm_ctx* ctx, const sfm_tracks* tracks, double threshold_px, double min_angle,

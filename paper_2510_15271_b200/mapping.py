@@ -380,6 +380,46 @@ def solve_sharded_emulated(arrays: BAArrays, loss: RobustLoss = TRIVIAL_LOSS,
 
 # --- tracks ------------------------------------------------------------------
 
+def build_tracks_arrays(pair_frames, pair_ptr, match_index):
+    """build_tracks (mapping.py:113-161) on arrays through the host-native
+    sfm_build_tracks -> (track_ptr, obs_frame, obs_feature)."""
+    lib = nat.load_library()
+    pf = np.ascontiguousarray(pair_frames, dtype=np.int32).reshape(-1, 2)
+    pp = np.ascontiguousarray(pair_ptr, dtype=np.int64)
+    mi = np.ascontiguousarray(match_index, dtype=np.int32).reshape(-1, 2)
+    nm = len(mi)
+    tp = np.empty(nm + 1, np.int64)
+    of = np.empty(max(2 * nm, 1), np.int32)
+    fi = np.empty(max(2 * nm, 1), np.int32)
+    nt, no = ctypes.c_int64(), ctypes.c_int64()
+    rc = lib.sfm_build_tracks(len(pf), nat.ptr(pf), nat.ptr(pp), nat.ptr(mi), nat.ptr(tp), nat.ptr(of),
+                              nat.ptr(fi), ctypes.byref(nt), ctypes.byref(no))
+    if rc != nat.SFM_OK:
+        from .errors import raise_for_code
+        raise_for_code(rc, "sfm_build_tracks: invalid pair / match arrays")
+    return tp[:nt.value + 1].copy(), of[:no.value].copy(), fi[:no.value].copy()
+
+
+def build_tracks(pair_matches, features_by_frame):
+    """mapping.py:113-161: connected components of the feature-match graph,
+    split on conflicts -> Tracks (PENDING) in the reference's order."""
+    keys = list(pair_matches)
+    pf = np.array(keys, dtype=np.int32).reshape(-1, 2)
+    counts = [len(pair_matches[k]) for k in keys]
+    pp = np.zeros(len(keys) + 1, np.int64)
+    np.cumsum(counts, out=pp[1:])
+    mi = np.array([(m.index_a, m.index_b) for k in keys for m in pair_matches[k]],
+                  dtype=np.int32).reshape(-1, 2)
+    tp, of, fi = build_tracks_arrays(pf, pp, mi)
+    tracks = []
+    for t in range(len(tp) - 1):
+        obs = []
+        for o in range(tp[t], tp[t + 1]):
+            kp = features_by_frame[int(of[o])].keypoints[int(fi[o])]
+            obs.append(Observation(int(of[o]), int(fi[o]), (kp.x, kp.y)))
+        tracks.append(Track(obs))
+    return tracks
+
 class TrackArrays:
     """Tracks as CSR over a frame table (sfm_tracks)."""
 
@@ -691,7 +731,8 @@ def mean_reprojection_error(sparse_map, ctx=None) -> float:
 
 __all__ = [
     "PENDING", "TRIANGULATED", "FAILED", "PURE", "LOCALIZATION_FIXED", "LOCALIZATION_ADJUST",
-    "RIG_EXTRINSIC", "Observation", "Track", "Landmark", "SparseMap", "StageConfig",
+    "RIG_EXTRINSIC", "build_tracks", "build_tracks_arrays", "Observation", "Track", "Landmark",
+    "SparseMap", "StageConfig",
     "MappingConfig", "BAArrays", "flatten_ba", "solve_arrays", "shard_ranges", "bundle_adjust",
     "triangulate_dlt", "triangulate_midpoint", "reprojection_error", "ransac_triangulate",
     "ransac_triangulate_batch", "remove_outliers", "iterative_map", "iterative_map_arrays",

@@ -447,6 +447,50 @@ def camera_kinds_fixtures():
                       models=KIND_MODELS)
 
 
+# --- build_tracks (mapping.py:113-161) ------------------------------------------
+
+def tracks_fixture():
+    from sfmkit.features import FeatureSet, Keypoint, Match
+    rng = np.random.default_rng(91)
+    n_frames, n_feat = 10, 60
+    feats = {f: FeatureSet(f, [Keypoint(float(3 * i), float(2 * i)) for i in range(n_feat)],
+                           np.tile([1.0, 0.0, 0.0, 0.0], (n_feat, 1))) for f in range(n_frames)}
+    pairs = {}
+    for fa in range(n_frames):
+        for fb in range(fa + 1, min(n_frames, fa + 4)):
+            k = int(rng.integers(15, 40))
+            ia = rng.choice(n_feat, size=k, replace=False)
+            # mostly consistent feature identities, with random re-links that
+            # create conflicting joins
+            ib = np.where(rng.random(k) < 0.8, ia, rng.integers(0, n_feat, k))
+            seen, ms = set(), []
+            for a, b in zip(ia, ib):
+                if (a, b) not in seen:
+                    seen.add((a, b))
+                    ms.append(Match(int(a), int(b), 0.1))
+            pairs[(fa, fb)] = ms
+    # insertion order shuffled: the reference sorts the pairs itself
+    keys = list(pairs)
+    rng.shuffle(keys)
+    pairs = {k: pairs[k] for k in keys}
+    tracks = M.build_tracks(pairs, feats)
+    pf = np.array(keys, np.int32)
+    pp = np.zeros(len(keys) + 1, np.int64)
+    pp[1:] = np.cumsum([len(pairs[k]) for k in keys])
+    mi = np.array([(m.index_a, m.index_b) for k in keys for m in pairs[k]], np.int32)
+    tp = np.zeros(len(tracks) + 1, np.int64)
+    tp[1:] = np.cumsum([len(t.observations) for t in tracks])
+    np.savez_compressed(os.path.join(HERE, "build_tracks.npz"), pair_frames=pf, pair_ptr=pp,
+                        match_index=mi,
+                        ref_track_ptr=tp,
+                        ref_obs_frame=np.array([o.frame_id for t in tracks for o in t.observations],
+                                               np.int32),
+                        ref_obs_feature=np.array([o.feature_index for t in tracks
+                                                  for o in t.observations], np.int32))
+    print(f"build_tracks: pairs={len(keys)} matches={len(mi)} tracks={len(tracks)} "
+          f"obs={int(tp[-1])}")
+
+
 # --- known-answer vectors for the geometry --------------------------------------
 
 def kat_fixture():
@@ -486,11 +530,13 @@ def kat_fixture():
 
 
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["kat", "tri", "gate", "imap", "ba", "kinds"]
+    which = sys.argv[1:] or ["kat", "tri", "gate", "imap", "ba", "kinds", "tracks"]
     if "kat" in which:
         kat_fixture()
     if "kinds" in which:
         camera_kinds_fixtures()
+    if "tracks" in which:
+        tracks_fixture()
     if "tri" in which:
         tri_fixtures()
     if "gate" in which:

@@ -151,3 +151,79 @@ def test_scene_generator_layout():
     assert np.all(np.diff(sc.obs_frame)[same] > 0)
     assert np.bincount(sc.obs_point).min() >= 2
     assert 0 < sc.outlier.mean() < 0.1
+
+
+# --- build_tracks (host-native, mapping.py:113-161): runs without a GPU -----
+
+def test_build_tracks_matches_reference_fixture(golden):
+    """sfm_build_tracks against sfmkit's build_tracks on a random match graph
+    with conflicting joins (tests/golden/make_golden.py): bit-exact CSR."""
+    from paper_2510_15271_b200.mapping import build_tracks_arrays
+    d = golden("build_tracks")
+    tp, of, fi = build_tracks_arrays(d["pair_frames"], d["pair_ptr"], d["match_index"])
+    np.testing.assert_array_equal(tp, d["ref_track_ptr"])
+    np.testing.assert_array_equal(of, d["ref_obs_frame"])
+    np.testing.assert_array_equal(fi, d["ref_obs_feature"])
+
+
+class _KP:
+    def __init__(self, x, y):
+        self.x, self.y = x, y
+
+
+class _Feats:
+    def __init__(self, n):
+        self.keypoints = [_KP(10.0 * i, 5.0 * i) for i in range(n)]
+
+
+class _M:
+    def __init__(self, a, b):
+        self.index_a, self.index_b = a, b
+
+
+def test_build_tracks_transitive_chain():
+    from paper_2510_15271_b200.mapping import PENDING, build_tracks
+    feats = {f: _Feats(4) for f in range(3)}
+    tracks = build_tracks({(0, 1): [_M(0, 0)], (1, 2): [_M(0, 0)]}, feats)
+    assert len(tracks) == 1
+    assert [(o.frame_id, o.feature_index) for o in tracks[0].observations] == [(0, 0), (1, 0), (2, 0)]
+    assert tracks[0].status == PENDING
+    assert tracks[0].observations[1].pixel.tolist() == [0.0, 0.0]
+
+
+def test_build_tracks_conflict_split():
+    from paper_2510_15271_b200.mapping import build_tracks
+    feats = {f: _Feats(6) for f in range(3)}
+    tracks = build_tracks({(0, 1): [_M(0, 0)], (0, 2): [_M(1, 5)], (1, 2): [_M(0, 5)]}, feats)
+    assert len(tracks) == 2
+    nodes = sorted((o.frame_id, o.feature_index) for t in tracks for o in t.observations)
+    assert nodes == [(0, 0), (0, 1), (1, 0), (2, 5)]
+    for t in tracks:
+        frames = [o.frame_id for o in t.observations]
+        assert len(frames) == len(set(frames))
+
+
+def test_build_tracks_matches_union_find():
+    from paper_2510_15271_b200.mapping import build_tracks
+    rng = np.random.default_rng(42)
+    n_frames, n_feat = 6, 12
+    feats = {f: _Feats(n_feat) for f in range(n_frames)}
+    pairs = {(f, f + 1): [_M(int(k), int(k)) for k in sorted(rng.choice(n_feat, 7, replace=False))]
+             for f in range(n_frames - 1)}
+    parent = {}
+
+    def find(x):
+        while parent.setdefault(x, x) != x:
+            parent[x] = parent[parent[x]]
+            x = parent[x]
+        return x
+    for (fa, fb), ms in pairs.items():
+        for m in ms:
+            parent[find((fa, m.index_a))] = find((fb, m.index_b))
+    comps = {}
+    for node in list(parent):
+        comps.setdefault(find(node), set()).add(node)
+    expected = sorted(sorted(c) for c in comps.values() if len(c) >= 2)
+    got = sorted(sorted((o.frame_id, o.feature_index) for o in t.observations)
+                 for t in build_tracks(pairs, feats))
+    assert got == expected
