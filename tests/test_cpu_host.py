@@ -227,3 +227,50 @@ def test_build_tracks_matches_union_find():
     got = sorted(sorted((o.frame_id, o.feature_index) for o in t.observations)
                  for t in build_tracks(pairs, feats))
     assert got == expected
+
+
+REF_SRC = "/root/reference/pkg/src"
+
+
+@pytest.mark.skipif(not os.path.isdir(REF_SRC), reason="reference package not mounted (GPU box)")
+def test_dropin_map_writes_reference_map_bin(tmp_path, golden):
+    """The drop-in's object model is what sfmkit's `map` stage serialises:
+    sfmkit.io.write_map on this package's SparseMap (built from the
+    reference iterative_map fixture) produces the same bytes as on the
+    equivalent sfmkit SparseMap, and read_map round-trips it (SURVEY.md
+    §8(f) row 4: map.bin compatibility)."""
+    import sys
+    if REF_SRC not in sys.path:
+        sys.path.insert(0, REF_SRC)
+    sys.dont_write_bytecode = True
+    import sfmkit.cameras as RC
+    import sfmkit.io as RIO
+    import sfmkit.keyframes as RK
+    import sfmkit.mapping as RM
+    import sfmkit.se3 as RS
+    from paper_2510_15271_b200 import (CameraModel, Keyframe, Landmark, Observation, Pose,
+                                       SparseMap, Track)
+    d = golden("iterative_map")
+    ptr, lm_track = d["track_ptr"], d["ref_lm_track"]
+    masks = np.split(d["ref_lm_mask"].astype(bool),
+                     np.cumsum([ptr[t + 1] - ptr[t] for t in lm_track])[:-1])
+
+    def build(Cam, Kf, Ps, Obs, Tr, Lm, Sm):
+        cam = Cam("pinhole", 500.0, 500.0, 320.0, 240.0, 640, 480)
+        kfs = {f: Kf(f, float(f), 0, Ps(d["ref_cam_q"][f], d["ref_cam_t"][f]))
+               for f in range(len(d["cam_q"]))}
+        lms = []
+        for i, t in enumerate(lm_track):
+            obs = [Obs(int(d["obs_frame"][o]), 0, d["obs_uv"][o]) for o in range(ptr[t], ptr[t + 1])]
+            lms.append(Lm(d["ref_lm_X"][i], Tr(obs, status="triangulated"), masks[i]))
+        return Sm(kfs, {0: cam}, lms, None, {}, {0})
+
+    ours = build(CameraModel, Keyframe, Pose, Observation, Track, Landmark, SparseMap)
+    ref = build(RC.CameraModel, RK.Keyframe, RS.Pose, RM.Observation, RM.Track, RM.Landmark,
+                RM.SparseMap)
+    RIO.write_map(ours, tmp_path / "ours.bin")
+    RIO.write_map(ref, tmp_path / "ref.bin")
+    assert (tmp_path / "ours.bin").read_bytes() == (tmp_path / "ref.bin").read_bytes()
+    back = RIO.read_map(tmp_path / "ours.bin")
+    assert len(back.landmarks) == len(ours.landmarks)
+    np.testing.assert_array_equal(np.array([lm.position for lm in back.landmarks]), d["ref_lm_X"])
