@@ -356,6 +356,7 @@ struct Pcg3Args {
   int max_it;
   double rtol;
   int fuse_zc;
+  int warm;                // start from the energy-optimal multiple of the previous solution
 };
 
 __device__ __forceinline__ double warp_sum(double v) {
@@ -669,20 +670,55 @@ __global__ void __launch_bounds__(kPcgMaxThreads, 1) k_pcg3(Pcg3Args a) {
     }
   };
 
-  // ---- prologue: x = 0, r = b, p = q = 0, rc = P^T b ------------------------
+  // ---- warm start: x0 = gamma * (the previous solve's solution, still in
+  // a.x), gamma = (x0.b)/(x0.S x0) the energy-optimal multiple, so the
+  // starting error is never larger than from x = 0.  Consecutive LM steps
+  // are nearly parallel late in a solve, where this removes most of the
+  // initial error; the converged solution (to rtol) is the same.
+  double gamma = 0.0;
+  if (a.warm) {
+    for (int i = warp; i < nrows; i += kPcgWarps)
+      if (lane < 6) a.z[(row0 + i) * 6 + lane] = a.x[(row0 + i) * 6 + lane];
+    grid.sync();
+    fill_zc(0);
+    __syncthreads();
+    spmv_segments(a, m.zc, m.lc, kc0, m.seg, m.Ssm);
+    __syncthreads();
+    double xb = 0.0, xw = 0.0;
+    for (int i = warp; i < nrows; i += kPcgWarps)
+      if (lane < 6) {
+        const int2 rs = a.rowseg[row0 + i];
+        double w = 0.0;
+        for (int sg = 0; sg < rs.y; ++sg) w += m.seg[(rs.x + sg) * 6 + lane];
+        m.q[i * 6 + lane] = w;  // S x0, consumed by the prologue below
+        const double x0 = a.x[(row0 + i) * 6 + lane];
+        xb += x0 * a.b[(row0 + i) * 6 + lane];
+        xw += x0 * w;
+      }
+    const double2 t = block_sum2(xb, xw, red);
+    if (threadIdx.x == 0) { part_rz[blockIdx.x] = t.x; part_rz[G + blockIdx.x] = t.y; }
+    grid.sync();
+    gather_after_sync(a, part_rz, sums, 2, m.rc, false, true, nullptr, nullptr);
+    const double g = sums[0] / sums[1];
+    gamma = (sums[1] > 0.0 && isfinite(g)) ? g : 0.0;
+  }
+
+  // ---- prologue: x = gamma x0, r = b - gamma S x0, p = q = 0, rc = P^T r ----
   double bb_l = 0.0;
   for (int i = warp; i < nrows; i += kPcgWarps) {
-    double bi = 0.0;
+    double ri = 0.0;
     if (lane < 6) {
-      bi = a.b[(row0 + i) * 6 + lane];
-      m.x[i * 6 + lane] = 0.0;
-      m.r[i * 6 + lane] = bi;
+      const double bi = a.b[(row0 + i) * 6 + lane];
+      const bool ws = gamma != 0.0;
+      ri = ws ? bi - gamma * m.q[i * 6 + lane] : bi;
+      m.x[i * 6 + lane] = ws ? gamma * a.x[(row0 + i) * 6 + lane] : 0.0;
+      m.r[i * 6 + lane] = ri;
       m.p[i * 6 + lane] = 0.0;
       m.q[i * 6 + lane] = 0.0;
-      bb_l += bi * bi;
+      bb_l += bi * bi;  // the stopping test stays relative to |b|
     }
     if (two) {
-      const double yv = restrict_row(m, i, bi);
+      const double yv = restrict_row(m, i, ri);
       if (lane < 6) m.y[i * 6 + lane] = yv;
     }
   }
@@ -811,6 +847,9 @@ void TwoLevelPcg::set_pattern(const int* row_ptr, const int* col, int nnzb, cuda
   const int nwarps = nt_ / 32;
   if (const char* e = std::getenv("SFM_COARSE_REFRESH")) refresh_ = std::max(1, std::atoi(e));
   lin_count_ = 0;
+  have_prev_ = false;
+  warm_ = true;
+  if (const char* e = std::getenv("SFM_PCG_WARM")) warm_ = std::atoi(e) != 0;
   int G = std::min((1024 / nt_) * nsm, nf_);
   std::vector<int> row0;
   for (;;) {
@@ -1052,6 +1091,8 @@ void TwoLevelPcg::solve(const PcgProblem& p, int max_it, double rtol, BAScalars*
   a.b = p.b; a.x = p.x; a.r = r_.get(); a.z = z_.get(); a.p = p_.get(); a.q = q_.get();
   a.rpart = rpart_.get(); a.part = part_.get(); a.sc = sc; a.max_it = max_it; a.rtol = rtol;
   a.fuse_zc = 1;
+  a.warm = have_prev_ && warm_ ? 1 : 0;
+  have_prev_ = true;
   if (const char* e = std::getenv("SFM_PCG_FUSEZC")) a.fuse_zc = std::atoi(e);
   void* args[] = {&a};
   ProfScope ps(*prof, "pcg", 0.0, s);

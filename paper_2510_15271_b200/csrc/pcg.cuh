@@ -49,6 +49,7 @@ class TwoLevelPcg {
   size_t smem_ = 0;
   int npairs_ = 0;
   bool coarse_valid_ = false;
+  bool have_prev_ = false, warm_ = true;  // warm start from the previous solution
   const double* Aci_ = nullptr;
   DevBuf<double> Minv_, Pm_, Ac_[2], r_, z_, p_, q_, rpart_, part_;
   DevBuf<int2> pair_cd_, rowseg_, wres_;
