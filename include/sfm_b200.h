@@ -216,6 +216,53 @@ int sfm_ba_eval(sfm_ctx* ctx, const sfm_ba_problem* prob, int32_t loss_kind,
                 double loss_param, double* out_cost_per_obs, double* out_res,
                 double* out_jc, double* out_jp);
 
+/* ---- rig-extrinsic / rolling-shutter bundle adjustment ------------------- */
+/* Residual kinds (mapping.py:310-356): the pose a residual projects through
+ * is composed from one or two SE(3) parameter blocks ("slots"). */
+#define SFM_RES_GLOBAL 0   /* pose = B[s0]                                 */
+#define SFM_RES_ROLLING 1  /* pose = B[s0] exp(alpha log(B[s0]^-1 B[s1]))  */
+#define SFM_RES_RIG 2      /* pose = B[s1] B[s0]  (extrinsic s1, vehicle s0) */
+
+/*
+ * The problem bundle_adjust builds when keyframes are rolling-shutter or in
+ * rig_extrinsic mode (mapping.py:414-509): pose blocks (frames; or vehicle
+ * instants + per-camera extrinsics), TRIANGULATED points, residuals in the
+ * reference residual order (landmark-major, so res_point is non-decreasing)
+ * with their kind, slots and scanline fraction, and the pose terms with
+ * per-term weights (lambda_c edges; lambda_a or extrinsic priors).
+ */
+typedef struct {
+  int32_t n_blocks;
+  int32_t n_models;
+  const double* block_q;        /* [n_blocks,4]                             */
+  const double* block_t;        /* [n_blocks,3]                             */
+  const uint8_t* block_fixed;   /* [n_blocks]                               */
+  const sfm_camera_model* models;
+  int64_t n_points;
+  const double* points;         /* [n_points,3]                             */
+  int64_t n_res;
+  const int32_t* res_point;     /* [n_res] non-decreasing                   */
+  const int32_t* res_model;     /* [n_res]                                  */
+  const int32_t* res_kind;      /* [n_res] SFM_RES_*                        */
+  const int32_t* res_slot;      /* [n_res,2] (second = -1 for GLOBAL)       */
+  const double* res_alpha;      /* [n_res] ROLLING scanline fraction or NULL */
+  const double* res_uv;         /* [n_res,2]                                */
+  int32_t n_edges;
+  int32_t n_priors;
+  const int32_t* edge_ab;       /* [n_edges,2] blocks (a, b)                */
+  const double* edge_weight;    /* [n_edges] information weight            */
+  const int32_t* prior_block;   /* [n_priors]                               */
+  const double* prior_weight;   /* [n_priors]                               */
+} sfm_gba_problem;
+
+/*
+ * solver.solve (solver.py:194-257) on that problem: same LM rules and
+ * report as sfm_ba_solve; final block poses and points written out.
+ */
+int sfm_gba_solve(sfm_ctx* ctx, const sfm_gba_problem* prob, const sfm_ba_options* opt,
+                  double* out_block_q, double* out_block_t, double* out_points,
+                  sfm_ba_report* report);
+
 /* ---- triangulation / gating --------------------------------------------- */
 /*
  * Tracks as CSR: observations of track i are [track_ptr[i], track_ptr[i+1]),

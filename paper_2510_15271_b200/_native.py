@@ -50,10 +50,11 @@ EXPORTED_SYMBOLS = (
     "sfm_prof_reset", "sfm_ba_solve", "sfm_ba_setup", "sfm_ba_iterate",
     "sfm_ba_download", "sfm_ba_eval", "sfm_ransac_triangulate", "sfm_triangulate",
     "sfm_gate", "sfm_reprojection_errors", "sfm_iterative_map", "sfm_ba_solve_emulated",
-    "sfm_build_tracks",
+    "sfm_build_tracks", "sfm_gba_solve",
 )
 
 TRACK_PENDING, TRACK_TRIANGULATED, TRACK_FAILED = 0, 1, 2
+RES_GLOBAL, RES_ROLLING, RES_RIG = 0, 1, 2
 
 _p = ctypes.c_void_p
 
@@ -102,6 +103,16 @@ class TracksC(ctypes.Structure):
                 ("cam_q", _p), ("cam_t", _p), ("frame_model", _p), ("models", _p),
                 ("n_tracks", ctypes.c_int64), ("n_obs", ctypes.c_int64),
                 ("track_ptr", _p), ("obs_frame", _p), ("obs_uv", _p), ("active", _p)]
+
+
+class GbaProblemC(ctypes.Structure):
+    _fields_ = [("n_blocks", ctypes.c_int32), ("n_models", ctypes.c_int32),
+                ("block_q", _p), ("block_t", _p), ("block_fixed", _p), ("models", _p),
+                ("n_points", ctypes.c_int64), ("points", _p), ("n_res", ctypes.c_int64),
+                ("res_point", _p), ("res_model", _p), ("res_kind", _p), ("res_slot", _p),
+                ("res_alpha", _p), ("res_uv", _p), ("n_edges", ctypes.c_int32),
+                ("n_priors", ctypes.c_int32), ("edge_ab", _p), ("edge_weight", _p),
+                ("prior_block", _p), ("prior_weight", _p)]
 
 
 class MapProblemC(ctypes.Structure):
@@ -172,6 +183,7 @@ def load_library(path: str = None):
         lib.sfm_triangulate.argtypes = [_p, P(TracksC), c_d, c_i32, _p, _p]
         lib.sfm_gate.argtypes = [_p, P(TracksC), _p, c_d, _p, _p, P(c_i64)]
         lib.sfm_reprojection_errors.argtypes = [_p, P(TracksC), _p, _p]
+        lib.sfm_gba_solve.argtypes = [_p, P(GbaProblemC), P(BAOptionsC), _p, _p, _p, P(BAReportC)]
         lib.sfm_build_tracks.argtypes = [c_i64, _p, _p, _p, _p, _p, _p, P(c_i64), P(c_i64)]
         lib.sfm_ba_solve_emulated.argtypes = [_p, c_i32, _p, P(BAOptionsC), _p, _p, _p,
                                               P(BAReportC)]

@@ -49,3 +49,11 @@ class RigCalibration:
 
     def extrinsic(self, camera_id) -> Pose:
         return self.cam_from_rig[camera_id]
+
+    @property
+    def reference_id(self):
+        """The camera whose extrinsic is the identity (cameras.py:197-202)."""
+        for cid in self.camera_ids:
+            if self.cam_from_rig[cid].almost_equal(Pose.identity()):
+                return cid
+        raise ValueError("no reference camera")

@@ -2004,4 +2004,6 @@ void BASolver::eval(cudaStream_t s, Profiler* prof, const sfm_ba_problem& pr, in
   SFM_CUDA(cudaStreamSynchronize(s));
 }
 
+#include "gba_impl.cuh"
+
 }  // namespace sfm

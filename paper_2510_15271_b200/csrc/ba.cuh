@@ -136,4 +136,45 @@ class BASolver {
   BAScalars h_sc_{};
 };
 
+struct GbaArgs;
+
+// Bundle adjustment with rig-extrinsic / rolling-shutter residuals (two SE(3)
+// slots per residual): csrc/gba_impl.cuh.
+class GBASolver {
+ public:
+  GBASolver(cudaStream_t s, Profiler* p) : stream_(s), prof_(p) {}
+  void setup(const sfm_gba_problem& prob, const sfm_ba_options& opt);
+  void iterate(int n, sfm_ba_report* rep);
+  void download(double* q, double* t, double* X);
+
+ private:
+  GbaArgs args(int blocks, int points) const;
+  double eval_cost(int blocks, int points);
+  void linearize();
+  bool trial(double lam, double* new_cost, double* step_norm);
+  void read();
+  void raise_projection(int blocks, int points);
+
+  cudaStream_t stream_;
+  Profiler* prof_;
+  sfm_ba_options opt_{};
+  int nb_ = 0, nf_ = 0, E_ = 0, A_ = 0, n_ub_ = 0, n_full_ = 0;
+  int64_t P_ = 0, R_ = 0, n_params_ = 0;
+  bool use_dense_ = true, finished_ = true;
+  double initial_cost_ = 0.0, cost_ = 0.0, lam_ = 0.0, gmax_ = 0.0;
+  int iters_ = 0, n_trials_ = 0, pcg_total_ = 0, term_ = 0, cur_ = 0;
+  BAScalars h_sc_{};
+  DevBuf<sfm_camera_model> models_;
+  DevBuf<double> q_[2], t_[2], Rt_[2], X_[2];
+  DevBuf<int> rpt_, rmodel_, rkind_, rslot_, free_idx_, free_block_, sptr_, ub_edge_, pos_up_, pos_lo_,
+      row_ptr_, col_, diag_pos_, edge_ab_, prior_block_, term_ptr_, term_list_;
+  DevBuf<double> ralpha_, ruv_, ew_, pw_, meas_inv_, init_inv_, rec_, V_, gp_, pv_, gc_, hdiag_, Ut_, gt_,
+      edge_H_, S_, b_, dc_, part_a_, part_b_, part_c_, part_d_;
+  DevBuf<int64_t> pptr_, slist_, ent_ptr_;
+  DevBuf<int2> ub_key_;
+  DevBuf<int4> ent_;
+  DevBuf<BAScalars> sc_;
+  TwoLevelPcg pcg_;
+};
+
 }  // namespace sfm

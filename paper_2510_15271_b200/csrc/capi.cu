@@ -171,6 +171,18 @@ int sfm_ba_solve_emulated(sfm_ctx* ctx, int32_t n_shards, const sfm_ba_problem* 
   });
 }
 
+int sfm_gba_solve(sfm_ctx* ctx, const sfm_gba_problem* prob, const sfm_ba_options* opt, double* out_block_q,
+                  double* out_block_t, double* out_points, sfm_ba_report* report) {
+  return guarded(ctx, [&] {
+    SFM_REQUIRE(prob && opt, "null problem/options");
+    ctx->ba.reset();
+    sfm::GBASolver solver(ctx->stream, &ctx->prof);
+    solver.setup(*prob, *opt);
+    solver.iterate(opt->max_iters > 0 ? opt->max_iters : 0, report);
+    solver.download(out_block_q, out_block_t, out_points);
+  });
+}
+
 int sfm_ba_eval(sfm_ctx* ctx, const sfm_ba_problem* prob, int32_t loss_kind, double loss_param,
                 double* out_cost_per_obs, double* out_res, double* out_jc, double* out_jp) {
   return guarded(ctx, [&] {

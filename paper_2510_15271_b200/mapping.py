@@ -239,18 +239,52 @@ def solve_arrays(arrays: BAArrays, loss: RobustLoss = TRIVIAL_LOSS,
     return q, t, X, report, rep
 
 
-def _check_supported(sparse_map, frames, mode):
-    if mode == RIG_EXTRINSIC:
-        raise NotImplementedError("rig_extrinsic residuals are a SURVEY §8(f) 'next' row")
+def _next_same_camera(sparse_map):
+    """frame_id -> next keyframe of the same camera by timestamp
+    (mapping.py:530-541)."""
     by_cam = {}
-    for f in frames:
-        by_cam.setdefault(sparse_map.keyframes[f].camera_id, []).append(sparse_map.keyframes[f])
+    for f in sorted(sparse_map.keyframes):
+        kf = sparse_map.keyframes[f]
+        by_cam.setdefault(kf.camera_id, []).append(kf)
+    nxt = {}
     for seq in by_cam.values():
-        seq = sorted(seq, key=lambda k: k.timestamp)
+        seq.sort(key=lambda k: k.timestamp)
         for a, b in zip(seq, seq[1:]):
-            if a.shutter == ROLLING_SHUTTER and b.timestamp - a.timestamp > 0:
-                raise NotImplementedError(
-                    "rolling-shutter residuals are a SURVEY §8(f) 'next' row")
+            nxt[a.frame_id] = b
+    return nxt
+
+
+def _shutter_alpha(kf, next_kf, pixel_row, height):
+    """Scanline interpolation fraction (mapping.py:379-387), None = global."""
+    if next_kf is None or kf.shutter != ROLLING_SHUTTER:
+        return None
+    s = pixel_row / max(height - 1, 1)
+    dt = next_kf.timestamp - kf.timestamp
+    if dt <= 0:
+        return None
+    return float(np.clip(s * kf.exposure / dt, 0.0, 1.0))
+
+
+def _needs_general(sparse_map, frames, mode):
+    """True when the residuals are not all global-shutter single-pose ones:
+    rig_extrinsic mode, or a rolling-shutter keyframe with a successor."""
+    if mode == RIG_EXTRINSIC:
+        return True
+    nxt = _next_same_camera(sparse_map)
+    for f in frames:
+        kf = sparse_map.keyframes[f]
+        if kf.shutter == ROLLING_SHUTTER and f in nxt and nxt[f].timestamp - kf.timestamp > 0:
+            return True
+    return False
+
+
+def _check_supported(sparse_map, frames, mode):
+    """The single-slot fast path (and the device-resident iterative_map)
+    takes global-shutter, non-rig problems; bundle_adjust routes the rest
+    to the general path (sfm_gba_solve)."""
+    if _needs_general(sparse_map, frames, mode):
+        raise NotImplementedError("rig / rolling-shutter residuals: use bundle_adjust "
+                                  "(general two-slot path)")
 
 
 def flatten_ba(sparse_map, config, stage=1, mode=PURE):
@@ -324,6 +358,8 @@ def bundle_adjust(sparse_map, config: MappingConfig = None, stage: int = 1, mode
     sharded across ranks and the camera system is all-reduced over NCCL."""
     if config is None:
         config = MappingConfig()
+    if _needs_general(sparse_map, sorted(sparse_map.keyframes), mode):
+        return _bundle_adjust_general(sparse_map, config, stage, mode, device, ctx)
     arrays, frames, lms, loss = flatten_ba(sparse_map, config, stage, mode)
     ctx = ctx or nat.default_context()
     sopt = SolverOptions(max_iters=config.max_solver_iters)
@@ -341,6 +377,144 @@ def bundle_adjust(sparse_map, config: MappingConfig = None, stage: int = 1, mode
     for pi, li in enumerate(lms):
         sparse_map.landmarks[li].position = X[pi].copy()
     return report
+
+
+def _bundle_adjust_general(sparse_map, config, stage, mode, device, ctx):
+    """bundle_adjust (mapping.py:390-527) for rig_extrinsic mode and rolling-
+    shutter keyframes: residuals over one or two SE(3) blocks, solved on the
+    device by sfm_gba_solve.  Same problem construction, write-back and
+    report as the reference."""
+    loss = config.stage1.loss if stage == 1 else config.stage2.loss
+    frames = sorted(sparse_map.keyframes)
+    fixed = set(sparse_map.fixed_frames)
+    if mode == LOCALIZATION_FIXED:
+        fixed |= {f for f in frames if sparse_map.provenance.get(f) == "prior"}
+    rig_mode = mode == RIG_EXTRINSIC
+    if not rig_mode and not fixed and config.lambda_a <= 0:
+        raise NoGauge("no fixed pose and no absolute prior")
+    kfs = sparse_map.keyframes
+    bq, bt, bfix = [], [], []
+    edges, ew, priors, pw = [], [], [], []
+    if rig_mode:
+        if sparse_map.rig is None:
+            raise NoGauge("rig_extrinsic mode needs a rig calibration")
+        rig = sparse_map.rig
+        instants = sorted({kfs[f].timestamp for f in frames})
+        instant_id = {tm: i for i, tm in enumerate(instants)}
+        vehicle_entry = {}
+        for f in frames:
+            i = instant_id[kfs[f].timestamp]
+            if i not in vehicle_entry:
+                vehicle_entry[i] = rig.extrinsic(kfs[f].camera_id).inverse() @ kfs[f].cam_from_world
+        vids = sorted(vehicle_entry)
+        vblock = {i: k for k, i in enumerate(vids)}
+        for i in vids:
+            bq.append(vehicle_entry[i].quat)
+            bt.append(vehicle_entry[i].t)
+            bfix.append(1 if i == 0 else 0)
+        eblock = {}
+        ref_id = rig.reference_id
+        for cid in rig.camera_ids:
+            eblock[cid] = len(bq)
+            bq.append(rig.extrinsic(cid).quat)
+            bt.append(rig.extrinsic(cid).t)
+            bfix.append(1 if cid == ref_id else 0)
+            if cid != ref_id and config.extrinsic_prior_weight > 0:
+                priors.append(eblock[cid])
+                pw.append(float(config.extrinsic_prior_weight))
+        if config.lambda_c > 0:
+            for a, b in zip(vids, vids[1:]):
+                edges.append((vblock[a], vblock[b]))
+                ew.append(float(config.lambda_c))
+    else:
+        fidx = {f: i for i, f in enumerate(frames)}
+        for f in frames:
+            bq.append(kfs[f].cam_from_world.quat)
+            bt.append(kfs[f].cam_from_world.t)
+            bfix.append(1 if f in fixed else 0)
+        e_arr, p_arr = _pose_terms(frames, fidx, sparse_map, config, fixed, mode)
+        edges = [tuple(e) for e in e_arr]
+        ew = [float(config.lambda_c)] * len(edges)
+        priors = list(p_arr)
+        pw = [float(config.lambda_a)] * len(priors)
+        next_of = _next_same_camera(sparse_map)
+    cams = sorted({kfs[f].camera_id for f in frames})
+    cam_models = [sparse_map.cameras[c] for c in cams]
+    models, n_models, cam_model_idx = model_table(cam_models)
+    model_of_cam = {c: int(cam_model_idx[k]) for k, c in enumerate(cams)}
+    lms = [li for li, lm in enumerate(sparse_map.landmarks) if lm.track.status == TRIANGULATED]
+    pts = np.array([sparse_map.landmarks[li].position for li in lms], dtype=np.float64).reshape(-1, 3)
+    rp, rm, rk, rs, ra, ruv = [], [], [], [], [], []
+    for pi, li in enumerate(lms):
+        lm = sparse_map.landmarks[li]
+        for o in lm.inlier_observations():
+            kf = kfs[o.frame_id]
+            rp.append(pi)
+            rm.append(model_of_cam[kf.camera_id])
+            ruv.append(o.pixel)
+            if rig_mode:
+                rk.append(nat.RES_RIG)
+                rs.append((vblock[instant_id[kf.timestamp]], eblock[kf.camera_id]))
+                ra.append(0.0)
+                continue
+            cam = sparse_map.cameras[kf.camera_id]
+            alpha = _shutter_alpha(kf, next_of.get(o.frame_id), o.pixel[1], cam.height)
+            if alpha is None:
+                rk.append(nat.RES_GLOBAL)
+                rs.append((fidx[o.frame_id], -1))
+                ra.append(0.0)
+            else:
+                rk.append(nat.RES_ROLLING)
+                rs.append((fidx[o.frame_id], fidx[next_of[o.frame_id].frame_id]))
+                ra.append(alpha)
+    keep = dict(
+        bq=np.ascontiguousarray(np.array(bq, dtype=np.float64).reshape(-1, 4)),
+        bt=np.ascontiguousarray(np.array(bt, dtype=np.float64).reshape(-1, 3)),
+        bf=np.ascontiguousarray(np.array(bfix, dtype=np.uint8)), pts=np.ascontiguousarray(pts),
+        rp=np.ascontiguousarray(np.array(rp, dtype=np.int32)),
+        rm=np.ascontiguousarray(np.array(rm, dtype=np.int32)),
+        rk=np.ascontiguousarray(np.array(rk, dtype=np.int32)),
+        rs=np.ascontiguousarray(np.array(rs, dtype=np.int32).reshape(-1, 2)),
+        ra=np.ascontiguousarray(np.array(ra, dtype=np.float64)),
+        ruv=np.ascontiguousarray(np.array(ruv, dtype=np.float64).reshape(-1, 2)),
+        eab=np.ascontiguousarray(np.array(edges, dtype=np.int32).reshape(-1, 2)),
+        ew=np.ascontiguousarray(np.array(ew, dtype=np.float64)),
+        pb=np.ascontiguousarray(np.array(priors, dtype=np.int32)),
+        pw=np.ascontiguousarray(np.array(pw, dtype=np.float64)))
+    prob = nat.GbaProblemC(
+        len(keep["bf"]), n_models, nat.ptr(keep["bq"]), nat.ptr(keep["bt"]), nat.ptr(keep["bf"]),
+        ctypes.addressof(models), len(keep["pts"]), nat.ptr(keep["pts"]), len(keep["rp"]),
+        nat.ptr(keep["rp"]), nat.ptr(keep["rm"]), nat.ptr(keep["rk"]), nat.ptr(keep["rs"]),
+        nat.ptr(keep["ra"]), nat.ptr(keep["ruv"]), len(keep["eab"]), len(keep["pb"]),
+        nat.ptr(keep["eab"]), nat.ptr(keep["ew"]), nat.ptr(keep["pb"]), nat.ptr(keep["pw"]))
+    opt = _options(loss, SolverOptions(max_iters=config.max_solver_iters),
+                   device or DEFAULT_DEVICE_OPTIONS)
+    q = keep["bq"].copy()
+    t = keep["bt"].copy()
+    X = keep["pts"].copy()
+    rep = nat.BAReportC()
+    ctx = ctx or nat.default_context()
+    ctx.check(ctx.lib.sfm_gba_solve(ctx.handle, ctypes.byref(prob), ctypes.byref(opt), nat.ptr(q),
+                                    nat.ptr(t), nat.ptr(X), ctypes.byref(rep)))
+    pose_type = type(kfs[frames[0]].cam_from_world) if frames else Pose
+    if rig_mode:
+        new_extr = {cid: pose_type(q[eblock[cid]], t[eblock[cid]]) for cid in rig.camera_ids}
+        sparse_map.rig = type(rig)(rig.camera_ids, new_extr)
+        for f in frames:
+            kf = kfs[f]
+            k = vblock[instant_id[kf.timestamp]]
+            kf.cam_from_world = new_extr[kf.camera_id] @ pose_type(q[k], t[k])
+    else:
+        for i, f in enumerate(frames):
+            if bfix[i]:
+                continue
+            if np.array_equal(q[i], keep["bq"][i]) and np.array_equal(t[i], keep["bt"][i]):
+                continue
+            kfs[f].cam_from_world = pose_type(q[i], t[i])
+    for pi, li in enumerate(lms):
+        sparse_map.landmarks[li].position = X[pi].copy()
+    return SolverReport(rep.initial_cost, rep.final_cost, rep.iterations,
+                        nat.TERMINATIONS[rep.termination])
 
 
 def _solve_sharded(arrays, loss, sopt, device, ctx):
@@ -680,10 +854,11 @@ def iterative_map(keyframes, tracks, cameras, config: MappingConfig = None, rig=
         new = [f for f in kf_map if sparse_map.provenance.get(f) != "prior"]
         sparse_map.fixed_frames = {min(new) if new else min(kf_map)}
     frames = sorted(kf_map)
+    if _needs_general(sparse_map, frames, mode):
+        return _iterative_map_host(sparse_map, tracks, config, mode, device, ctx)
     fixed = set(sparse_map.fixed_frames)
     if mode == LOCALIZATION_FIXED:
         fixed |= {f for f in frames if sparse_map.provenance.get(f) == "prior"}
-    _check_supported(sparse_map, frames, mode)
     if mode != RIG_EXTRINSIC and not fixed and config.lambda_a <= 0:
         raise NoGauge("no fixed pose and no absolute prior")
     fidx = {f: i for i, f in enumerate(frames)}
@@ -714,6 +889,41 @@ def iterative_map(keyframes, tracks, cameras, config: MappingConfig = None, rig=
                                      res.inlier_mask[ptr[i]:ptr[i + 1]].copy())
                             for i in res.lm_track]
     sparse_map.round_stats = res.round_stats
+    return sparse_map
+
+
+def _iterative_map_host(sparse_map, tracks, config, mode, device, ctx):
+    """mapping.py:596-623 driven from the host for problems the device-
+    resident loop does not take (rolling-shutter keyframes, rig mode): each
+    round's triangulation and gating are one batched device call, the BA the
+    general two-slot solve."""
+    kf_map = sparse_map.keyframes
+    stats = []
+    for round_idx in range(config.max_outer_iters):
+        poses = {f: kf.cam_from_world for f, kf in kf_map.items()}
+        cams = {f: sparse_map.camera_of(f) for f in kf_map}
+        pending = [t for t in tracks if t.status == PENDING]
+        results = ransac_triangulate_batch(
+            pending, poses, cams, threshold_px=config.stage1.outlier_px,
+            min_angle=config.min_triangulation_angle, method=config.triangulation, ctx=ctx)
+        added = 0
+        for lm in results:
+            if lm is not None:
+                sparse_map.landmarks.append(lm)
+                added += 1
+        if sparse_map.landmarks:
+            bundle_adjust(sparse_map, config, stage=1, mode=mode, device=device, ctx=ctx)
+        _, removed = remove_outliers(sparse_map, config.stage1.outlier_px, ctx=ctx)
+        stats.append({"round": round_idx, "added": added, "removed": removed,
+                      "landmarks": len(sparse_map.landmarks)})
+        if added == 0 and removed == 0:
+            break
+    if sparse_map.landmarks:
+        bundle_adjust(sparse_map, config, stage=2, mode=mode, device=device, ctx=ctx)
+        _, removed = remove_outliers(sparse_map, config.stage2.outlier_px, ctx=ctx)
+        stats.append({"round": "final", "added": 0, "removed": removed,
+                      "landmarks": len(sparse_map.landmarks)})
+    sparse_map.round_stats = stats
     return sparse_map
 
 

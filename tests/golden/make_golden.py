@@ -29,7 +29,7 @@ import sfmkit.solver as SV  # noqa: E402
 from sfmkit.cameras import CameraModel, project, project_with_pose_jacobian, unproject  # noqa: E402
 from sfmkit.keyframes import Keyframe  # noqa: E402
 from sfmkit.posegraph import PoseEdge, _edge_residual_fn  # noqa: E402
-from sfmkit.se3 import Pose, exp_map  # noqa: E402
+from sfmkit.se3 import Pose, exp_map, interpolate_pose  # noqa: E402
 
 from paper_2510_15271_b200 import mapping as D  # noqa: E402  (flattening only)
 
@@ -491,6 +491,199 @@ def tracks_fixture():
           f"obs={int(tp[-1])}")
 
 
+# --- rig-extrinsic / rolling-shutter BA (mapping.py:321-356)
+
+KIND_CODE = {"pinhole": 0, "pinhole_radial": 1, "equidistant_fisheye": 2}
+
+
+def general_ba_fixture(name, smap, config, stage, mode):
+    """Serialises the object-level inputs, runs sfmkit's bundle_adjust, and
+    stores its outputs."""
+    frames = sorted(smap.keyframes)
+    kf = [smap.keyframes[f] for f in frames]
+    cids = sorted(smap.cameras)
+    lms = smap.landmarks
+    out = dict(
+        kf_id=np.array(frames, np.int64), kf_ts=np.array([k.timestamp for k in kf]),
+        kf_cam=np.array([k.camera_id for k in kf], np.int64),
+        kf_q=np.array([k.cam_from_world.quat for k in kf]), kf_t=np.array([k.cam_from_world.t for k in kf]),
+        kf_rolling=np.array([k.shutter == "rolling" for k in kf], np.uint8),
+        kf_exposure=np.array([k.exposure for k in kf]),
+        cam_id=np.array(cids, np.int64),
+        cam_par=np.array([[KIND_CODE[smap.cameras[c].kind], smap.cameras[c].fx, smap.cameras[c].fy,
+                           smap.cameras[c].cx, smap.cameras[c].cy, smap.cameras[c].width,
+                           smap.cameras[c].height,
+                           *(list(smap.cameras[c].distortion) + [0.0, 0.0])[:2]] for c in cids]),
+        lm_pos=np.array([lm.position for lm in lms]),
+        lm_tri=np.array([lm.track.status == "triangulated" for lm in lms], np.uint8),
+        lm_ptr=np.concatenate([[0], np.cumsum([len(lm.track.observations) for lm in lms])]).astype(np.int64),
+        obs_frame=np.array([o.frame_id for lm in lms for o in lm.track.observations], np.int64),
+        obs_uv=np.array([o.pixel for lm in lms for o in lm.track.observations]),
+        lm_mask=np.concatenate([lm.inlier_mask for lm in lms]).astype(np.uint8),
+        fixed=np.array(sorted(smap.fixed_frames), np.int64),
+        prior=np.array(sorted(f for f, v in smap.provenance.items() if v == "prior"), np.int64),
+        stage=stage, mode=mode, loss_kind=LOSS_CODE[config.stage1.loss.kind],
+        loss_param=float(config.stage1.loss.param), lambda_c=config.lambda_c,
+        lambda_a=config.lambda_a, extrinsic_prior_weight=config.extrinsic_prior_weight,
+        max_iters=config.max_solver_iters)
+    if smap.rig is not None:
+        out.update(rig_ids=np.array(smap.rig.camera_ids, np.int64),
+                   rig_q=np.array([smap.rig.extrinsic(c).quat for c in smap.rig.camera_ids]),
+                   rig_t=np.array([smap.rig.extrinsic(c).t for c in smap.rig.camera_ids]))
+    rep = M.bundle_adjust(smap, config, stage=stage, mode=mode)
+    out.update(ref_initial_cost=rep.initial_cost, ref_final_cost=rep.final_cost,
+               ref_iterations=rep.iterations, ref_termination=rep.termination,
+               ref_kf_q=np.array([smap.keyframes[f].cam_from_world.quat for f in frames]),
+               ref_kf_t=np.array([smap.keyframes[f].cam_from_world.t for f in frames]),
+               ref_lm_pos=np.array([lm.position for lm in lms]))
+    if smap.rig is not None:
+        out.update(ref_rig_q=np.array([smap.rig.extrinsic(c).quat for c in smap.rig.camera_ids]),
+                   ref_rig_t=np.array([smap.rig.extrinsic(c).t for c in smap.rig.camera_ids]))
+    np.savez_compressed(os.path.join(HERE, f"ba_{name}.npz"), **out)
+    print(f"ba_{name}: {rep.termination} iters={rep.iterations} cost {rep.initial_cost:.4g} -> "
+          f"{rep.final_cost:.4g}")
+
+
+def rig_rs_fixtures():
+    from sfmkit.cameras import RigCalibration
+    from sfmkit.se3 import interpolate_pose
+    # rig: test_mapping.py:420-461 scene, and a noisy Huber stage-1 variant
+    for name, n_inst, n_pts, noise, seed, stage, cfg in (
+            ("rig", 5, 40, 0.0, 1, 2, M.MappingConfig(lambda_a=0.0, lambda_c=10.0,
+                                                      extrinsic_prior_weight=1e-6,
+                                                      max_solver_iters=100)),
+            ("rig_huber", 7, 70, 0.4, 2, 1, M.MappingConfig(lambda_c=5.0, extrinsic_prior_weight=1e-3,
+                                                            max_solver_iters=40))):
+        rng = np.random.default_rng(seed)
+        true_E1 = exp_map(np.array([0.0, 0.01, 0.0, 0.5, 0.02, 0.0]))
+        rig = RigCalibration((0, 1), {0: Pose.identity(), 1: true_E1})
+        pts = rng.uniform([-4, -3, 6], [4, 3, 14], (n_pts, 3))
+        kfs, fid, vposes = {}, 0, {}
+        for i in range(n_inst):
+            T_v = cam_pose([0.7 * i, 0.03 * i, 0], (0.01 * i, -0.02 * i, 0.0))
+            vposes[i] = T_v
+            for cid in (0, 1):
+                kfs[fid] = Keyframe(fid, float(i), cid, rig.extrinsic(cid) @ T_v)
+                fid += 1
+        smap = M.SparseMap(kfs, {0: CAM, 1: CAM}, rig=rig)
+        for p in pts:
+            obs = []
+            for f, kf in kfs.items():
+                pix = project(CAM, kf.cam_from_world, p)
+                if 0 <= pix[0] < CAM.width and 0 <= pix[1] < CAM.height:
+                    obs.append(M.Observation(f, 0, pix + (rng.normal(0, noise, 2) if noise else 0.0)))
+            if len(obs) >= 2:
+                smap.landmarks.append(M.Landmark(p.copy(), M.Track(obs, status=M.TRIANGULATED),
+                                                 np.ones(len(obs), bool)))
+        bad_E1 = exp_map(np.array([0.01, -0.005, 0.008, 0.04, -0.03, 0.02])) @ true_E1
+        smap.rig = RigCalibration((0, 1), {0: Pose.identity(), 1: bad_E1})
+        for f, kf in kfs.items():
+            if kf.camera_id == 1:
+                kf.cam_from_world = bad_E1 @ vposes[int(kf.timestamp)]
+        if noise:
+            for lm in smap.landmarks:
+                lm.position = lm.position + rng.normal(0, 0.02, 3)
+        general_ba_fixture(name, smap, cfg, stage, "rig_extrinsic")
+    # rolling shutter: test_mapping.py:463-498 scene, and a longer sequence
+    rng = np.random.default_rng(3)
+    T_a = cam_pose([0, 0, 0])
+    T_b_true = cam_pose([0.6, 0.04, 0.01], (0.02, -0.01, 0.015))
+    pts = rng.uniform([-3, -2, 6], [3, 2, 12], (30, 3))
+    exposure, dt = 0.03, 0.1
+    kfs = {0: Keyframe(0, 0.0, 0, T_a, shutter="rolling", exposure=exposure), 1: Keyframe(1, dt, 0, T_b_true)}
+    smap = M.SparseMap(kfs, {0: CAM}, fixed_frames={0})
+    for p in pts:
+        pix = project(CAM, T_a, p)
+        for _ in range(8):
+            alpha = (pix[1] / (CAM.height - 1)) * exposure / dt
+            pix = project(CAM, interpolate_pose(T_a, T_b_true, alpha), p)
+        pix_b = project(CAM, T_b_true, p)
+        if not all(0 <= q[0] < CAM.width and 0 <= q[1] < CAM.height for q in (pix, pix_b)):
+            continue
+        smap.landmarks.append(M.Landmark(p.copy(), M.Track([M.Observation(0, 0, pix), M.Observation(1, 0, pix_b)],
+                                                           status=M.TRIANGULATED), np.ones(2, bool)))
+    kfs[1].cam_from_world = exp_map(rng.normal(0, 0.005, 6)) @ T_b_true
+    general_ba_fixture("rolling", smap, M.MappingConfig(lambda_a=0.0, lambda_c=0.0, max_solver_iters=100), 2,
+                       "pure")
+    rng = np.random.default_rng(4)
+    n = 8
+    poses = {i: cam_pose([0.5 * i, 0.02 * i, 0], (0.01 * i, -0.015 * i, 0.005 * i)) for i in range(n)}
+    kfs = {i: Keyframe(i, 0.1 * i, 0, poses[i], shutter="rolling", exposure=0.025) for i in range(n)}
+    smap = M.SparseMap(kfs, {0: CAM}, fixed_frames={0})
+    pts = rng.uniform([-4, -3, 6], [8, 3, 16], (80, 3))
+    for p in pts:
+        obs = []
+        for i in range(n):
+            pix = project(CAM, poses[i], p)
+            if i + 1 < n:
+                for _ in range(8):
+                    alpha = (pix[1] / (CAM.height - 1)) * 0.025 / 0.1
+                    pix = project(CAM, interpolate_pose(poses[i], poses[i + 1], alpha), p)
+            if 0 <= pix[0] < CAM.width and 0 <= pix[1] < CAM.height:
+                obs.append(M.Observation(i, 0, pix + rng.normal(0, 0.3, 2)))
+        if len(obs) >= 2:
+            smap.landmarks.append(M.Landmark(p + rng.normal(0, 0.02, 3), M.Track(obs, status=M.TRIANGULATED),
+                                             np.ones(len(obs), bool)))
+    for i in range(1, n):
+        kfs[i].cam_from_world = exp_map(rng.normal(0, 0.003, 6)) @ poses[i]
+    general_ba_fixture("rolling_seq", smap, M.MappingConfig(max_solver_iters=40), 1, "pure")
+
+
+def iterative_map_rolling_fixture(name="iterative_map_rolling"):
+    """iterative_map (mapping.py:569-624) over rolling-shutter keyframes:
+    observations from the interpolated-pose model (mapping.py:321-356), a
+    gross outlier on every 5th track, and pending tracks throughout."""
+    rng = np.random.default_rng(21)
+    n, exposure, dt = 7, 0.006, 0.1
+    poses = {i: cam_pose([0.5 * i, 0.02 * i, 0], (0.01 * i, -0.015 * i, 0.005 * i)) for i in range(n)}
+    pts = rng.uniform([-4, -3, 6], [8, 3, 16], (60, 3))
+    tracks = []
+    for k, p in enumerate(pts):
+        obs = []
+        for i in range(n):
+            pix = project(CAM, poses[i], p)
+            if i + 1 < n:
+                for _ in range(8):
+                    alpha = (pix[1] / (CAM.height - 1)) * exposure / dt
+                    pix = project(CAM, interpolate_pose(poses[i], poses[i + 1], alpha), p)
+            if 0 <= pix[0] < CAM.width and 0 <= pix[1] < CAM.height:
+                obs.append(M.Observation(i, 0, pix + rng.normal(0, 0.3, 2)))
+        if len(obs) < 3:
+            continue
+        if k % 5 == 0:
+            obs[1] = M.Observation(obs[1].frame_id, 0, obs[1].pixel + np.array([40.0, 30.0]))
+        tracks.append(M.Track(obs))
+    kfs = [Keyframe(i, dt * i, 0, poses[i], shutter="rolling", exposure=exposure) for i in range(n)]
+    for kf in kfs[1:]:
+        kf.cam_from_world = exp_map(rng.normal(0, 0.003, 6)) @ kf.cam_from_world
+    q0 = np.array([kf.cam_from_world.quat for kf in kfs])
+    t0 = np.array([kf.cam_from_world.t for kf in kfs])
+    ptr = np.zeros(len(tracks) + 1, np.int64)
+    ptr[1:] = np.cumsum([len(t.observations) for t in tracks])
+    of = np.array([o.frame_id for t in tracks for o in t.observations], np.int32)
+    uv = np.array([o.pixel for t in tracks for o in t.observations])
+    config = M.MappingConfig(max_solver_iters=30)
+    smap = M.iterative_map(kfs, tracks, {0: CAM}, config=config)
+    lm_track = np.array([next(i for i, t in enumerate(tracks) if t is lm.track)
+                         for lm in smap.landmarks], np.int64)
+    rs = smap.round_stats
+    np.savez_compressed(
+        os.path.join(HERE, f"{name}.npz"), cam_q=q0, cam_t=t0, track_ptr=ptr, obs_frame=of,
+        obs_uv=uv, kf_timestamp=np.array([kf.timestamp for kf in kfs]),
+        kf_exposure=np.full(n, exposure),
+        ref_cam_q=np.array([smap.keyframes[f].cam_from_world.quat for f in range(n)]),
+        ref_cam_t=np.array([smap.keyframes[f].cam_from_world.t for f in range(n)]),
+        ref_lm_track=lm_track, ref_lm_X=np.array([lm.position for lm in smap.landmarks]),
+        ref_lm_mask=np.concatenate([lm.inlier_mask for lm in smap.landmarks]).astype(np.uint8),
+        ref_status=np.array([{"pending": 0, "triangulated": 1, "failed": 2}[t.status] for t in tracks]),
+        ref_round_added=np.array([r["added"] for r in rs]),
+        ref_round_removed=np.array([r["removed"] for r in rs]),
+        ref_round_landmarks=np.array([r["landmarks"] for r in rs]),
+        ref_mean_err=M.mean_reprojection_error(smap))
+    print(f"{name}: tracks={len(tracks)} landmarks={len(smap.landmarks)} rounds={len(rs)} "
+          f"added={[r['added'] for r in rs]} removed={[r['removed'] for r in rs]}")
+
+
 # --- known-answer vectors for the geometry --------------------------------------
 
 def kat_fixture():
@@ -530,13 +723,16 @@ def kat_fixture():
 
 
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["kat", "tri", "gate", "imap", "ba", "kinds", "tracks"]
+    which = sys.argv[1:] or ["kat", "tri", "gate", "imap", "ba", "kinds", "tracks", "rigrs"]
     if "kat" in which:
         kat_fixture()
     if "kinds" in which:
         camera_kinds_fixtures()
     if "tracks" in which:
         tracks_fixture()
+    if "rigrs" in which:
+        rig_rs_fixtures()
+        iterative_map_rolling_fixture()
     if "tri" in which:
         tri_fixtures()
     if "gate" in which:

@@ -39,7 +39,8 @@ def test_ctypes_struct_layout_matches_header(tmp_path):
     structs = {"sfm_camera_model": nat.CameraModelC, "sfm_ba_problem": nat.BAProblemC,
                "sfm_ba_options": nat.BAOptionsC, "sfm_ba_report": nat.BAReportC,
                "sfm_tracks": nat.TracksC, "sfm_map_problem": nat.MapProblemC,
-               "sfm_map_options": nat.MapOptionsC, "sfm_round_stat": nat.RoundStatC}
+               "sfm_map_options": nat.MapOptionsC, "sfm_round_stat": nat.RoundStatC,
+               "sfm_gba_problem": nat.GbaProblemC}
     lines = ["#include <stdio.h>", "#include <stddef.h>", '#include "sfm_b200.h"', "int main(void){"]
     for cname, cls in structs.items():
         lines.append(f'printf("{cname} %zu\\n", sizeof({cname}));')
@@ -114,7 +115,9 @@ def test_no_gauge_raised_before_device_call():
         bundle_adjust(smap, MappingConfig(lambda_a=0.0, lambda_c=0.0), stage=2)
 
 
-def test_unsupported_modes_raise_not_implemented():
+def test_single_slot_flatten_rejects_two_slot_problems():
+    """flatten_ba is the single-slot (global-shutter, non-rig) layout;
+    bundle_adjust routes rolling-shutter / rig problems to sfm_gba_solve."""
     from paper_2510_15271_b200 import (CameraModel, Keyframe, MappingConfig, Pose, SparseMap,
                                        flatten_ba)
     cam = CameraModel("pinhole", 500.0, 500.0, 320.0, 240.0, 640, 480)

@@ -192,13 +192,15 @@ def test_gate_matches_reference(golden):
 def imap_config(case):
     from paper_2510_15271_b200 import MappingConfig, StageConfig
     from paper_2510_15271_b200.solver import RobustLoss
+    if case == "iterative_map_rolling":
+        return MappingConfig(max_solver_iters=30)
     if case == "iterative_map_large":  # tests/golden/make_golden.py
         return MappingConfig(stage1=StageConfig(4.0, RobustLoss("cauchy", 1.0)), lambda_c=0.5,
                              lambda_a=2.0, max_solver_iters=25)
     return MappingConfig()
 
 
-@pytest.mark.parametrize("case", ["iterative_map", "iterative_map_large"])
+@pytest.mark.parametrize("case", ["iterative_map", "iterative_map_large", "iterative_map_rolling"])
 def test_iterative_map_matches_reference(golden, case):
     """The device-resident loop (sfm_iterative_map) through the object-level
     drop-in: track status, landmark order, masks, positions, poses and
@@ -207,7 +209,13 @@ def test_iterative_map_matches_reference(golden, case):
                                        iterative_map, mean_reprojection_error)
     d = golden(case)
     cam = CameraModel("pinhole", 500.0, 500.0, 320.0, 240.0, 640, 480)
-    kfs = [Keyframe(f, float(f), 0, Pose(d["cam_q"][f], d["cam_t"][f])) for f in range(len(d["cam_q"]))]
+    if "kf_exposure" in d:  # rolling-shutter keyframes: the host-driven loop + sfm_gba_solve
+        kfs = [Keyframe(f, float(d["kf_timestamp"][f]), 0, Pose(d["cam_q"][f], d["cam_t"][f]),
+                        shutter="rolling", exposure=float(d["kf_exposure"][f]))
+               for f in range(len(d["cam_q"]))]
+    else:
+        kfs = [Keyframe(f, float(f), 0, Pose(d["cam_q"][f], d["cam_t"][f]))
+               for f in range(len(d["cam_q"]))]
     ptr = d["track_ptr"]
     tracks = [Track([Observation(int(d["obs_frame"][o]), 0, d["obs_uv"][o])
                      for o in range(ptr[i], ptr[i + 1])]) for i in range(len(ptr) - 1)]
@@ -294,3 +302,65 @@ def test_point_sharded_depth_failure_matches_single_rank(golden):
     with pytest.raises(NonPositiveDepth):
         solve_sharded_emulated(arrays_from_npz(d), RobustLoss("huber", 2.0), SolverOptions(max_iters=5),
                                DeviceOptions(linear_solver="pcg"), 2)
+
+
+KIND_NAMES = {0: "pinhole", 1: "pinhole_radial", 2: "equidistant_fisheye"}
+
+
+def general_map_from_npz(d):
+    from paper_2510_15271_b200 import (CameraModel, Keyframe, Landmark, Observation, Pose,
+                                       RigCalibration, SparseMap, Track)
+    cams = {}
+    for cid, par in zip(d["cam_id"], d["cam_par"]):
+        kind = KIND_NAMES[int(par[0])]
+        cams[int(cid)] = CameraModel(kind, *[float(v) for v in par[1:5]], int(par[5]), int(par[6]),
+                                     tuple(float(v) for v in par[7:9]) if kind == "pinhole_radial" else ())
+    kfs = {}
+    for i, fid in enumerate(d["kf_id"]):
+        kfs[int(fid)] = Keyframe(int(fid), float(d["kf_ts"][i]), int(d["kf_cam"][i]),
+                                 Pose(d["kf_q"][i], d["kf_t"][i]),
+                                 shutter="rolling" if d["kf_rolling"][i] else "global",
+                                 exposure=float(d["kf_exposure"][i]))
+    rig = None
+    if "rig_ids" in d:
+        rig = RigCalibration(tuple(int(c) for c in d["rig_ids"]),
+                             {int(c): Pose(d["rig_q"][k], d["rig_t"][k]) for k, c in enumerate(d["rig_ids"])})
+    lms = []
+    ptr = d["lm_ptr"]
+    for i in range(len(d["lm_pos"])):
+        obs = [Observation(int(d["obs_frame"][o]), 0, d["obs_uv"][o]) for o in range(ptr[i], ptr[i + 1])]
+        lms.append(Landmark(d["lm_pos"][i], Track(obs, "triangulated" if d["lm_tri"][i] else "pending"),
+                            d["lm_mask"][ptr[i]:ptr[i + 1]].astype(bool)))
+    return SparseMap(kfs, cams, lms, rig, {int(f): "prior" for f in d["prior"]},
+                     {int(f) for f in d["fixed"]})
+
+
+@pytest.mark.parametrize("case", ["rig", "rig_huber", "rolling", "rolling_seq"])
+def test_rig_and_rolling_shutter_ba_match_reference(golden, case):
+    """bundle_adjust with rig-extrinsic residuals
+    (refine-extrinsics, mapping.py:321-333) and rolling-shutter residuals
+    (mapping.py:336-356) -- two SE(3) slots per residual, solved on the
+    device (sfm_gba_solve) -- against sfmkit's results."""
+    from paper_2510_15271_b200 import MappingConfig, StageConfig, bundle_adjust
+    from paper_2510_15271_b200.solver import RobustLoss
+    d = golden("ba_" + case)
+    smap = general_map_from_npz(d)
+    cfg = MappingConfig(stage1=StageConfig(4.0, RobustLoss(LOSS_NAMES[int(d["loss_kind"])],
+                                                           float(d["loss_param"]))),
+                        lambda_c=float(d["lambda_c"]), lambda_a=float(d["lambda_a"]),
+                        extrinsic_prior_weight=float(d["extrinsic_prior_weight"]),
+                        max_solver_iters=int(d["max_iters"]))
+    rep = bundle_adjust(smap, cfg, stage=int(d["stage"]), mode=str(d["mode"]))
+    assert rep.initial_cost == pytest.approx(float(d["ref_initial_cost"]), rel=1e-10)
+    assert rep.final_cost == pytest.approx(float(d["ref_final_cost"]), rel=1e-6, abs=1e-12)
+    frames = sorted(smap.keyframes)
+    q = np.array([smap.keyframes[f].cam_from_world.quat for f in frames])
+    t = np.array([smap.keyframes[f].cam_from_world.t for f in frames])
+    scale = max(1.0, np.abs(d["ref_lm_pos"]).max())
+    np.testing.assert_allclose(q, d["ref_kf_q"], atol=1e-7)
+    np.testing.assert_allclose(t, d["ref_kf_t"], atol=1e-6 * scale)
+    np.testing.assert_allclose([lm.position for lm in smap.landmarks], d["ref_lm_pos"], atol=1e-6 * scale)
+    if "ref_rig_q" in d:
+        ids = [int(c) for c in d["rig_ids"]]
+        np.testing.assert_allclose([smap.rig.extrinsic(c).quat for c in ids], d["ref_rig_q"], atol=1e-7)
+        np.testing.assert_allclose([smap.rig.extrinsic(c).t for c in ids], d["ref_rig_t"], atol=1e-6)

@@ -290,12 +290,11 @@ def test_ba_relative_consistency_terms(rng):
         assert smap.keyframes[f].cam_from_world.almost_equal(pose, tol=1e-8)
 
 
-def test_rig_and_rolling_shutter_modes_are_next_rows(rng):
-    """rig-extrinsic mode and rolling-shutter keyframes
-    raise NotImplementedError before any device work."""
+def test_rig_mode_without_rig_raises_no_gauge(rng):
+    """mapping.py:424-425: rig_extrinsic mode needs a rig calibration."""
     points, poses = scene(rng, n_frames=3, n_points=10)
     smap = map_from_scene(points, poses)
-    with pytest.raises(NotImplementedError):
+    with pytest.raises(NoGauge):
         bundle_adjust(smap, MappingConfig(), stage=1, mode="rig_extrinsic")
 
 
