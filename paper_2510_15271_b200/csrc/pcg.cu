@@ -19,7 +19,10 @@ namespace {
 
 constexpr int kNB = 48;          // Gauss-Jordan tile (8 clusters x 6)
 constexpr int kGJThreads = 256;
-constexpr int kPcgMaxThreads = 1024;  // CTA size chosen at setup (512 or 1024)
+#ifndef SFM_PCG_MAXT
+#define SFM_PCG_MAXT 512
+#endif
+constexpr int kPcgMaxThreads = SFM_PCG_MAXT;  // CTA size chosen at setup (512 or 1024)
 #define kPcgThreads ((int)blockDim.x)
 #define kPcgWarps ((int)(blockDim.x >> 5))
 
@@ -468,6 +471,7 @@ struct PcgSmem {
   double* Ssm;  // [resblocks*36] resident S blocks
   double* zc;   // [maxdist*6] z cache (distinct columns of the CTA's rows)
   int* lc;      // [maxblk] local column index of each of the CTA's blocks
+  int2* rs;     // [maxrows] (first segment, count) of each of the CTA's rows
 };
 
 // z_i = D_i^-1 r_i (+ P_i e) for lanes 0..5 of the warp owning local row i
@@ -581,6 +585,20 @@ __device__ __forceinline__ double2 block_sum2(double u, double v, double2* red) 
   return r;
 }
 
+#ifdef SFM_PCG_PHASES  // A/B instrumentation: per-phase cycles on CTA 0, thread 0
+#define PH_INIT() long long ph_t = clock64(), ph[11] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0}
+#define PH(k) do { const long long t_ = clock64(); ph[k] += t_ - ph_t; ph_t = t_; } while (0)
+#define PH_DUMP(it) do { if (blockIdx.x == 0 && threadIdx.x == 0 && (it) > 0) \
+  printf("PCGPH it=%d spmv=%lld row1=%lld sync1=%lld gather=%lld coarse=%lld row2=%lld sync2=%lld zc=%lld" \
+         " r1loop=%lld r1rpart=%lld r1bsum=%lld\n", \
+         (it), ph[0] / (it), ph[1] / (it), ph[2] / (it), ph[3] / (it), ph[4] / (it), ph[5] / (it), \
+         ph[6] / (it), ph[7] / (it), ph[8] / (it), ph[9] / (it), ph[10] / (it)); } while (0)
+#else
+#define PH_INIT() do {} while (0)
+#define PH(k) do {} while (0)
+#define PH_DUMP(it) do {} while (0)
+#endif
+
 __global__ void __launch_bounds__(kPcgMaxThreads, 1) k_pcg3(Pcg3Args a) {
   cg::grid_group grid = cg::this_grid();
   extern __shared__ double psm[];
@@ -600,6 +618,7 @@ __global__ void __launch_bounds__(kPcgMaxThreads, 1) k_pcg3(Pcg3Args a) {
   m.Ssm = m.Pc + 36 * MR;
   m.zc = m.Ssm + 36 * a.resblocks;
   m.lc = reinterpret_cast<int*>(m.zc + 6 * a.maxdist);
+  m.rs = reinterpret_cast<int2*>(m.lc + ((a.maxblk + 1) & ~1));
   __shared__ double2 red[32];
   __shared__ double tmp[16];
   __shared__ double e[6];
@@ -651,6 +670,7 @@ __global__ void __launch_bounds__(kPcgMaxThreads, 1) k_pcg3(Pcg3Args a) {
       m.Ae[t] = a.Aci[(int64_t)(6 * k + t / n6) * a.npad + t % n6];
   }
   for (int t = threadIdx.x; t < nblk; t += kPcgThreads) m.lc[t] = __ldg(a.lcol + kc0 + t);
+  for (int t = threadIdx.x; t < nrows; t += kPcgThreads) m.rs[t] = a.rowseg[row0 + t];
   // resident S blocks: the head of every warp's chunk (18 double2 per block)
   for (int w = 0; w < kPcgWarps; ++w) {
     const int4 ch = a.wchunk[blockIdx.x * kPcgWarps + w];
@@ -687,7 +707,7 @@ __global__ void __launch_bounds__(kPcgMaxThreads, 1) k_pcg3(Pcg3Args a) {
     double xb = 0.0, xw = 0.0;
     for (int i = warp; i < nrows; i += kPcgWarps)
       if (lane < 6) {
-        const int2 rs = a.rowseg[row0 + i];
+        const int2 rs = m.rs[i];
         double w = 0.0;
         for (int sg = 0; sg < rs.y; ++sg) w += m.seg[(rs.x + sg) * 6 + lane];
         m.q[i * 6 + lane] = w;  // S x0, consumed by the prologue below
@@ -749,15 +769,17 @@ __global__ void __launch_bounds__(kPcgMaxThreads, 1) k_pcg3(Pcg3Args a) {
   if (!(bnorm > 0.0) || !isfinite(bnorm)) {
     fail = !isfinite(bnorm);
   } else {
+    PH_INIT();
     for (it = 0; it < a.max_it;) {
       // ---- phase 1: w = S z; p = z + beta p; q = w + beta q; P^T q --------
       spmv_segments(a, m.zc, m.lc, kc0, m.seg, m.Ssm);
       __syncthreads();
+      PH(0);
       double pq_l = 0.0;
       for (int i = warp; i < nrows; i += kPcgWarps) {
         double qv = 0.0;
         if (lane < 6) {
-          const int2 rs = a.rowseg[row0 + i];
+          const int2 rs = m.rs[i];
           double w = 0.0;
           for (int sg = 0; sg < rs.y; ++sg) w += m.seg[(rs.x + sg) * 6 + lane];
           const double pv = m.z[i * 6 + lane] + beta * m.p[i * 6 + lane];
@@ -771,16 +793,23 @@ __global__ void __launch_bounds__(kPcgMaxThreads, 1) k_pcg3(Pcg3Args a) {
           if (lane < 6) m.y[i * 6 + lane] = yv;
         }
       }
+      PH(8);
       if (two) write_rpart();
+      PH(9);
       const double2 s = block_sum2(pq_l, 0.0, red);
       if (threadIdx.x == 0) part_pq[blockIdx.x] = s.x;
+      PH(10);
+      PH(1);
       grid.sync();
+      PH(2);
       // ---- phase 2: x += alpha p; r -= alpha q; rc -= alpha P^T q; z = M^-1 r
       gather_after_sync(a, part_pq, sums, 1, m.rc, two, false, &rz_old, &sums[0]);
       const double pq = sums[0];
       if (!(pq > 0.0) || !isfinite(pq)) { fail = 1; break; }
       const double alpha = rz_old / pq;
+      PH(3);
       if (two) coarse_apply(a, m, e, tmp);
+      PH(4);
       double rz_n = 0.0, rr_n = 0.0;
       for (int i = warp; i < nrows; i += kPcgWarps) {
         double ri = 0.0;
@@ -799,8 +828,11 @@ __global__ void __launch_bounds__(kPcgMaxThreads, 1) k_pcg3(Pcg3Args a) {
       }
       const double2 t = block_sum2(rz_n, rr_n, red);
       if (threadIdx.x == 0) { part_rz[blockIdx.x] = t.x; part_rz[G + blockIdx.x] = t.y; }
+      PH(5);
       grid.sync();
+      PH(6);
       sums_and_zc(part_rz, 2);
+      PH(7);
       const double rz_new = sums[0], rr = sums[1];
       ++it;
       if (!isfinite(rr) || !isfinite(rz_new)) { fail = 1; break; }
@@ -808,6 +840,7 @@ __global__ void __launch_bounds__(kPcgMaxThreads, 1) k_pcg3(Pcg3Args a) {
       beta = rz_new / rz_old;
       rz_old = rz_new;
     }
+    PH_DUMP(it);
   }
   for (int i = warp; i < nrows; i += kPcgWarps)
     if (lane < 6) a.x[(row0 + i) * 6 + lane] = m.x[i * 6 + lane];
@@ -841,16 +874,26 @@ void TwoLevelPcg::set_pattern(const int* row_ptr, const int* col, int nnzb, cuda
   const int64_t kRowCost = 4;
   auto cost_upto = [&](int r) { return (int64_t)rp[r] + kRowCost * r; };
   const int64_t total = cost_upto(nf_);
-  // CTA size: 1024 threads x 1 per SM (default) or 512 x 2 (SFM_PCG_CTA=512)
-  nt_ = 1024;
-  if (const char* e = std::getenv("SFM_PCG_CTA")) nt_ = std::atoi(e) == 512 ? 512 : 1024;
+  // CTA size: 512 threads x 1 per SM.  Measured on config 3: 16.2 us per
+  // iteration vs 17.7 with 1024 threads, whose 64-register cap spills in
+  // the row loops (SFM_PCG_CTA / -DSFM_PCG_MAXT=1024 to compare).
+  nt_ = kPcgMaxThreads;
+  if (const char* e = std::getenv("SFM_PCG_CTA")) {
+    const int v = std::atoi(e);
+    if (v >= 512 && v <= 1024 && v % 32 == 0) nt_ = v;
+  }
   const int nwarps = nt_ / 32;
   if (const char* e = std::getenv("SFM_COARSE_REFRESH")) refresh_ = std::max(1, std::atoi(e));
   lin_count_ = 0;
   have_prev_ = false;
   warm_ = true;
   if (const char* e = std::getenv("SFM_PCG_WARM")) warm_ = std::atoi(e) != 0;
-  int G = std::min((1024 / nt_) * nsm, nf_);
+  nt_ = std::min(nt_, kPcgMaxThreads);
+  int per_sm = 0;  // co-resident CTAs per SM the register budget allows
+  SFM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pcg3, nt_, 0));
+  per_sm = std::max(1, std::min(per_sm, 1024 / nt_));
+  if (const char* e = std::getenv("SFM_PCG_PERSM")) per_sm = std::max(1, std::min(per_sm, std::atoi(e)));
+  int G = std::min(per_sm * nsm, nf_);
   std::vector<int> row0;
   for (;;) {
     row0.assign(1, 0);
@@ -939,8 +982,9 @@ void TwoLevelPcg::set_pattern(const int* row_ptr, const int* col, int nnzb, cuda
   // (the head of each warp's chunk, the same fraction in every warp)
   int max_smem = 0;
   SFM_CUDA(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
-  const size_t per_cta_avail = (size_t)max_smem / (1024 / nt_) - 2048;  // static smem margin
-  const size_t zbytes = sizeof(double) * 6 * (size_t)maxdist_ + sizeof(int) * (size_t)maxblk_ + 16;
+  const size_t per_cta_avail = (size_t)max_smem / per_sm - 2048;  // static smem margin
+  const size_t zbytes = sizeof(double) * 6 * (size_t)maxdist_ + sizeof(int) * (size_t)(maxblk_ + 1) +
+                        sizeof(int2) * maxrows_ + 16;
   SFM_REQUIRE(smem_ + zbytes <= per_cta_avail, "PCG z cache does not fit in shared memory");
   // Measured on config 3: keeping S blocks resident costs the L1 capacity
   // the rest of the loop relies on and is slower (20.5 vs 18.2 us/iteration),
@@ -965,11 +1009,11 @@ void TwoLevelPcg::set_pattern(const int* row_ptr, const int* col, int nnzb, cuda
   }
   resblocks_ = maxres;
   smem_ += sizeof(double) * 36 * (size_t)maxres;
-  smem_ += sizeof(double) * 6 * (size_t)maxdist_ + sizeof(int) * (size_t)maxblk_ + 16;
+  smem_ += sizeof(double) * 6 * (size_t)maxdist_ + sizeof(int) * (size_t)(maxblk_ + 1) + sizeof(int2) * maxrows_ + 16;
   SFM_CUDA(cudaFuncSetAttribute(k_pcg3, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_));
-  int per_sm = 0;
-  SFM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pcg3, nt_, smem_));
-  SFM_REQUIRE(per_sm > 0 && G <= per_sm * nsm, "PCG grid cannot be made co-resident");
+  int resident = 0;
+  SFM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&resident, k_pcg3, nt_, smem_));
+  SFM_REQUIRE(resident > 0 && G <= resident * nsm, "PCG grid cannot be made co-resident");
   cta_row0_.upload(row0.data(), row0.size(), s);
   wchunk_.upload(wchunk.data(), wchunk.size(), s);
   wres_.upload(wres.data(), wres.size(), s);
