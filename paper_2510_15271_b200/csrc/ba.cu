@@ -67,6 +67,9 @@ struct BlkArgs {
   const double* cm_uv;         // camera-major pixels
   const double4* geo_cm;       // camera-major linearisation records
   const int* diag_pos;         // [nf] BSR slot of the diagonal blocks
+  const int4* offrec;          // [2*n] off-diagonal work: {frame lo, frame hi, model lo, model hi},
+                               //   {pos_up, pos_lo, edge, 0}
+  const longlong2* offk;       // [n] pair range of each off-diagonal block
   const double* U;
   const double* Dc;
   const double* gc;
@@ -649,6 +652,27 @@ __device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, dou
 constexpr int kOffWarps = 4;
 constexpr int kOffLd = 13;  // padded row of the staged factors (bank spread)
 
+// One packed header per off-diagonal work item (structure build): the
+// kernel's prologue is then one independent load instead of the
+// work -> key -> frame -> pose / pair-range chain.
+__global__ void k_off_records(int n, const int* __restrict__ work, const unsigned long long* __restrict__ ub_key,
+                              int nf, const int* __restrict__ ub_pb, const int* __restrict__ ub_edge,
+                              const int* __restrict__ pos_up, const int* __restrict__ pos_lo,
+                              const int* __restrict__ free_frame, const int* __restrict__ frame_model,
+                              const int64_t* __restrict__ pb_pair_ptr, int4* __restrict__ rec,
+                              longlong2* __restrict__ kr) {
+  const int w = blockIdx.x * blockDim.x + threadIdx.x;
+  if (w >= n) return;
+  const int u = work[w];
+  const unsigned long long key = ub_key[u];
+  const int lo = (int)(key / nf), hi = (int)(key % nf);
+  const int fa = free_frame[lo], fb = free_frame[hi];
+  const int pb = ub_pb[u];
+  rec[2 * w] = make_int4(fa, fb, frame_model[fa], frame_model[fb]);
+  rec[2 * w + 1] = make_int4(pos_up[u], pos_lo[u], ub_edge[u], 0);
+  kr[w] = pb >= 0 ? make_longlong2(pb_pair_ptr[pb], pb_pair_ptr[pb + 1]) : make_longlong2(0, 0);
+}
+
 __global__ void __launch_bounds__(kOffWarps * 32, 5) k_offdiag_blocks(BlkArgs a) {
   __shared__ double Ast[kOffWarps][32 * kOffLd];
   __shared__ double Bst[kOffWarps][32 * kOffLd];
@@ -657,31 +681,29 @@ __global__ void __launch_bounds__(kOffWarps * 32, 5) k_offdiag_blocks(BlkArgs a)
   const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (w >= a.n) return;
-  const int u = a.work[w];
-  const unsigned long long key = a.ub_key[u];
-  const int lo = (int)(key / a.nf), hi = (int)(key % a.nf);
-  const int pb = a.ub_pb[u];
+  const int4 hd = __ldg(a.offrec + 2 * w);
+  const int4 out = __ldg(a.offrec + 2 * w + 1);
+  const longlong2 kr = __ldg(a.offk + w);
   double d0 = 0.0, d1 = 0.0, e0 = 0.0, e1 = 0.0;
   const int fr = lane >> 2;          // fragment row (A) / column (B)
   const int fk = lane & 3;           // fragment k: pair (fk >> 1), component (fk & 1)
-  if (pb >= 0) {
+  if (kr.y > kr.x) {
     // warp-uniform cameras staged in shared memory (keeps registers for
     // the per-pair factors)
-    const int fa = a.free_frame[lo], fb = a.free_frame[hi];
     if (lane < 9) {
-      Rsm[warp][0].m[lane] = __ldg(a.Rt + (int64_t)fa * 12 + lane);
-      Rsm[warp][1].m[lane] = __ldg(a.Rt + (int64_t)fb * 12 + lane);
+      Rsm[warp][0].m[lane] = __ldg(a.Rt + (int64_t)hd.x * 12 + lane);
+      Rsm[warp][1].m[lane] = __ldg(a.Rt + (int64_t)hd.y * 12 + lane);
     }
     if (lane == 0) {
-      Csm[warp][0] = a.models[a.frame_model[fa]];
-      Csm[warp][1] = a.models[a.frame_model[fb]];
+      Csm[warp][0] = a.models[hd.z];
+      Csm[warp][1] = a.models[hd.w];
     }
     __syncwarp();
     const Mat3& Ra = Rsm[warp][0];
     const Mat3& Rb = Rsm[warp][1];
     const sfm_camera_model& ca = Csm[warp][0];
     const sfm_camera_model& cb = Csm[warp][1];
-    const int64_t k0 = a.pb_pair_ptr[pb], k1 = a.pb_pair_ptr[pb + 1];
+    const int64_t k0 = kr.x, k1 = kr.y;
     double* As = &Ast[warp][lane * kOffLd];
     double* Bs = &Bst[warp][lane * kOffLd];
     for (int64_t kb = k0; kb < k1; kb += 32) {
@@ -740,15 +762,15 @@ __global__ void __launch_bounds__(kOffWarps * 32, 5) k_offdiag_blocks(BlkArgs a)
   d1 += e1;
   const int c0 = 2 * fk;
   if (fr < 6 && c0 < 6) {
-    if (a.rank == 0 && a.ub_edge[u] >= 0) {
-      const double* H = a.edge_H + (int64_t)a.ub_edge[u] * 36;
+    if (a.rank == 0 && out.z >= 0) {
+      const double* H = a.edge_H + (int64_t)out.z * 36;
       d0 += H[fr * 6 + c0];
       d1 += H[fr * 6 + c0 + 1];
     }
-    double* up = a.S + (int64_t)a.pos_up[u] * 36;
+    double* up = a.S + (int64_t)out.x * 36;
     up[fr * 6 + c0] = d0;
     up[fr * 6 + c0 + 1] = d1;
-    double* dn = a.S + (int64_t)a.pos_lo[u] * 36;
+    double* dn = a.S + (int64_t)out.y * 36;
     dn[c0 * 6 + fr] = d0;
     dn[(c0 + 1) * 6 + fr] = d1;
   }
@@ -1548,6 +1570,14 @@ void BASolver::setup(const sfm_ba_problem& pr, const sfm_ba_options& opt) {
       if (hk[u] / nfree_ != hk[u] % nfree_) off.push_back(u);
     n_off_ = (int)off.size();
     work_.upload(off.data(), off.size(), s);
+    offrec_.resize((size_t)2 * n_off_);
+    offk_.resize(n_off_);
+    if (n_off_) {
+      k_off_records<<<grid_for(n_off_, 256), 256, 0, s>>>(
+          n_off_, work_.get(), ub_key_.get(), nfree_, ub_pb_.get(), ub_edge_.get(), ub_pos_up_.get(),
+          ub_pos_lo_.get(), free_frame_.get(), frame_model_.get(), pb_pair_ptr_.get(), offrec_.get(), offk_.get());
+      SFM_CHECK_LAUNCH();
+    }
   }
   tm.mark("camera-major streams");
   // pose terms per free camera (edge side 0 = from/a, 1 = to/b, prior 2)
@@ -1766,6 +1796,7 @@ void BASolver::linearize() {
 BlkArgs BASolver::blk_args(double lam) const {
   BlkArgs ba{};
   ba.work = work_.get(); ba.nf = nfree_; ba.rank = rank_; ba.lam = lam;
+  ba.offrec = offrec_.get(); ba.offk = offk_.get();
   ba.ub_key = ub_key_.get(); ba.ub_pb = ub_pb_.get(); ba.ub_edge = ub_edge_.get();
   ba.pos_up = ub_pos_up_.get(); ba.pos_lo = ub_pos_lo_.get(); ba.diag_ub = diag_ub_.get();
   ba.pb_pair_ptr = pb_pair_ptr_.get(); ba.pairs = pairs_.get(); ba.op = obs_point_.get();

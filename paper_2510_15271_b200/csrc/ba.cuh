@@ -99,6 +99,8 @@ class BASolver {
   DevBuf<unsigned long long> pairs_;     // (obs_lo << 32) | obs_hi
   DevBuf<int64_t> pb_pair_ptr_;          // [n_pb+1] pair range per pair block
   DevBuf<int> work_;                     // [n_off] off-diagonal S blocks (row-major)
+  DevBuf<int4> offrec_;                  // [2*n_off] packed work headers (k_off_records)
+  DevBuf<longlong2> offk_;               // [n_off] pair range per off-diagonal block
   DevBuf<int> pair_pt_;                  // [n_pairs] point of each pair
   int n_off_ = 0;
   int64_t n_cm_ = 0;                     // observations in free cameras
