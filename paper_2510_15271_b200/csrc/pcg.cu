@@ -588,11 +588,19 @@ __device__ __forceinline__ double2 block_sum2(double u, double v, double2* red) 
 #ifdef SFM_PCG_PHASES  // A/B instrumentation: per-phase cycles on CTA 0, thread 0
 #define PH_INIT() long long ph_t = clock64(), ph[11] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0}
 #define PH(k) do { const long long t_ = clock64(); ph[k] += t_ - ph_t; ph_t = t_; } while (0)
+#ifdef SFM_PCG_PHASES_ALL  // every CTA (pipe through tools/pcg_phases.py)
+#define PH_DUMP(it) do { if (threadIdx.x == 0 && (it) > 0) \
+  printf("PCGCTA %d rows=%d blk=%d it=%d spmv=%lld row1=%lld sync1=%lld gather=%lld coarse=%lld row2=%lld " \
+         "sync2=%lld zc=%lld r1loop=%lld r1rpart=%lld r1bsum=%lld\n", blockIdx.x, nrows, nblk, \
+         (it), ph[0] / (it), ph[1] / (it), ph[2] / (it), ph[3] / (it), ph[4] / (it), ph[5] / (it), \
+         ph[6] / (it), ph[7] / (it), ph[8] / (it), ph[9] / (it), ph[10] / (it)); } while (0)
+#else
 #define PH_DUMP(it) do { if (blockIdx.x == 0 && threadIdx.x == 0 && (it) > 0) \
   printf("PCGPH it=%d spmv=%lld row1=%lld sync1=%lld gather=%lld coarse=%lld row2=%lld sync2=%lld zc=%lld" \
          " r1loop=%lld r1rpart=%lld r1bsum=%lld\n", \
          (it), ph[0] / (it), ph[1] / (it), ph[2] / (it), ph[3] / (it), ph[4] / (it), ph[5] / (it), \
          ph[6] / (it), ph[7] / (it), ph[8] / (it), ph[9] / (it), ph[10] / (it)); } while (0)
+#endif
 #else
 #define PH_INIT() do {} while (0)
 #define PH(k) do {} while (0)
