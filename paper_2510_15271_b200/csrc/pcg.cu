@@ -406,7 +406,7 @@ __device__ __forceinline__ double dot6_ss(const double* s, const double* v) {  /
 // The head of every warp's chunk (wres.x blocks) is resident in shared
 // memory for the whole solve (Ssm).
 __device__ __forceinline__ void spmv_segments(const Pcg3Args& a, const double* zc, const int* lc, int kc0,
-                                              double* seg, const double* Ssm) {
+                                              double* seg, const double* Ssm, const int* rpl) {
   const unsigned full = 0xffffffffu;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int grp = lane / 6, comp = lane % 6;
@@ -418,7 +418,7 @@ __device__ __forceinline__ void spmv_segments(const Pcg3Args& a, const double* z
   const double* Sres = Ssm + ((int64_t)wr.y - ch.x) * 36 + comp * 6;  // Sres + k*36 for resident k
   const int* lcb = lc - kc0;                       // lcb[k] for global block k
   while (kb < ke) {
-    const int re = min(ke, __ldg(a.row_ptr + r + 1));
+    const int re = min(ke, rpl[r + 1]);  // row ends staged in smem: no L2 round trip per segment
     double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, acc3 = 0.0;
     if (lane < 30) {
       int k = kb + grp;
@@ -472,6 +472,7 @@ struct PcgSmem {
   double* zc;   // [maxdist*6] z cache (distinct columns of the CTA's rows)
   int* lc;      // [maxblk] local column index of each of the CTA's blocks
   int2* rs;     // [maxrows] (first segment, count) of each of the CTA's rows
+  int* rp;      // [maxrows+1] row_ptr of the CTA's rows
 };
 
 // z_i = D_i^-1 r_i (+ P_i e) for lanes 0..5 of the warp owning local row i
@@ -627,6 +628,7 @@ __global__ void __launch_bounds__(kPcgMaxThreads, 1) k_pcg3(Pcg3Args a) {
   m.zc = m.Ssm + 36 * a.resblocks;
   m.lc = reinterpret_cast<int*>(m.zc + 6 * a.maxdist);
   m.rs = reinterpret_cast<int2*>(m.lc + ((a.maxblk + 1) & ~1));
+  m.rp = reinterpret_cast<int*>(m.rs + a.maxrows);
   __shared__ double2 red[32];
   __shared__ double tmp[16];
   __shared__ double e[6];
@@ -679,6 +681,8 @@ __global__ void __launch_bounds__(kPcgMaxThreads, 1) k_pcg3(Pcg3Args a) {
   }
   for (int t = threadIdx.x; t < nblk; t += kPcgThreads) m.lc[t] = __ldg(a.lcol + kc0 + t);
   for (int t = threadIdx.x; t < nrows; t += kPcgThreads) m.rs[t] = a.rowseg[row0 + t];
+  for (int t = threadIdx.x; t <= nrows; t += kPcgThreads) m.rp[t] = __ldg(a.row_ptr + row0 + t);
+  const int* rpl = m.rp - row0;  // rpl[r] = row_ptr[r] for the CTA's rows
   // resident S blocks: the head of every warp's chunk (18 double2 per block)
   for (int w = 0; w < kPcgWarps; ++w) {
     const int4 ch = a.wchunk[blockIdx.x * kPcgWarps + w];
@@ -710,7 +714,7 @@ __global__ void __launch_bounds__(kPcgMaxThreads, 1) k_pcg3(Pcg3Args a) {
     grid.sync();
     fill_zc(0);
     __syncthreads();
-    spmv_segments(a, m.zc, m.lc, kc0, m.seg, m.Ssm);
+    spmv_segments(a, m.zc, m.lc, kc0, m.seg, m.Ssm, rpl);
     __syncthreads();
     double xb = 0.0, xw = 0.0;
     for (int i = warp; i < nrows; i += kPcgWarps)
@@ -780,7 +784,7 @@ __global__ void __launch_bounds__(kPcgMaxThreads, 1) k_pcg3(Pcg3Args a) {
     PH_INIT();
     for (it = 0; it < a.max_it;) {
       // ---- phase 1: w = S z; p = z + beta p; q = w + beta q; P^T q --------
-      spmv_segments(a, m.zc, m.lc, kc0, m.seg, m.Ssm);
+      spmv_segments(a, m.zc, m.lc, kc0, m.seg, m.Ssm, rpl);
       __syncthreads();
       PH(0);
       double pq_l = 0.0;
@@ -992,7 +996,7 @@ void TwoLevelPcg::set_pattern(const int* row_ptr, const int* col, int nnzb, cuda
   SFM_CUDA(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
   const size_t per_cta_avail = (size_t)max_smem / per_sm - 2048;  // static smem margin
   const size_t zbytes = sizeof(double) * 6 * (size_t)maxdist_ + sizeof(int) * (size_t)(maxblk_ + 1) +
-                        sizeof(int2) * maxrows_ + 16;
+                        sizeof(int2) * maxrows_ + sizeof(int) * (maxrows_ + 1) + 16;
   SFM_REQUIRE(smem_ + zbytes <= per_cta_avail, "PCG z cache does not fit in shared memory");
   // Measured on config 3: keeping S blocks resident costs the L1 capacity
   // the rest of the loop relies on and is slower (20.5 vs 18.2 us/iteration),
@@ -1017,7 +1021,8 @@ void TwoLevelPcg::set_pattern(const int* row_ptr, const int* col, int nnzb, cuda
   }
   resblocks_ = maxres;
   smem_ += sizeof(double) * 36 * (size_t)maxres;
-  smem_ += sizeof(double) * 6 * (size_t)maxdist_ + sizeof(int) * (size_t)(maxblk_ + 1) + sizeof(int2) * maxrows_ + 16;
+  smem_ += sizeof(double) * 6 * (size_t)maxdist_ + sizeof(int) * (size_t)(maxblk_ + 1) + sizeof(int2) * maxrows_ +
+           sizeof(int) * (maxrows_ + 1) + 16;
   SFM_CUDA(cudaFuncSetAttribute(k_pcg3, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_));
   int resident = 0;
   SFM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&resident, k_pcg3, nt_, smem_));
