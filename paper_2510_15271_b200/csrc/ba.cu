@@ -1284,6 +1284,15 @@ struct SetupTimer {
 };
 }  // namespace
 
+BASolver::~BASolver() {
+  if (side_) {
+    cudaStreamSynchronize(side_);
+    cudaStreamDestroy(side_);
+  }
+  if (side_ready_) cudaEventDestroy(side_ready_);
+  if (side_done_) cudaEventDestroy(side_done_);
+}
+
 void BASolver::setup(const sfm_ba_problem& pr, const sfm_ba_options& opt) {
   opt_ = opt;
   rank_ = comm_ ? comm_->rank : 0;
@@ -1318,16 +1327,46 @@ void BASolver::setup(const sfm_ba_problem& pr, const sfm_ba_options& opt) {
   free_idx_.upload(free_idx.data(), F_, s);
   free_frame_.upload(free_frame.data(), nfree_, s);
   for (int k = 0; k < 2; ++k) {
-    q_[k].upload(pr.cam_q, (size_t)F_ * 4, s);
-    t_[k].upload(pr.cam_t, (size_t)F_ * 3, s);
+    if (k == 0) {
+      q_[0].upload(pr.cam_q, (size_t)F_ * 4, s);
+      t_[0].upload(pr.cam_t, (size_t)F_ * 3, s);
+    } else {  // the second state buffer starts as a device copy of the first
+      q_[1].resize((size_t)F_ * 4);
+      t_[1].resize((size_t)F_ * 3);
+      if (F_) {
+        SFM_CUDA(cudaMemcpyAsync(q_[1].get(), q_[0].get(), sizeof(double) * 4 * F_, cudaMemcpyDeviceToDevice, s));
+        SFM_CUDA(cudaMemcpyAsync(t_[1].get(), t_[0].get(), sizeof(double) * 3 * F_, cudaMemcpyDeviceToDevice, s));
+      }
+    }
     Rt_[k].resize((size_t)F_ * 12);
     if (F_) { k_frames_rt<<<grid_for(F_, 128), 128, 0, s>>>(F_, q_[k].get(), t_[k].get(), Rt_[k].get()); SFM_CHECK_LAUNCH(); }
-    X_[k].upload(pr.points, (size_t)P_ * 3, s);
   }
   cur_ = 0;
+  // The points and pixels (~2/3 of the input bytes) are not read until the
+  // camera-major streams: they go over a side stream while the index
+  // arrays arrive and the pair list / S pattern are built.
+  if (!side_) {
+    SFM_CUDA(cudaStreamCreateWithFlags(&side_, cudaStreamNonBlocking));
+    SFM_CUDA(cudaEventCreateWithFlags(&side_ready_, cudaEventDisableTiming));
+    SFM_CUDA(cudaEventCreateWithFlags(&side_done_, cudaEventDisableTiming));
+  }
+  struct SideJoin {  // no early exit leaves a copy in flight into freed buffers
+    cudaStream_t st;
+    ~SideJoin() { cudaStreamSynchronize(st); }
+  } side_join{side_};
+  X_[0].resize((size_t)P_ * 3);
+  X_[1].resize((size_t)P_ * 3);
+  obs_uv_.resize((size_t)N_ * 2);
+  SFM_CUDA(cudaEventRecord(side_ready_, s));
+  SFM_CUDA(cudaStreamWaitEvent(side_, side_ready_, 0));
+  if (P_) {
+    SFM_CUDA(cudaMemcpyAsync(X_[0].get(), pr.points, sizeof(double) * 3 * P_, cudaMemcpyDefault, side_));
+    SFM_CUDA(cudaMemcpyAsync(X_[1].get(), X_[0].get(), sizeof(double) * 3 * P_, cudaMemcpyDeviceToDevice, side_));
+  }
+  if (N_) SFM_CUDA(cudaMemcpyAsync(obs_uv_.get(), pr.obs_uv, sizeof(double) * 2 * N_, cudaMemcpyDefault, side_));
+  SFM_CUDA(cudaEventRecord(side_done_, side_));
   obs_frame_.upload(pr.obs_frame, N_, s);
   obs_point_.upload(pr.obs_point, N_, s);
-  obs_uv_.upload(pr.obs_uv, (size_t)N_ * 2, s);
   geo_.resize(N_);
   sc_.resize(1);
   SFM_CUDA(cudaMemsetAsync(sc_.get(), 0, sizeof(BAScalars), s));
@@ -1545,6 +1584,7 @@ void BASolver::setup(const sfm_ba_problem& pr, const sfm_ba_options& opt) {
     }
     n_cm_ = cptr[nfree_];
     cm_ptr_.upload(cptr.data(), cptr.size(), s);
+    SFM_CUDA(cudaStreamWaitEvent(s, side_done_, 0));  // pixels + points resident from here on
     cm_obs_.resize(n_cm_);
     cm_pt_.resize(n_cm_);
     cm_uv_.resize((size_t)n_cm_ * 2);
@@ -1601,6 +1641,7 @@ void BASolver::setup(const sfm_ba_problem& pr, const sfm_ba_options& opt) {
     term_ptr_.upload(tp.data(), tp.size(), s);
     term_list_.upload(tl.data(), tl.size(), s);
   }
+  tm.mark("pose-term lists");
   edge_meas_inv_.resize((size_t)n_edges_ * 7);
   prior_init_inv_.resize((size_t)n_priors_ * 7);
   edge_H_.resize((size_t)n_edges_ * 36);
@@ -1639,6 +1680,7 @@ void BASolver::setup(const sfm_ba_problem& pr, const sfm_ba_options& opt) {
   }
   if (!use_dense_ && nfree_ > 0) {
     const int cl = opt_.coarse_cluster == 0 ? 8 : opt_.coarse_cluster;
+    tm.mark("buffers");
     pcg_.setup(nfree_, cl, opt_.coarse_refresh > 0 ? opt_.coarse_refresh : 8, s);
     pcg_.set_pattern(row_ptr_.get(), col_idx_.get(), n_full_, s);
   }

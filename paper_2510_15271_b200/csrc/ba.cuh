@@ -39,6 +39,9 @@ struct BAScalars {
 class BASolver {
  public:
   BASolver(cudaStream_t s, Profiler* p, Comm* c) : stream_(s), prof_(p), comm_(c) {}
+  ~BASolver();
+  BASolver(const BASolver&) = delete;
+  BASolver& operator=(const BASolver&) = delete;
   void setup(const sfm_ba_problem& prob, const sfm_ba_options& opt);
   // Runs up to n LM iterations continuing the current solve.
   void iterate(int n, sfm_ba_report* rep);
@@ -60,6 +63,8 @@ class BASolver {
   BlkArgs blk_args(double lam) const;
 
   cudaStream_t stream_;
+  cudaStream_t side_ = nullptr;          // setup: bulk H2D copies overlapped with the structure build
+  cudaEvent_t side_ready_ = nullptr, side_done_ = nullptr;
   Profiler* prof_;
   Comm* comm_;
   sfm_ba_options opt_{};

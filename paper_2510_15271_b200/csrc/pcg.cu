@@ -3,6 +3,8 @@
 #include <cooperative_groups.h>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
 #include <array>
 #include <cstdlib>
 #include <vector>
@@ -874,6 +876,16 @@ void TwoLevelPcg::setup(int nf, int cluster, int refresh, cudaStream_t s) {
 
 void TwoLevelPcg::set_pattern(const int* row_ptr, const int* col, int nnzb, cudaStream_t s) {
   if (nf_ <= 0) return;
+  const bool timing = std::getenv("SFM_TIMING") != nullptr;
+  auto tp = std::chrono::steady_clock::now();
+  auto mark = [&](const char* what) {
+    if (!timing) return;
+    cudaStreamSynchronize(s);
+    const auto t1 = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[sfm pcg plan] %-24s %8.3f ms\n", what,
+                 std::chrono::duration<double, std::milli>(t1 - tp).count());
+    tp = t1;
+  };
   std::vector<int> rp(nf_ + 1), cl(nnzb);
   SFM_CUDA(cudaMemcpyAsync(rp.data(), row_ptr, sizeof(int) * (nf_ + 1), cudaMemcpyDeviceToHost, s));
   SFM_CUDA(cudaMemcpyAsync(cl.data(), col, sizeof(int) * nnzb, cudaMemcpyDeviceToHost, s));
@@ -881,6 +893,7 @@ void TwoLevelPcg::set_pattern(const int* row_ptr, const int* col, int nnzb, cuda
   int dev = 0, nsm = 0;
   SFM_CUDA(cudaGetDevice(&dev));
   SFM_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+  mark("download pattern");
 
   // ---- CTA row ranges balanced by (stored blocks + per-row overhead) -------
   const int64_t kRowCost = 4;
@@ -925,6 +938,7 @@ void TwoLevelPcg::set_pattern(const int* row_ptr, const int* col, int nnzb, cuda
     row0.push_back(nf_);
     break;
   }
+  mark("partition");
   // ---- per-warp chunks and segments ----------------------------------------
   std::vector<int4> wchunk((size_t)G * nwarps);
   std::vector<int2> rowseg(nf_);
@@ -953,26 +967,37 @@ void TwoLevelPcg::set_pattern(const int* row_ptr, const int* col, int nnzb, cuda
     }
     maxsegs = std::max(maxsegs, sidx);
   }
+  mark("chunks");
   // ---- per-CTA z cache: distinct columns and the local index of each block --
   std::vector<int> zl_ptr(G + 1, 0), zl, lcol(nnzb);
   maxdist_ = 1;
   maxblk_ = 1;
   {
-    std::vector<int> mark(nf_, -1);
+    // distinct columns ascending: flag pass + ordered sweep when the CTA
+    // touches a large share of the columns, sort of the few otherwise;
+    // local index through a dense position map (no per-block search)
+    std::vector<int> mark(nf_, -1), pos(nf_, 0);
+    std::vector<int> d;
     for (int c = 0; c < G; ++c) {
       const int k0 = rp[row0[c]], k1 = rp[row0[c + 1]];
-      std::vector<int> d;
+      d.clear();
       for (int k = k0; k < k1; ++k)
         if (mark[cl[k]] != c) { mark[cl[k]] = c; d.push_back(cl[k]); }
-      std::sort(d.begin(), d.end());
-      for (size_t i = 0; i < d.size(); ++i) mark[d[i]] = c, zl.push_back(d[i]);
-      for (int k = k0; k < k1; ++k)
-        lcol[k] = (int)(std::lower_bound(d.begin(), d.end(), cl[k]) - d.begin());
+      if ((int64_t)d.size() * 16 > nf_) {
+        d.clear();
+        for (int j = 0; j < nf_; ++j)
+          if (mark[j] == c) d.push_back(j);
+      } else {
+        std::sort(d.begin(), d.end());
+      }
+      for (size_t i = 0; i < d.size(); ++i) pos[d[i]] = (int)i, zl.push_back(d[i]);
+      for (int k = k0; k < k1; ++k) lcol[k] = pos[cl[k]];
       zl_ptr[c + 1] = (int)zl.size();
       maxdist_ = std::max(maxdist_, (int)d.size());
       maxblk_ = std::max(maxblk_, k1 - k0);
     }
   }
+  mark("z cache");
   // ---- coarse clusters = groups of consecutive CTAs -------------------------
   const bool two = cluster_ > 0;
   nc_ = two ? std::min(G, std::max(1, (nf_ + cluster_ - 1) / cluster_)) : 1;
@@ -1027,6 +1052,7 @@ void TwoLevelPcg::set_pattern(const int* row_ptr, const int* col, int nnzb, cuda
   int resident = 0;
   SFM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&resident, k_pcg3, nt_, smem_));
   SFM_REQUIRE(resident > 0 && G <= resident * nsm, "PCG grid cannot be made co-resident");
+  mark("smem plan + occupancy");
   cta_row0_.upload(row0.data(), row0.size(), s);
   wchunk_.upload(wchunk.data(), wchunk.size(), s);
   wres_.upload(wres.data(), wres.size(), s);
@@ -1037,6 +1063,7 @@ void TwoLevelPcg::set_pattern(const int* row_ptr, const int* col, int nnzb, cuda
   cta_cluster_.upload(cta_cluster.data(), cta_cluster.size(), s);
   cluster_cta0_.upload(cluster_cta0.data(), cluster_cta0.size(), s);
 
+  mark("uploads");
   Minv_.resize((size_t)nf_ * 36);
   Pm_.resize((size_t)nf_ * 36);
   r_.resize((size_t)nf_ * 6); z_.resize((size_t)nf_ * 6); p_.resize((size_t)nf_ * 6); q_.resize((size_t)nf_ * 6);
@@ -1065,9 +1092,14 @@ void TwoLevelPcg::set_pattern(const int* row_ptr, const int* col, int nnzb, cuda
         k = k1;
       }
     }
-    std::stable_sort(rr.begin(), rr.end(), [](const std::array<int, 4>& x, const std::array<int, 4>& y) {
-      return x[0] < y[0];
-    });
+    {  // stable counting sort by coarse pair key (keys < nc^2)
+      std::vector<int> cnt((size_t)nc_ * nc_ + 1, 0);
+      for (const auto& e : rr) ++cnt[e[0] + 1];
+      for (size_t k = 1; k < cnt.size(); ++k) cnt[k] += cnt[k - 1];
+      std::vector<std::array<int, 4>> sorted(rr.size());
+      for (const auto& e : rr) sorted[cnt[e[0]]++] = e;
+      rr.swap(sorted);
+    }
     std::vector<int2> cd;
     std::vector<int> ptr(1, 0);
     std::vector<int4> runs;
@@ -1081,6 +1113,7 @@ void TwoLevelPcg::set_pattern(const int* row_ptr, const int* col, int nnzb, cuda
     }
     if (!rr.empty()) ptr.push_back((int)runs.size());
     npairs_ = (int)cd.size();
+    mark("coarse runs");
     pair_cd_.upload(cd.data(), cd.size(), s);
     pair_ptr_.upload(ptr.data(), ptr.size(), s);
     runs_.upload(runs.data(), runs.size(), s);
@@ -1091,6 +1124,7 @@ void TwoLevelPcg::set_pattern(const int* row_ptr, const int* col, int nnzb, cuda
     npairs_ = 0;
   }
   SFM_CUDA(cudaStreamSynchronize(s));
+  mark("coarse uploads");
 }
 
 void TwoLevelPcg::set_basis(const int* free_frame, const double* q, const double* t, const double* Rt,

@@ -8,8 +8,11 @@ from paper_2510_15271_b200.scenes import config_scene, scene_arrays
 from paper_2510_15271_b200.mapping import DeviceBA, solve_arrays
 from paper_2510_15271_b200.solver import DeviceOptions, RobustLoss, SolverOptions
 a = scene_arrays(config_scene(int(sys.argv[1]) if len(sys.argv) > 1 else 3, seed=0))
+import dataclasses, torch
+a = dataclasses.replace(a, **{f.name: torch.from_numpy(getattr(a, f.name)).pin_memory().numpy()
+                              for f in dataclasses.fields(a) if isinstance(getattr(a, f.name), np.ndarray)})
 loss = RobustLoss("huber", 2.0)
-dopt = DeviceOptions(linear_solver="pcg", pcg_rtol=1e-10, pcg_max_iters=500)
+dopt = DeviceOptions(linear_solver="pcg", pcg_rtol=1e-8, pcg_max_iters=500)
 for rep in range(2):
     t0 = time.perf_counter(); ba = DeviceBA(a, loss, SolverOptions(max_iters=10), dopt)
     t1 = time.perf_counter(); r = ba.iterate(10)
