@@ -165,10 +165,12 @@ __global__ void k_pad_identity(int first, int npad, double* Ac) {
 // Blocked Gauss-Jordan inversion of the SPD coarse matrix (no pivoting).
 // Ping-pongs between two buffers so each block step reads one and writes
 // the other: one grid barrier per step.  Result in buf[T & 1].  256
-// threads as 16x16, each owning a 3x3 patch of a 48x48 tile: the pivot
-// tile is inverted in registers (one barrier per column, double-buffered
-// pivot row/column in smem) and the tile updates are register-blocked
-// 48x48x48 products.
+// threads as 16x16, each owning a 3x3 patch of a 48x48 tile; the tile
+// updates are register-blocked 48x48x48 products.  The 48x48 pivot inverse
+// of step K+1 is computed once, by the CTA that writes tile (K+1, K+1) in
+// step K (it does that tile first and inverts it in registers while the
+// other CTAs finish their tiles), and handed over through `pivg` -- the
+// sequential 48-column elimination runs in one CTA per step, not in all.
 __device__ __forceinline__ void tile_mm(const double* __restrict__ A, const double* __restrict__ B, int ty,
                                         int tx, double acc[3][3]) {
 #pragma unroll 4
@@ -181,7 +183,83 @@ __device__ __forceinline__ void tile_mm(const double* __restrict__ A, const doub
   }
 }
 
-__global__ void __launch_bounds__(kGJThreads) k_gj_inverse(double* A0, double* A1, int n, BAScalars* sc) {
+// In-register Gauss-Jordan inverse of the CTA's 48x48 tile P (thread
+// (ty, tx) holds rows 3ty.., columns 3tx..); one barrier per column, the
+// pivot row / column double-buffered in smem.  Writes the inverse to g.
+__device__ __forceinline__ void gj_invert_tile(double P[3][3], double* cbuf, double* rbuf, int* bad, double* g) {
+  const int tid = threadIdx.x, ty = tid >> 4, tx = tid & 15;
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+    if (tx == 0) cbuf[ty * 3 + a] = P[a][0];
+#pragma unroll
+  for (int b = 0; b < 3; ++b)
+    if (ty == 0) rbuf[tx * 3 + b] = P[0][b];
+  __syncthreads();
+  for (int k = 0; k < kNB; ++k) {
+    const double* ck = cbuf + (k & 1) * kNB;
+    const double* rk = rbuf + (k & 1) * kNB;
+    const double pk = ck[k];
+    if (tid == 0 && !(pk > 0.0)) *bad = 1;
+    const double ip = 1.0 / pk;
+    // branch-free update (selects, not divergent branches: this loop is the
+    // inversion's sequential critical path)
+    double rj[3];
+#pragma unroll
+    for (int b = 0; b < 3; ++b) rj[b] = rk[tx * 3 + b] * ip;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      const int i = ty * 3 + a;
+      const double ci = ck[i];
+      const double cip = -ci * ip;
+#pragma unroll
+      for (int b = 0; b < 3; ++b) {
+        const int j = tx * 3 + b;
+        const double gen = fma(-ci, rj[b], P[a][b]);
+        const double rowk = (j == k) ? ip : rj[b];
+        const double other = (j == k) ? cip : gen;
+        P[a][b] = (i == k) ? rowk : other;
+      }
+    }
+    if (k + 1 < kNB) {
+      double* cn = cbuf + ((k + 1) & 1) * kNB;
+      double* rn = rbuf + ((k + 1) & 1) * kNB;
+      const int kk = k + 1;
+      const int km = kk % 3;
+      if (tx == kk / 3) {
+#pragma unroll
+        for (int a = 0; a < 3; ++a) cn[ty * 3 + a] = km == 0 ? P[a][0] : (km == 1 ? P[a][1] : P[a][2]);
+      }
+      if (ty == kk / 3) {
+#pragma unroll
+        for (int b = 0; b < 3; ++b) rn[tx * 3 + b] = km == 0 ? P[0][b] : (km == 1 ? P[1][b] : P[2][b]);
+      }
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+#pragma unroll
+    for (int b = 0; b < 3; ++b) g[(ty * 3 + a) * kNB + tx * 3 + b] = P[a][b];
+}
+
+// 48x48 tile (row stride n) -> shared memory: all nine loads per thread in
+// flight before the first store (the generic-pointer stores would otherwise
+// order each load behind the previous store).
+__device__ __forceinline__ void load_tile(const double* src, int64_t n, double* dst) {
+  constexpr int kPer = kNB * kNB / kGJThreads;
+  static_assert(kPer * kGJThreads == kNB * kNB, "tile / CTA size");
+  double v[kPer];
+#pragma unroll
+  for (int q = 0; q < kPer; ++q) {
+    const int e = threadIdx.x + q * kGJThreads;
+    v[q] = __ldcg(src + (e / kNB) * n + e % kNB);
+  }
+#pragma unroll
+  for (int q = 0; q < kPer; ++q) dst[threadIdx.x + q * kGJThreads] = v[q];
+}
+
+__global__ void __launch_bounds__(kGJThreads) k_gj_inverse(double* A0, double* A1, int n, double* pivg,
+                                                          BAScalars* sc) {
   cg::grid_group grid = cg::this_grid();
   extern __shared__ double gsm[];
   double* piv = gsm;                      // 48x48 (inverted pivot tile)
@@ -194,61 +272,39 @@ __global__ void __launch_bounds__(kGJThreads) k_gj_inverse(double* A0, double* A
   const int T = n / kNB;
   const int tid = threadIdx.x, ty = tid >> 4, tx = tid & 15;
   if (tid == 0) bad = 0;
-  for (int K = 0; K < T; ++K) {
-    const double* src = (K & 1) ? A1 : A0;
-    double* dst = (K & 1) ? A0 : A1;
-    const double* pk_tile = src + (int64_t)(K * kNB) * n + K * kNB;
+  __syncthreads();
+  if (blockIdx.x == 0) {  // pivot 0 straight from the input
     double P[3][3];
 #pragma unroll
     for (int a = 0; a < 3; ++a)
 #pragma unroll
-      for (int b = 0; b < 3; ++b) P[a][b] = __ldcg(pk_tile + (int64_t)(ty * 3 + a) * n + tx * 3 + b);
-#pragma unroll
-    for (int a = 0; a < 3; ++a)
-      if (tx == 0) cbuf[ty * 3 + a] = P[a][0];
-#pragma unroll
-    for (int b = 0; b < 3; ++b)
-      if (ty == 0) rbuf[tx * 3 + b] = P[0][b];
+      for (int b = 0; b < 3; ++b) P[a][b] = __ldcg(A0 + (int64_t)(ty * 3 + a) * n + tx * 3 + b);
+    gj_invert_tile(P, cbuf, rbuf, &bad, pivg);
+  }
+  grid.sync();
+#ifdef SFM_GJ_PHASES
+  long long gt[6] = {0, 0, 0, 0, 0, 0}, g0 = clock64();
+#define GJP(k) do { const long long t_ = clock64(); gt[k] += t_ - g0; g0 = t_; } while (0)
+#else
+#define GJP(k) do {} while (0)
+#endif
+  for (int K = 0; K < T; ++K) {
+    const double* src = (K & 1) ? A1 : A0;
+    double* dst = (K & 1) ? A0 : A1;
+    const double* pg = pivg + (K & 1) * kNB * kNB;
+    double* pg_next = pivg + ((K + 1) & 1) * kNB * kNB;
+    load_tile(pg, kNB, piv);
     __syncthreads();
-    for (int k = 0; k < kNB; ++k) {
-      const double* ck = cbuf + (k & 1) * kNB;
-      const double* rk = rbuf + (k & 1) * kNB;
-      const double pk = ck[k];
-      if (tid == 0 && !(pk > 0.0)) bad = 1;
-      const double ip = 1.0 / pk;
-#pragma unroll
-      for (int a = 0; a < 3; ++a) {
-        const int i = ty * 3 + a;
-        const double ci = ck[i];
-#pragma unroll
-        for (int b = 0; b < 3; ++b) {
-          const int j = tx * 3 + b;
-          if (i == k) P[a][b] = (j == k) ? ip : rk[j] * ip;
-          else P[a][b] = (j == k) ? -ci * ip : P[a][b] - ci * rk[j] * ip;
-        }
-      }
-      if (k + 1 < kNB) {
-        double* cn = cbuf + ((k + 1) & 1) * kNB;
-        double* rn = rbuf + ((k + 1) & 1) * kNB;
-        const int kk = k + 1;
-        const int km = kk % 3;
-        if (tx == kk / 3) {
-#pragma unroll
-          for (int a = 0; a < 3; ++a) cn[ty * 3 + a] = km == 0 ? P[a][0] : (km == 1 ? P[a][1] : P[a][2]);
-        }
-        if (ty == kk / 3) {
-#pragma unroll
-          for (int b = 0; b < 3; ++b) rn[tx * 3 + b] = km == 0 ? P[0][b] : (km == 1 ? P[1][b] : P[2][b]);
-        }
-      }
-      __syncthreads();
-    }
-#pragma unroll
-    for (int a = 0; a < 3; ++a)
-#pragma unroll
-      for (int b = 0; b < 3; ++b) piv[(ty * 3 + a) * kNB + tx * 3 + b] = P[a][b];
-    __syncthreads();
-    for (int tile = blockIdx.x; tile < T * T; tile += gridDim.x) {
+    GJP(0);
+    // tile (K+1, K+1) first: its owner inverts it for the next step
+    const int nt = T * T;
+    const int next_diag = K + 1 < T ? (K + 1) * T + (K + 1) : -1;
+    const int owner = next_diag >= 0 ? next_diag % (int)gridDim.x : -1;
+    const int G = (int)gridDim.x, bx = (int)blockIdx.x;
+    for (int it = bx - (owner == bx ? G : 0); it < nt; it += G) {
+      const bool first = it < 0;
+      const int tile = first ? next_diag : it;
+      if (!first && tile == next_diag) continue;  // done first
       const int I = tile / T, J = tile % T;
       double* out = dst;
       if (I == K && J == K) {
@@ -256,13 +312,12 @@ __global__ void __launch_bounds__(kGJThreads) k_gj_inverse(double* A0, double* A
         for (int a = 0; a < 3; ++a)
 #pragma unroll
           for (int b = 0; b < 3; ++b)
-            out[(int64_t)(K * kNB + ty * 3 + a) * n + K * kNB + tx * 3 + b] = P[a][b];
+            out[(int64_t)(K * kNB + ty * 3 + a) * n + K * kNB + tx * 3 + b] = piv[(ty * 3 + a) * kNB + tx * 3 + b];
         continue;
       }
       double acc[3][3];
       if (I == K || J != K) {  // tM = KKinv * src_KJ
-        for (int e = tid; e < kNB * kNB; e += kGJThreads)
-          tKJ[e] = __ldcg(src + (int64_t)(K * kNB + e / kNB) * n + J * kNB + e % kNB);
+        load_tile(src + (int64_t)(K * kNB) * n + J * kNB, n, tKJ);
         __syncthreads();
 #pragma unroll
         for (int a = 0; a < 3; ++a)
@@ -283,8 +338,15 @@ __global__ void __launch_bounds__(kGJThreads) k_gj_inverse(double* A0, double* A
 #pragma unroll
           for (int b = 0; b < 3; ++b) tM[(ty * 3 + a) * kNB + tx * 3 + b] = acc[a][b];
       }
-      for (int e = tid; e < kNB * kNB; e += kGJThreads)
-        tIK[e] = __ldcg(src + (int64_t)(I * kNB + e / kNB) * n + K * kNB + e % kNB);
+      load_tile(src + (int64_t)(I * kNB) * n + K * kNB, n, tIK);
+      double old_ij[3][3];
+      if (J != K) {
+#pragma unroll
+        for (int a = 0; a < 3; ++a)
+#pragma unroll
+          for (int b = 0; b < 3; ++b)
+            old_ij[a][b] = __ldcg(src + (int64_t)(I * kNB + ty * 3 + a) * n + J * kNB + tx * 3 + b);
+      }
       __syncthreads();
 #pragma unroll
       for (int a = 0; a < 3; ++a)
@@ -304,13 +366,27 @@ __global__ void __launch_bounds__(kGJThreads) k_gj_inverse(double* A0, double* A
 #pragma unroll
           for (int b = 0; b < 3; ++b) {
             const int64_t g = (int64_t)(I * kNB + ty * 3 + a) * n + J * kNB + tx * 3 + b;
-            out[g] = __ldcg(src + g) - acc[a][b];
+            acc[a][b] = old_ij[a][b] - acc[a][b];
+            out[g] = acc[a][b];
           }
+        GJP(1);
+        if (first) {  // the next step's pivot tile: invert it now
+          __syncthreads();
+          gj_invert_tile(acc, cbuf, rbuf, &bad, pg_next);
+          GJP(2);
+        }
       }
       __syncthreads();
     }
+    GJP(3);
     grid.sync();
+    GJP(4);
   }
+#ifdef SFM_GJ_PHASES
+  if (tid == 0 && (blockIdx.x < 2 || blockIdx.x == 100))
+    printf("GJ cta %d T=%d piv=%lld tiles=%lld inv=%lld tail=%lld sync=%lld\n", blockIdx.x, T, gt[0] / T, gt[1] / T,
+           gt[2] / T, gt[3] / T, gt[4] / T);
+#endif
   if (bad && tid == 0) atomicOr(&sc->nonfinite, 1);
 }
 
@@ -1072,6 +1148,7 @@ void TwoLevelPcg::set_pattern(const int* row_ptr, const int* col, int nnzb, cuda
   if (two) {
     Ac_[0].resize((size_t)npad_ * npad_);
     Ac_[1].resize((size_t)npad_ * npad_);
+    gjpiv_.resize((size_t)2 * kNB * kNB);
     const size_t gsm = sizeof(double) * (4 * kNB * kNB + 4 * kNB);
     SFM_CUDA(cudaFuncSetAttribute(k_gj_inverse, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gsm));
     int per = 0;
@@ -1161,8 +1238,9 @@ void TwoLevelPcg::solve(const PcgProblem& p, int max_it, double rtol, BAScalars*
     }
     double* A0 = Ac_[0].get();
     double* A1 = Ac_[1].get();
+    double* pg = gjpiv_.get();
     int n = npad_;
-    void* args[] = {&A0, &A1, &n, &sc};
+    void* args[] = {&A0, &A1, &n, &pg, &sc};
     const size_t gsm = sizeof(double) * (4 * kNB * kNB + 4 * kNB);
     {
       ProfScope ps(*prof, "coarse_inverse", 0.0, s);

@@ -51,7 +51,7 @@ class TwoLevelPcg {
   bool coarse_valid_ = false;
   bool have_prev_ = false, warm_ = true;  // warm start from the previous solution
   const double* Aci_ = nullptr;
-  DevBuf<double> Minv_, Pm_, Ac_[2], r_, z_, p_, q_, rpart_, part_;
+  DevBuf<double> Minv_, Pm_, Ac_[2], gjpiv_, r_, z_, p_, q_, rpart_, part_;
   DevBuf<int2> pair_cd_, rowseg_, wres_;
   DevBuf<int> pair_ptr_, cta_row0_, cta_cluster_, cluster_cta0_, zl_ptr_, zl_, lcol_;
   DevBuf<int4> runs_, wchunk_;
