@@ -552,17 +552,33 @@ __global__ void k_finalize(const double* __restrict__ pa, int na, const double* 
                            int nd, BAScalars* sc, int mode) {
   __shared__ double red[8];
   double a = 0.0, b = 0.0, c = 0.0;
-  for (int i = threadIdx.x; i < na; i += blockDim.x) a += pa[i];
-  for (int i = threadIdx.x; i < nc; i += blockDim.x) c += pc[i];
+  // eight partial loads in flight per thread, then the additions in the
+  // same (ascending) order as a plain strided loop
+  auto strided_sum = [](const double* __restrict__ p, int n) {
+    double acc = 0.0;
+    for (int i0 = threadIdx.x; i0 < n; i0 += 8 * blockDim.x) {
+      double v[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int i = i0 + q * (int)blockDim.x;
+        v[q] = i < n ? __ldg(p + i) : 0.0;
+      }
+#pragma unroll
+      for (int q = 0; q < 8; ++q) acc += v[q];
+    }
+    return acc;
+  };
+  a = strided_sum(pa, na);
+  c = strided_sum(pc, nc);
   double sa = block_sum<256>(a, red);
   double sc_ = block_sum<256>(c, red);
   if (mode == 1) {
-    for (int i = threadIdx.x; i < nb; i += blockDim.x) b += pb[i];
+    b = strided_sum(pb, nb);
   }
   double sb = block_sum<256>(b, red);
   double d = 0.0;
   if (mode == 1)
-    for (int i = threadIdx.x; i < nd; i += blockDim.x) d += pd[i];
+    d = strided_sum(pd, nd);
   double sd = block_sum<256>(d, red);
   if (threadIdx.x == 0) {
     sc->cost = sa + sc_;
@@ -965,37 +981,87 @@ struct CamArgs {
   double* gc;
 };
 
+// Pose terms, one thread per edge / prior: each term is evaluated once and
+// its normal-equation contributions J^T J | J^T r (42 doubles per side)
+// written to `contrib` (edge e side 0/1 at 2e / 2e+1, prior a at 2E + a);
+// an edge between two free cameras also writes its off-diagonal block
+// (the lower camera's J^T times the upper camera's J) to H.
+__global__ void k_terms_lin(int E, int A, const int* __restrict__ ab, const int* __restrict__ pf,
+                            const int* __restrict__ free_idx, const double* __restrict__ meas_inv,
+                            const double* __restrict__ init_inv, double we, double wa, const double* q,
+                            const double* t, const double* Rt, double* __restrict__ contrib,
+                            double* __restrict__ H) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= E + A) return;
+  double r[6];
+  auto emit = [&](const double* J, double* out) {
+#pragma unroll
+    for (int rr = 0; rr < 6; ++rr) {
+#pragma unroll
+      for (int cc = 0; cc < 6; ++cc) {
+        double s = 0.0;
+#pragma unroll
+        for (int m = 0; m < 6; ++m) s += J[m * 6 + rr] * J[m * 6 + cc];
+        out[rr * 6 + cc] = s;
+      }
+      double s = 0.0;
+#pragma unroll
+      for (int m = 0; m < 6; ++m) s += J[m * 6 + rr] * r[m];
+      out[36 + rr] = s;
+    }
+  };
+  if (i < E) {
+    const int fa = ab[2 * i], fb = ab[2 * i + 1];
+    const int ja = free_idx[fa], jb = free_idx[fb];
+    Pose Ta = load_pose(q, t, Rt, fa), Tb = load_pose(q, t, Rt, fb);
+    double Ja[36], Jb[36];
+    edge_eval(meas_inv + i * 7, Ta, Tb, we, r, Ja, Jb);
+    if (ja >= 0) emit(Ja, contrib + (int64_t)(2 * i) * 42);
+    if (jb >= 0) emit(Jb, contrib + (int64_t)(2 * i + 1) * 42);
+    if (ja >= 0 && jb >= 0 && ja != jb) {
+      const double* L = ja < jb ? Ja : Jb;
+      const double* Rr = ja < jb ? Jb : Ja;
+      for (int rr = 0; rr < 6; ++rr)
+        for (int cc = 0; cc < 6; ++cc) {
+          double s = 0.0;
+          for (int m = 0; m < 6; ++m) s += L[m * 6 + rr] * Rr[m * 6 + cc];
+          H[(int64_t)i * 36 + rr * 6 + cc] = s;
+        }
+    }
+  } else {
+    const int pi = i - E;
+    if (free_idx[pf[pi]] < 0) return;
+    Pose T = load_pose(q, t, Rt, pf[pi]);
+    double J[36];
+    prior_eval(init_inv + pi * 7, T, wa, r, J);
+    emit(J, contrib + (int64_t)(2 * E + pi) * 42);
+  }
+}
+
 // + the incident pose terms (rank 0 only holds them), in term order.
-__global__ void k_cam_terms(CamArgs a) {
-  int j = blockIdx.x * blockDim.x + threadIdx.x;
+__global__ void k_cam_terms_sum(CamArgs a, const double* __restrict__ contrib) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= a.nf || a.term_ptr[j] == a.term_ptr[j + 1]) return;
   double* U = a.U + (int64_t)j * 36;
   double* g = a.gc + (int64_t)j * 6;
+  double Ua[36], ga[6];
+#pragma unroll
+  for (int i = 0; i < 36; ++i) Ua[i] = U[i];
+#pragma unroll
+  for (int i = 0; i < 6; ++i) ga[i] = g[i];
   for (int k = a.term_ptr[j]; k < a.term_ptr[j + 1]; ++k) {
     const int code = a.term_list[k];
     const int term = code >> 2, side = code & 3;
-    double r[6], J[36];
-    if (term < a.E) {
-      Pose Ta = load_pose(a.q, a.t, a.Rt, a.ab[2 * term]);
-      Pose Tb = load_pose(a.q, a.t, a.Rt, a.ab[2 * term + 1]);
-      if (side == 0) edge_eval(a.meas_inv + term * 7, Ta, Tb, a.we, r, J, nullptr);
-      else edge_eval(a.meas_inv + term * 7, Ta, Tb, a.we, r, nullptr, J);
-    } else {
-      const int pi = term - a.E;
-      Pose T = load_pose(a.q, a.t, a.Rt, a.pf[pi]);
-      prior_eval(a.init_inv + pi * 7, T, a.wa, r, J);
-    }
-    for (int rr = 0; rr < 6; ++rr) {
-      for (int cc = 0; cc < 6; ++cc) {
-        double s = 0.0;
-        for (int m = 0; m < 6; ++m) s += J[m * 6 + rr] * J[m * 6 + cc];
-        U[rr * 6 + cc] += s;
-      }
-      double s = 0.0;
-      for (int m = 0; m < 6; ++m) s += J[m * 6 + rr] * r[m];
-      g[rr] += s;
-    }
+    const double* c = contrib + (int64_t)(term < a.E ? 2 * term + side : 2 * a.E + (term - a.E)) * 42;
+#pragma unroll
+    for (int i = 0; i < 36; ++i) Ua[i] += __ldg(c + i);
+#pragma unroll
+    for (int i = 0; i < 6; ++i) ga[i] += __ldg(c + 36 + i);
   }
+#pragma unroll
+  for (int i = 0; i < 36; ++i) U[i] = Ua[i];
+#pragma unroll
+  for (int i = 0; i < 6; ++i) g[i] = ga[i];
 }
 
 __global__ void k_cam_post(int nf, const double* __restrict__ U, const double* __restrict__ gc,
@@ -1014,27 +1080,6 @@ __global__ void k_cam_post(int nf, const double* __restrict__ U, const double* _
 }
 
 // Off-diagonal edge block oriented as the upper block (lo, hi).
-__global__ void k_edge_lin(int E, const int* __restrict__ ab, const int* __restrict__ free_idx,
-                           const double* __restrict__ meas_inv, double we, const double* q,
-                           const double* t, const double* Rt, double* __restrict__ H) {
-  int e = blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= E) return;
-  int fa = ab[2 * e], fb = ab[2 * e + 1];
-  int ja = free_idx[fa], jb = free_idx[fb];
-  if (ja < 0 || jb < 0 || ja == jb) return;
-  Pose Ta = load_pose(q, t, Rt, fa), Tb = load_pose(q, t, Rt, fb);
-  double r[6], Ja[36], Jb[36];
-  edge_eval(meas_inv + e * 7, Ta, Tb, we, r, Ja, Jb);
-  const double* L = ja < jb ? Ja : Jb;
-  const double* Rr = ja < jb ? Jb : Ja;
-  for (int rr = 0; rr < 6; ++rr)
-    for (int cc = 0; cc < 6; ++cc) {
-      double s = 0.0;
-      for (int m = 0; m < 6; ++m) s += L[m * 6 + rr] * Rr[m * 6 + cc];
-      H[(int64_t)e * 36 + rr * 6 + cc] = s;
-    }
-}
-
 // ---------------------------------------------------------------------------
 // Schur complement (per LM trial)
 // ---------------------------------------------------------------------------
@@ -1814,7 +1859,11 @@ void BASolver::linearize() {
     c.q = q_[cur_].get(); c.t = t_[cur_].get(); c.Rt = Rt_[cur_].get(); c.U = U_.get(); c.gc = gc_.get();
     if (n_edges_ + n_priors_) {
       ProfScope ps(*prof_, "cam_terms", 0.0, s);
-      k_cam_terms<<<grid_for(nfree_, 64), 64, 0, s>>>(c);
+      term_contrib_.resize((size_t)(2 * n_edges_ + n_priors_) * 42);
+      k_terms_lin<<<grid_for(n_edges_ + n_priors_, 32), 32, 0, s>>>(
+          n_edges_, n_priors_, edge_ab_.get(), prior_frame_.get(), free_idx_.get(), edge_meas_inv_.get(),
+          prior_init_inv_.get(), edge_w_, prior_w_, c.q, c.t, c.Rt, term_contrib_.get(), edge_H_.get());
+      k_cam_terms_sum<<<grid_for(nfree_, 64), 64, 0, s>>>(c, term_contrib_.get());
     }
     if (comm_ && comm_->active()) {
       comm_->sum(U_.get(), (size_t)nfree_ * 36, s);
@@ -1824,10 +1873,6 @@ void BASolver::linearize() {
       ProfScope ps(*prof_, "cam_post", 0.0, s);
       k_cam_post<<<grid_for(nfree_, 128), 128, 0, s>>>(nfree_, U_.get(), gc_.get(), Dc_.get(), sc_.get());
     }
-  }
-  if (n_edges_) {
-    ProfScope ps(*prof_, "edge_lin", 0.0, s);
-    k_edge_lin<<<grid_for(n_edges_, 64), 64, 0, s>>>(n_edges_, edge_ab_.get(), free_idx_.get(), edge_meas_inv_.get(), edge_w_, q_[cur_].get(), t_[cur_].get(), Rt_[cur_].get(), edge_H_.get());
   }
   if (!use_dense_ && nfree_)
     pcg_.set_basis(free_frame_.get(), q_[cur_].get(), t_[cur_].get(), Rt_[cur_].get(), s, prof_);

@@ -33,37 +33,53 @@ __global__ void k_block_jacobi(int nf, const int* __restrict__ diag_pos, const d
                                double* __restrict__ Minv, BAScalars* sc) {
   int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= nf) return;
-  const double* A = S + (int64_t)diag_pos[j] * 36;
+  const double* Ag = S + (int64_t)diag_pos[j] * 36;
+  // fully unrolled: the block and both factors stay in registers
+  double A[36];
+#pragma unroll
+  for (int i = 0; i < 36; ++i) A[i] = __ldg(Ag + i);
   double L[36];
+#pragma unroll
   for (int i = 0; i < 36; ++i) L[i] = 0.0;
   bool ok = true;
+#pragma unroll
   for (int c = 0; c < 6; ++c) {
     double s = A[c * 6 + c];
+#pragma unroll
     for (int k = 0; k < c; ++k) s -= L[c * 6 + k] * L[c * 6 + k];
     if (!(s > 0.0)) { ok = false; s = 1.0; }
     double d = sqrt(s);
     L[c * 6 + c] = d;
+#pragma unroll
     for (int r = c + 1; r < 6; ++r) {
       double v = A[r * 6 + c];
+#pragma unroll
       for (int k = 0; k < c; ++k) v -= L[r * 6 + k] * L[c * 6 + k];
       L[r * 6 + c] = v / d;
     }
   }
   double Li[36];
+#pragma unroll
   for (int i = 0; i < 36; ++i) Li[i] = 0.0;
+#pragma unroll
   for (int c = 0; c < 6; ++c) {
     Li[c * 6 + c] = 1.0 / L[c * 6 + c];
+#pragma unroll
     for (int r = c + 1; r < 6; ++r) {
       double s = 0.0;
+#pragma unroll
       for (int k = c; k < r; ++k) s += L[r * 6 + k] * Li[k * 6 + c];
       Li[r * 6 + c] = -s / L[r * 6 + r];
     }
   }
   double* M = Minv + (int64_t)j * 36;
+#pragma unroll
   for (int r = 0; r < 6; ++r)
+#pragma unroll
     for (int c = 0; c < 6; ++c) {
       double s = 0.0;
-      for (int k = max(r, c); k < 6; ++k) s += Li[k * 6 + r] * Li[k * 6 + c];
+#pragma unroll
+      for (int k = (r > c ? r : c); k < 6; ++k) s += Li[k * 6 + r] * Li[k * 6 + c];
       M[r * 6 + c] = s;
     }
   if (!ok) atomicOr(&sc->nonfinite, 1);
