@@ -175,3 +175,14 @@ if os.environ.get("MORE"):
         z = z + Q(r - S @ z)
         return z + jac(r - S @ z)
     pcg(vcyc, zero, "V-cycle (J, coarse, J)")
+
+if os.environ.get("CLUSTERS"):
+    for Cx in [int(v) for v in os.environ["CLUSTERS"].split(",")]:
+        ncx = (nf + Cx - 1) // Cx
+        clx = np.arange(nf) // Cx
+        Pd = np.zeros((nf, 6, 6))
+        for i, f in enumerate(free):
+            Pd[i] = G.adjoint(G.pose(q[f], t[f]))
+        Px = sp.bsr_matrix((Pd, clx, np.arange(nf + 1)), shape=(6 * nf, 6 * ncx)).tocsr()
+        Acix = np.linalg.inv((Px.T @ (S @ Px)).toarray())
+        pcg(lambda r: jac(r) + Px @ (Acix @ (Px.T @ r)), zero, f"additive two-level C={Cx} (nc={ncx})")
