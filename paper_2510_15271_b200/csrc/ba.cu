@@ -689,7 +689,13 @@ __global__ void k_off_records(int n, const int* __restrict__ work, const unsigne
   kr[w] = pb >= 0 ? make_longlong2(pb_pair_ptr[pb], pb_pair_ptr[pb + 1]) : make_longlong2(0, 0);
 }
 
-__global__ void __launch_bounds__(kOffWarps * 32, 5) k_offdiag_blocks(BlkArgs a) {
+#ifndef SFM_OFF_MINB
+#define SFM_OFF_MINB 5
+#endif
+#ifndef SFM_CAM_MINB
+#define SFM_CAM_MINB 5
+#endif
+__global__ void __launch_bounds__(kOffWarps * 32, SFM_OFF_MINB) k_offdiag_blocks(BlkArgs a) {
   __shared__ double Ast[kOffWarps][32 * kOffLd];
   __shared__ double Bst[kOffWarps][32 * kOffLd];
   __shared__ Mat3 Rsm[kOffWarps][2];
@@ -807,7 +813,7 @@ constexpr int kCamLd = 29;  // staged factors per observation: A (12) | B (16), 
 // DMMA.8x8x4 over its 32-observation batches (two observations per step)
 // and the four warp results are added in warp order -- fixed order.
 template <int MODE>
-__global__ void __launch_bounds__(kCamWarps * 32, 5) k_cam_blocks(BlkArgs a) {
+__global__ void __launch_bounds__(kCamWarps * 32, SFM_CAM_MINB) k_cam_blocks(BlkArgs a) {
   __shared__ double St[kCamWarps][32 * kCamLd];
   __shared__ double Wsum[kCamWarps][64];
   const int j = blockIdx.x;
