@@ -62,10 +62,40 @@ def max_over_ranks(x, world):
     return float(t.item())
 
 
+def _clock_poller(device, conn, period):
+    """Child process of ClockSampler: NVML SM clock + clocks-event reasons
+    every `period` s, each sample stamped with CLOCK_MONOTONIC (comparable
+    across processes), until the parent says stop."""
+    try:
+        import pynvml
+        pynvml.nvmlInit()
+        h = pynvml.nvmlDeviceGetHandleByIndex(device)
+        smax = float(pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM))
+    except Exception as e:  # no NVML / no device: the parent reports no samples
+        conn.send(f"error: {e}")
+        return
+    out = []
+    first = True
+    while True:
+        try:
+            out.append((time.monotonic(), float(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)),
+                        int(pynvml.nvmlDeviceGetCurrentClocksEventReasons(h))))
+        except Exception:
+            pass
+        if first:
+            conn.send("ready")
+            first = False
+        if conn.poll(period):
+            conn.recv()
+            break
+    conn.send((smax, out))
+
+
 class ClockSampler:
     """SM clocks and throttle reasons sampled DURING the timed region: NVML
-    (nvidia-ml-py) polled from a thread every 2 ms (the timed region is tens
-    of milliseconds, too short for `nvidia-smi -lms`), nvidia-smi fallback."""
+    polled every 1 ms from a separate process (no GIL or host-thread
+    scheduling interplay with the driving thread); only samples stamped
+    inside [enter, exit] are reported."""
 
     REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
                "sw_power_cap": 0x4}
@@ -75,42 +105,53 @@ class ClockSampler:
         self.samples = []
         self.reasons = set()
         self.smax = None
+        self.proc = None
 
     def __enter__(self):
-        import threading
-        self.stop = threading.Event()
+        import multiprocessing as mp
         try:
-            import pynvml
-            pynvml.nvmlInit()
-            h = pynvml.nvmlDeviceGetHandleByIndex(self.device)
-            self.smax = float(pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM))
-
-            def poll():
-                while not self.stop.is_set():
-                    try:
-                        self.samples.append(float(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)))
-                        bits = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
-                        for n, m in self.REASONS.items():
-                            if bits & m:
-                                self.reasons.add(n)
-                    except Exception:
-                        pass
-                    self.stop.wait(0.002)
-            self.th = threading.Thread(target=poll, daemon=True)
-            self.th.start()
+            ctx = mp.get_context("spawn")
+            self.conn, child = ctx.Pipe()
+            self.proc = ctx.Process(target=_clock_poller, args=(self.device, child, 0.001), daemon=True)
+            self.proc.start()
+            msg = None
+            for _ in range(600):  # <= 60 s for the child's imports + nvmlInit
+                if self.conn.poll(0.1):
+                    msg = self.conn.recv()
+                    break
+                if not self.proc.is_alive():
+                    break
+            if msg != "ready":
+                raise RuntimeError(f"clock poller did not start: {msg}")
         except Exception:
-            self.th = None
+            if self.proc is not None and self.proc.is_alive():
+                self.proc.kill()
+            self.proc = None
+        self.t0 = time.monotonic()
         return self
 
     def __exit__(self, *exc):
-        self.stop.set()
-        if self.th:
-            self.th.join()
+        t1 = time.monotonic()
+        if self.proc is None:
+            return
+        try:
+            self.conn.send("stop")
+            if self.conn.poll(30.0):
+                self.smax, out = self.conn.recv()
+                for ts, mhz, bits in out:
+                    if self.t0 <= ts <= t1:
+                        self.samples.append(mhz)
+                        for n, m in self.REASONS.items():
+                            if bits & m:
+                                self.reasons.add(n)
+        finally:
+            self.proc.join(timeout=10)
 
     def summary(self):
         return {"sm_mhz": float(np.median(self.samples)) if self.samples else None,
                 "sm_max_mhz": self.smax, "reasons": sorted(self.reasons),
-                "samples": len(self.samples), "source": "NVML, 2 ms polling during the timed region"}
+                "samples": len(self.samples),
+                "source": "NVML, 1 ms polling from a separate process, samples inside the timed region"}
 
 
 def build_workload(seed):
