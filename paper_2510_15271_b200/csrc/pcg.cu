@@ -410,7 +410,7 @@ __global__ void __launch_bounds__(kGJThreads) k_gj_inverse(double* A0, double* A
 // Persistent two-level PCG.
 //
 // Partition (built on the host once per BSR pattern, set_pattern): G CTAs
-// (<= 2 per SM, all co-resident) own contiguous block-row ranges of S
+// (one 512-thread CTA per SM by default, all co-resident) own contiguous block-row ranges of S
 // balanced by stored blocks; inside a CTA the range's blocks are cut into
 // kPcgWarps contiguous chunks, one per warp, so every warp streams the same
 // number of S blocks whatever the row lengths.  A warp's chunk meets one or
