@@ -684,6 +684,50 @@ def iterative_map_rolling_fixture(name="iterative_map_rolling"):
           f"added={[r['added'] for r in rs]} removed={[r['removed'] for r in rs]}")
 
 
+def edge_fixture():
+    """Empty / degenerate inputs through the reference entry points
+    (bundle_adjust without landmarks, all frames fixed, empty gate, empty and
+    single-track iterative_map) -> edge_cases.npz."""
+    poses = {i: exp_map(np.array([0.01 * i, -0.02 * i, 0.005 * i, 0.3 * i, 0.0, 0.0])) for i in range(4)}
+    out = {"poses4": np.array([np.concatenate([poses[i].quat, poses[i].t]) for i in range(4)])}
+    # E1: free frames, pose terms only
+    smap = M.SparseMap({i: Keyframe(i, float(i), 0, poses[i]) for i in range(4)}, {0: CAM}, fixed_frames={0})
+    rep = M.bundle_adjust(smap, M.MappingConfig(), stage=1)
+    out["e1_term"], out["e1_iters"], out["e1_cost"] = rep.termination, rep.iterations, rep.final_cost
+    # E2: every frame fixed, no landmarks
+    smap = M.SparseMap({i: Keyframe(i, float(i), 0, poses[i]) for i in range(4)}, {0: CAM},
+                       fixed_frames={0, 1, 2, 3})
+    rep = M.bundle_adjust(smap, M.MappingConfig(), stage=1)
+    out["e2_term"], out["e2_iters"] = rep.termination, rep.iterations
+    # E3: gate on a map without landmarks
+    smap = M.SparseMap({i: Keyframe(i, float(i), 0, poses[i]) for i in range(4)}, {0: CAM}, fixed_frames={0})
+    out["e3_removed"] = M.remove_outliers(smap, 2.0)[1]
+    # E4: iterative_map without tracks
+    sm = M.iterative_map([Keyframe(i, float(i), 0, poses[i]) for i in range(4)], [], {0: CAM})
+    out["e4_stats"] = np.array([[r["added"], r["removed"], r["landmarks"]] for r in sm.round_stats])
+    out["e4_fixed"] = np.array(sorted(sm.fixed_frames))
+    # E5: iterative_map with one two-view track
+    trs = [M.Track([M.Observation(0, 0, np.array([100.0, 100.0])), M.Observation(1, 0, np.array([100.0, 100.0]))])]
+    sm = M.iterative_map([Keyframe(i, float(i), 0, poses[i]) for i in range(4)], trs, {0: CAM})
+    out["e5_stats"] = np.array([[r["added"], r["removed"], r["landmarks"]] for r in sm.round_stats])
+    out["e5_status"] = trs[0].status
+    out["e5_X"] = np.array([lm.position for lm in sm.landmarks])
+    # E6: all frames fixed, landmarks free (points-only problem)
+    rng = np.random.default_rng(11)
+    pts, sposes = scene(rng, 5, 25)
+    smap = map_from_scene(pts, sposes, 0.01, rng, fixed_frames=tuple(range(5)), noise=0.3)
+    X0 = np.array([lm.position for lm in smap.landmarks])
+    rep = M.bundle_adjust(smap, M.MappingConfig(max_solver_iters=30), stage=1)
+    out["e6_X0"] = X0
+    out["e6_X"] = np.array([lm.position for lm in smap.landmarks])
+    out["e6_term"], out["e6_iters"], out["e6_cost"] = rep.termination, rep.iterations, rep.final_cost
+    out["e6_poses"] = np.array([np.concatenate([sposes[f].quat, sposes[f].t]) for f in sorted(sposes)])
+    out["e6_obs"] = np.array([[k, o.frame_id, o.pixel[0], o.pixel[1]] for k, lm in enumerate(smap.landmarks)
+                              for o in lm.track.observations])
+    np.savez_compressed(os.path.join(HERE, "edge_cases.npz"), **out)
+    print("edge_cases:", {k: v for k, v in out.items() if np.ndim(v) == 0})
+
+
 # --- known-answer vectors for the geometry --------------------------------------
 
 def kat_fixture():
@@ -723,13 +767,15 @@ def kat_fixture():
 
 
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["kat", "tri", "gate", "imap", "ba", "kinds", "tracks", "rigrs"]
+    which = sys.argv[1:] or ["kat", "tri", "gate", "imap", "ba", "kinds", "tracks", "rigrs", "edge"]
     if "kat" in which:
         kat_fixture()
     if "kinds" in which:
         camera_kinds_fixtures()
     if "tracks" in which:
         tracks_fixture()
+    if "edge" in which:
+        edge_fixture()
     if "rigrs" in which:
         rig_rs_fixtures()
         iterative_map_rolling_fixture()
