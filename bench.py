@@ -339,6 +339,9 @@ def main():
                if isinstance(getattr(part, f.name), np.ndarray)}
         part_pinned = dataclasses.replace(part, **pin)
         del ba  # the stepwise session's device memory returns to the pool
+        # one untimed call first (host first-touch of the structure-build
+        # buffers, pool growth), then the timed call
+        solve_arrays(part_pinned, loss, SolverOptions(max_iters=args.steps), dopt, ctx)
         barrier_sync(world)
         t0 = time.perf_counter()
         q, t, X, rep_e, raw_e = solve_arrays(part_pinned, loss, SolverOptions(max_iters=args.steps),
@@ -353,8 +356,9 @@ def main():
                "h2d_bytes_per_step": int(h2d / max(rep_e.iterations, 1)),
                "d2h_bytes_per_step": int(d2h / max(rep_e.iterations, 1)),
                "iterations": rep_e.iterations, "seconds": e2e_s,
-               "note": "one sfm_ba_solve call from pinned host arrays: H2D + structure build + "
-                       "initial cost + LM iterations 1..steps + D2H, amortised over its iterations"}
+               "note": "one sfm_ba_solve call from pinned host arrays (after one untimed warm-up call): "
+                       "H2D + structure build + initial cost + LM iterations 1..steps + D2H, amortised "
+                       "over its iterations"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
