@@ -312,7 +312,7 @@ def main():
     value = iters_done / t_step if iters_done else 0.0
 
     # residual+Jacobian throughput: linearisation kernels (point side + camera side)
-    lin_ms = sum(prof.get(k, {}).get("ms", 0.0) for k in ("point_lin", "cam_lin_chunks"))
+    lin_ms = sum(prof.get(k, {}).get("ms", 0.0) for k in ("point_lin", "cam_lin"))
     lin_launch = prof.get("point_lin", {}).get("launches", 0)
     n_obs_local = len(part.obs_frame)
     obs_per_s_local = n_obs_local * lin_launch / (lin_ms / 1000.0) if lin_ms > 0 else 0.0
