@@ -186,3 +186,46 @@ if os.environ.get("CLUSTERS"):
         Px = sp.bsr_matrix((Pd, clx, np.arange(nf + 1)), shape=(6 * nf, 6 * ncx)).tocsr()
         Acix = np.linalg.inv((Px.T @ (S @ Px)).toarray())
         pcg(lambda r: jac(r) + Px @ (Acix @ (Px.T @ r)), zero, f"additive two-level C={Cx} (nc={ncx})")
+
+
+# --- the kernel-shaped deflated CG (next-round design, see DESIGN "Next") ---
+# Per iteration, with clusters = CTAs: u = S z (own rows); t_c = P_c^T u
+# (own cluster); mu = E^-1 t (E = P^T S P exact); p = z + beta p - P mu;
+# q = u + beta q - (SP) mu;  pq from the recurrence formula (no extra
+# reduction); alpha = rz / pq; x += alpha p; r -= alpha q; z = D^-1 r.
+# Three reductions per iteration: (t, z.u, z.q_old) | (t.mu) | (r.z, r.r).
+if os.environ.get("DCG"):
+    E = (P.T @ (S @ P)).toarray()
+    Ei = np.linalg.inv(E)
+    SP = (S @ P).tocsr()
+
+    def dcg(x0, name, maxit=5000, rtol=1e-8, formula=True):
+        bn = np.linalg.norm(b)
+        # x0 -> x0 + Q (b - S x0): residual orthogonal to range(P)
+        x = x0 + P @ (Ei @ (P.T @ (b - S @ x0)))
+        r = b - S @ x
+        z = jac(r)
+        p = np.zeros_like(b); q = np.zeros_like(b)
+        rz = r @ z; pq_old = 1.0; beta = 0.0
+        for it in range(1, maxit + 1):
+            u = S @ z
+            t = P.T @ u
+            mu = Ei @ t
+            zu, zq = z @ u, z @ q
+            p = z + beta * p - P @ mu
+            q = u + beta * q - SP @ mu
+            pq = (zu + beta * beta * pq_old + 2 * beta * zq - t @ mu) if formula else p @ q
+            al = rz / pq
+            x += al * p
+            r -= al * q
+            if np.linalg.norm(r) <= rtol * bn:
+                break
+            z = jac(r)
+            rz_new = r @ z
+            beta = rz_new / rz
+            rz = rz_new
+            pq_old = pq
+        true = np.linalg.norm(b - S @ x) / bn
+        print(f"{name:28s} iterations {it:5d}  |r|/|b| {true:.2e}  |x| {np.linalg.norm(x):.6e}", flush=True)
+    dcg(zero, "DCG, pq direct", formula=False)
+    dcg(zero, "DCG, pq recurrence")
