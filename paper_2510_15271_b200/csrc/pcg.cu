@@ -567,6 +567,7 @@ struct PcgSmem {
   int* lc;      // [maxblk] local column index of each of the CTA's blocks
   int2* rs;     // [maxrows] (first segment, count) of each of the CTA's rows
   int* rp;      // [maxrows+1] row_ptr of the CTA's rows
+  int* cc0;     // [nc+1] first CTA of each coarse cluster
 };
 
 // z_i = D_i^-1 r_i (+ P_i e) for lanes 0..5 of the warp owning local row i
@@ -612,7 +613,7 @@ __device__ __forceinline__ double restrict_row(const PcgSmem& m, int i, double v
 //   rc[t] = sum_c rpart (assign) or rc[t] -= scale * sum_c rpart.
 __device__ __forceinline__ void gather_after_sync(const Pcg3Args& a, const double* part, double* out, int nsum,
                                                   double* rc, bool two, bool assign, const double* scale_num,
-                                                  const double* scale_den) {
+                                                  const double* scale_den, const int* cc0) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (warp < nsum) {
     double s = 0.0;
@@ -620,15 +621,29 @@ __device__ __forceinline__ void gather_after_sync(const Pcg3Args& a, const doubl
     s = warp_sum(s);
     if (lane == 0) out[warp] = s;
   }
-  double qs[4];
+  // up to four restriction entries per thread: the first CTA of each
+  // entry's cluster is one independent load (cluster bounds from smem), so
+  // the four L2 round trips overlap; clusters of several CTAs add the rest
+  // in CTA order
+  double qs[4] = {0.0, 0.0, 0.0, 0.0};
   int nq = 0;
-  if (two)
-    for (int t = threadIdx.x - 32 * nsum; t < 6 * a.nc && t >= 0 && nq < 4; t += kPcgThreads - 32 * nsum) {
-      const int k = t / 6, mm = t % 6;
-      double s = 0.0;
-      for (int c = a.cluster_cta0[k]; c < a.cluster_cta0[k + 1]; ++c) s += __ldcg(a.rpart + c * 6 + mm);
-      qs[nq++] = s;
+  const int t0 = threadIdx.x - 32 * nsum, tstride = kPcgThreads - 32 * nsum;
+  if (two && t0 >= 0) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int t = t0 + j * tstride;
+      if (t < 6 * a.nc) {
+        qs[j] = __ldcg(a.rpart + cc0[t / 6] * 6 + t % 6);
+        nq = j + 1;
+      }
     }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int t = t0 + j * tstride;
+      if (j < nq)
+        for (int c = cc0[t / 6] + 1; c < cc0[t / 6 + 1]; ++c) qs[j] += __ldcg(a.rpart + c * 6 + t % 6);
+    }
+  }
   __syncthreads();
   if (two) {
     const double alpha = assign ? 0.0 : (*scale_num) / (*scale_den);
@@ -640,7 +655,7 @@ __device__ __forceinline__ void gather_after_sync(const Pcg3Args& a, const doubl
          t += kPcgThreads - 32 * nsum) {
       const int k = t / 6, mm = t % 6;
       double s = 0.0;
-      for (int c = a.cluster_cta0[k]; c < a.cluster_cta0[k + 1]; ++c) s += __ldcg(a.rpart + c * 6 + mm);
+      for (int c = cc0[k]; c < cc0[k + 1]; ++c) s += __ldcg(a.rpart + c * 6 + mm);
       rc[t] = assign ? s : rc[t] - alpha * s;
     }
   }
@@ -723,6 +738,7 @@ __global__ void __launch_bounds__(kPcgMaxThreads, 1) k_pcg3(Pcg3Args a) {
   m.lc = reinterpret_cast<int*>(m.zc + 6 * a.maxdist);
   m.rs = reinterpret_cast<int2*>(m.lc + ((a.maxblk + 1) & ~1));
   m.rp = reinterpret_cast<int*>(m.rs + a.maxrows);
+  m.cc0 = m.rp + a.maxrows + 1;
   __shared__ double2 red[32];
   __shared__ double tmp[16];
   __shared__ double e[6];
@@ -776,6 +792,7 @@ __global__ void __launch_bounds__(kPcgMaxThreads, 1) k_pcg3(Pcg3Args a) {
   for (int t = threadIdx.x; t < nblk; t += kPcgThreads) m.lc[t] = __ldg(a.lcol + kc0 + t);
   for (int t = threadIdx.x; t < nrows; t += kPcgThreads) m.rs[t] = a.rowseg[row0 + t];
   for (int t = threadIdx.x; t <= nrows; t += kPcgThreads) m.rp[t] = __ldg(a.row_ptr + row0 + t);
+  for (int t = threadIdx.x; t <= a.nc; t += kPcgThreads) m.cc0[t] = a.cluster_cta0[t];
   const int* rpl = m.rp - row0;  // rpl[r] = row_ptr[r] for the CTA's rows
   // resident S blocks: the head of every warp's chunk (18 double2 per block)
   for (int w = 0; w < kPcgWarps; ++w) {
@@ -824,7 +841,7 @@ __global__ void __launch_bounds__(kPcgMaxThreads, 1) k_pcg3(Pcg3Args a) {
     const double2 t = block_sum2(xb, xw, red);
     if (threadIdx.x == 0) { part_rz[blockIdx.x] = t.x; part_rz[G + blockIdx.x] = t.y; }
     grid.sync();
-    gather_after_sync(a, part_rz, sums, 2, m.rc, false, true, nullptr, nullptr);
+    gather_after_sync(a, part_rz, sums, 2, m.rc, false, true, nullptr, nullptr, m.cc0);
     const double g = sums[0] / sums[1];
     gamma = (sums[1] > 0.0 && isfinite(g)) ? g : 0.0;
   }
@@ -852,7 +869,7 @@ __global__ void __launch_bounds__(kPcgMaxThreads, 1) k_pcg3(Pcg3Args a) {
   double2 sb = block_sum2(bb_l, 0.0, red);
   if (threadIdx.x == 0) part_bb[blockIdx.x] = sb.x;
   grid.sync();
-  gather_after_sync(a, part_bb, sums, 1, m.rc, two, true, nullptr, nullptr);
+  gather_after_sync(a, part_bb, sums, 1, m.rc, two, true, nullptr, nullptr, m.cc0);
   const double bnorm = sqrt(sums[0]);
   if (two) coarse_apply(a, m, e, tmp);
   double rz_l = 0.0;
@@ -909,7 +926,7 @@ __global__ void __launch_bounds__(kPcgMaxThreads, 1) k_pcg3(Pcg3Args a) {
       grid.sync();
       PH(2);
       // ---- phase 2: x += alpha p; r -= alpha q; rc -= alpha P^T q; z = M^-1 r
-      gather_after_sync(a, part_pq, sums, 1, m.rc, two, false, &rz_old, &sums[0]);
+      gather_after_sync(a, part_pq, sums, 1, m.rc, two, false, &rz_old, &sums[0], m.cc0);
       const double pq = sums[0];
       if (!(pq > 0.0) || !isfinite(pq)) { fail = 1; break; }
       const double alpha = rz_old / pq;
@@ -1113,7 +1130,7 @@ void TwoLevelPcg::set_pattern(const int* row_ptr, const int* col, int nnzb, cuda
   SFM_CUDA(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
   const size_t per_cta_avail = (size_t)max_smem / per_sm - 2048;  // static smem margin
   const size_t zbytes = sizeof(double) * 6 * (size_t)maxdist_ + sizeof(int) * (size_t)(maxblk_ + 1) +
-                        sizeof(int2) * maxrows_ + sizeof(int) * (maxrows_ + 1) + 16;
+                        sizeof(int2) * maxrows_ + sizeof(int) * (maxrows_ + 1 + nc_ + 1) + 16;
   SFM_REQUIRE(smem_ + zbytes <= per_cta_avail, "PCG z cache does not fit in shared memory");
   // Measured on config 3: keeping S blocks resident costs the L1 capacity
   // the rest of the loop relies on and is slower (20.5 vs 18.2 us/iteration),
@@ -1139,7 +1156,7 @@ void TwoLevelPcg::set_pattern(const int* row_ptr, const int* col, int nnzb, cuda
   resblocks_ = maxres;
   smem_ += sizeof(double) * 36 * (size_t)maxres;
   smem_ += sizeof(double) * 6 * (size_t)maxdist_ + sizeof(int) * (size_t)(maxblk_ + 1) + sizeof(int2) * maxrows_ +
-           sizeof(int) * (maxrows_ + 1) + 16;
+           sizeof(int) * (maxrows_ + 1 + nc_ + 1) + 16;
   SFM_CUDA(cudaFuncSetAttribute(k_pcg3, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_));
   int resident = 0;
   SFM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&resident, k_pcg3, nt_, smem_));
