@@ -607,6 +607,21 @@ __device__ __forceinline__ double restrict_row(const PcgSmem& m, int i, double v
   return y;
 }
 
+// Sum of n per-CTA partials by one warp: every lane's loads issued together
+// (8 per batch), then added in ascending index order -- the order of a plain
+// strided loop, one L2 round trip for n <= 256.
+__device__ __forceinline__ double lane_partial_sum(const double* __restrict__ p, int n, int lane) {
+  double s = 0.0;
+  for (int i0 = lane; i0 < n; i0 += 256) {
+    double v[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) v[q] = i0 + 32 * q < n ? __ldcg(p + i0 + 32 * q) : 0.0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) s += v[q];
+  }
+  return s;
+}
+
 // After a grid barrier: the scalar sum over the G per-CTA partials `part`
 // (warp 0, fixed order) and, for the two-level preconditioner, the cluster
 // restriction sums (other warps), in one round trip.
@@ -617,7 +632,7 @@ __device__ __forceinline__ void gather_after_sync(const Pcg3Args& a, const doubl
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (warp < nsum) {
     double s = 0.0;
-    for (int i = lane; i < a.G; i += 32) s += __ldcg(part + warp * a.G + i);
+    s = lane_partial_sum(part + warp * a.G, a.G, lane);
     s = warp_sum(s);
     if (lane == 0) out[warp] = s;
   }
@@ -763,7 +778,7 @@ __global__ void __launch_bounds__(kPcgMaxThreads, 1) k_pcg3(Pcg3Args a) {
   auto sums_and_zc = [&](const double* part, int nsum) {
     if (warp < nsum) {
       double sacc = 0.0;
-      for (int i = lane; i < G; i += 32) sacc += __ldcg(part + warp * G + i);
+      sacc = lane_partial_sum(part + warp * G, G, lane);
       sacc = warp_sum(sacc);
       if (lane == 0) sums[warp] = sacc;
     }
