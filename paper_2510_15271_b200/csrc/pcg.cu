@@ -511,6 +511,48 @@ __device__ __forceinline__ void spmv_segments(const Pcg3Args& a, const double* z
   const int kres = ch.x + wr.x;                    // first non-resident block
   const double* Sres = Ssm + ((int64_t)wr.y - ch.x) * 36 + comp * 6;  // Sres + k*36 for resident k
   const int* lcb = lc - kc0;                       // lcb[k] for global block k
+  // Chunks over one or two rows (nearly all of them) stream all their blocks
+  // in one loop: a block's product goes to the accumulators of its row, so
+  // the loads do not stop and restart at the row boundary.
+  const int rb = rpl[r + 1];  // end of the first row
+  if (wr.x == 0 && (rb >= ke || rpl[r + 2] >= ke)) {
+    const int bnd = min(rb, ke);
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;  // first row
+    double b0 = 0.0, b1 = 0.0, b2 = 0.0, b3 = 0.0;  // second row
+    if (lane < 30) {
+      int k = kb + grp;
+      for (; k + 15 < ke; k += 20) {
+        const double* s0 = a.S + (int64_t)k * 36 + comp * 6;
+        const double d0 = dot6_sg(s0, zc + lcb[k] * 6);
+        const double d1 = dot6_sg(s0 + 5 * 36, zc + lcb[k + 5] * 6);
+        const double d2 = dot6_sg(s0 + 10 * 36, zc + lcb[k + 10] * 6);
+        const double d3 = dot6_sg(s0 + 15 * 36, zc + lcb[k + 15] * 6);
+        if (k < bnd) a0 += d0; else b0 += d0;
+        if (k + 5 < bnd) a1 += d1; else b1 += d1;
+        if (k + 10 < bnd) a2 += d2; else b2 += d2;
+        if (k + 15 < bnd) a3 += d3; else b3 += d3;
+      }
+      for (; k < ke; k += 5) {
+        const double d = dot6_sg(a.S + (int64_t)k * 36 + comp * 6, zc + lcb[k] * 6);
+        if (k < bnd) a0 += d; else b0 += d;
+      }
+    }
+    double acc = (a0 + a1) + (a2 + a3);
+    double v1 = __shfl_sync(full, acc, comp + 6);
+    double v2 = __shfl_sync(full, acc, comp + 12);
+    double v3 = __shfl_sync(full, acc, comp + 18);
+    double v4 = __shfl_sync(full, acc, comp + 24);
+    if (lane < 6) seg[sidx * 6 + lane] = (((acc + v1) + v2) + v3) + v4;
+    if (bnd < ke) {
+      acc = (b0 + b1) + (b2 + b3);
+      v1 = __shfl_sync(full, acc, comp + 6);
+      v2 = __shfl_sync(full, acc, comp + 12);
+      v3 = __shfl_sync(full, acc, comp + 18);
+      v4 = __shfl_sync(full, acc, comp + 24);
+      if (lane < 6) seg[(sidx + 1) * 6 + lane] = (((acc + v1) + v2) + v3) + v4;
+    }
+    return;
+  }
   while (kb < ke) {
     const int re = min(ke, rpl[r + 1]);  // row ends staged in smem: no L2 round trip per segment
     double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, acc3 = 0.0;
