@@ -827,10 +827,23 @@ __global__ void __launch_bounds__(kCamWarps * 32, SFM_CAM_MINB) k_cam_blocks(Blk
   double* As = &St[warp][lane * kCamLd];
   double* Bs = As + 12;
   const int fr = lane >> 2, fk = lane & 3;
+  // one batch ahead: MODE 0 loads the next linearisation record, MODE 1 the
+  // next point id (the packed point record load then does not wait on it)
+  const int64_t kfirst = k0 + (int64_t)warp * 32 + lane;
+  double4 g_nx = make_double4(0.0, 0.0, 0.0, 0.0);
+  int pt_nx = 0;
+  if (MODE == 0 && kfirst < k1) g_nx = ldg256(a.geo_cm + kfirst);
+  if (MODE == 1 && kfirst < k1) pt_nx = __ldg(a.cm_pt + kfirst);
   for (int64_t kb = k0 + (int64_t)warp * 32; kb < k1; kb += kCamWarps * 32) {
     const int64_t k = kb + lane;
+    const double4 g_pf = g_nx;
+    const int pt_cur = pt_nx;
+    if (k + kCamWarps * 32 < k1) {
+      if (MODE == 0) g_nx = ldg256(a.geo_cm + k + kCamWarps * 32);
+      else pt_nx = __ldg(a.cm_pt + k + kCamWarps * 32);
+    }
     if (k < k1) {
-      const double4 g = ldg256(a.geo_cm + k);
+      const double4 g = MODE == 0 ? g_pf : ldg256(a.geo_cm + k);
       double Jc[12], Jp[6];
       geo_jacobians(cm, R, g, Jc, Jp);
 #pragma unroll
@@ -845,7 +858,7 @@ __global__ void __launch_bounds__(kCamWarps * 32, SFM_CAM_MINB) k_cam_blocks(Blk
         for (int c = 0; c < 6; ++c) { Bs[c] = Jc[c]; Bs[8 + c] = Jc[6 + c]; }
         Bs[6] = r0; Bs[14] = r1;
       } else {
-        const double* pv = a.pv + (int64_t)a.cm_pt[k] * 12;
+        const double* pv = a.pv + (int64_t)pt_cur * 12;
         const double4 pva = ldg256(pv), pvb = ldg256(pv + 4);
         const double v0 = pva.x, v1 = pva.y, v2 = pva.z, v3_ = pva.w, v4 = pvb.x, v5 = pvb.y;
         const double pe0 = pvb.z, pe1 = pvb.w, pe2 = __ldg(pv + 8);
