@@ -64,9 +64,13 @@ def build(q, t, X, lam):
     return S, b, dblocks, dict(W=W, j=j, Vinv=Vinv, e=e)
 
 
+prev_dc = []  # camera steps of the previous LM iterations (warm-start study)
+
+
 def step(S, b, aux, q, t, X):
     import scipy.sparse.linalg as spl
     dc = spl.spsolve(S.tocsc(), b).reshape(-1, 6)
+    prev_dc.append(dc.reshape(-1).copy())
     W, j, Vinv, e = aux["W"], aux["j"], aux["Vinv"], aux["e"]
     acc = np.zeros((pb.P, 3))
     fr = j >= 0
@@ -229,3 +233,21 @@ if os.environ.get("DCG"):
         print(f"{name:28s} iterations {it:5d}  |r|/|b| {true:.2e}  |x| {np.linalg.norm(x):.6e}", flush=True)
     dcg(zero, "DCG, pq direct", formula=False)
     dcg(zero, "DCG, pq recurrence")
+
+
+# --- warm starts: energy-optimal multiple of the previous step (the kernel)
+# vs the energy-optimal combination of the previous two steps ---------------
+if os.environ.get("WARM") and len(prev_dc) >= 2:
+    x1, x2 = prev_dc[-1], prev_dc[-2]
+    Sx1, Sx2 = S @ x1, S @ x2
+    g = (x1 @ b) / (x1 @ Sx1)
+    pcg(lambda r: jac(r) + Q(r), g * x1, "additive, warm gamma*x_prev")
+    G2 = np.array([[x1 @ Sx1, x1 @ Sx2], [x2 @ Sx1, x2 @ Sx2]])
+    c = np.linalg.solve(G2, np.array([x1 @ b, x2 @ b]))
+    pcg(lambda r: jac(r) + Q(r), c[0] * x1 + c[1] * x2, "additive, warm 2-vector")
+    if len(prev_dc) >= 3:
+        x3 = prev_dc[-3]
+        V = np.stack([x1, x2, x3], 1)
+        SV = np.stack([Sx1, Sx2, S @ x3], 1)
+        c3 = np.linalg.solve(V.T @ SV, V.T @ b)
+        pcg(lambda r: jac(r) + Q(r), V @ c3, "additive, warm 3-vector")
