@@ -83,8 +83,10 @@ nlm = int(sys.argv[4]) if len(sys.argv) > 4 else 0
 q, t, X = pb.q0, pb.t0, pb.X0
 lam_k = lam
 basis0 = None
+S_hist = []
 for k in range(nlm):
     S, b, dblocks, aux = build(q, t, X, lam_k)
+    S_hist.append((S, q.copy(), t.copy()))
     if basis0 is None:
         basis0 = (q.copy(), t.copy(), S)
     q, t, X = step(S, b, aux, q, t, X)
@@ -251,3 +253,19 @@ if os.environ.get("WARM") and len(prev_dc) >= 2:
         SV = np.stack([Sx1, Sx2, S @ x3], 1)
         c3 = np.linalg.solve(V.T @ SV, V.T @ b)
         pcg(lambda r: jac(r) + Q(r), V @ c3, "additive, warm 3-vector")
+
+
+# --- Newton-Schulz refresh of the coarse inverse: how far is the previous
+# solve's exact inverse from the new one?  eps0 = ||I - E_new X_old||_2 ----
+if os.environ.get("NS") and S_hist:
+    P_new, Aci_new = coarse(q, t, S)
+    E_new = (P_new.T @ (S @ P_new)).toarray()
+    Sp, qp, tp = S_hist[-1]
+    P_old, X_old = coarse(qp, tp, Sp)
+    I = np.eye(E_new.shape[0])
+    e0 = np.linalg.norm(I - E_new @ X_old, 2)
+    print(f"NS: eps0 (previous LM iteration, new basis) = {e0:.3e}", flush=True)
+    X = X_old.copy()
+    for it in range(4):
+        X = X @ (2 * I - E_new @ X)
+        print(f"NS step {it + 1}: ||I - E X|| = {np.linalg.norm(I - E_new @ X, 2):.3e}", flush=True)
