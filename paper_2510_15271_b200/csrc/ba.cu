@@ -78,6 +78,8 @@ struct BlkArgs {
   double* b;
   double* Uout;
   double* gout;
+  BAScalars* sc;
+  const BAScalars* pre;        // MODE 1: flags of a point prep done at linearisation (or null)
 };
 
 namespace {
@@ -429,6 +431,9 @@ struct PointArgs {
   const double* Rt_eval;  // state whose cost is evaluated
   double* X_out;          // trial points (TRIAL) or unused
   const double* pv;       // packed V*^-1 | e per point
+  double lam;              // k_point_lin: also prepare pv for this lambda (the first trial's)
+  double* pv_out;          //   into pv_out (null: skip), flags into sc_pre
+  BAScalars* sc_pre;
   const double* dc;
   const double4* geo;     // linearisation records (TRIAL) / output (LIN)
   const int* cm_pos;      // camera-major slot of each observation (-1: fixed)
@@ -593,6 +598,30 @@ __global__ void k_finalize(const double* __restrict__ pa, int na, const double* 
 // linearization (solver.py:210-217 restricted to the Schur blocks)
 // ---------------------------------------------------------------------------
 
+// V* = V + lam max(diag V, 1e-12), V*^-1 (adjugate), e = V*^-1 g -> the
+// packed point record; returns false when V* is not invertible / finite.
+__device__ __forceinline__ bool point_prep_one(const double* v, const double* g, double lam, double* o) {
+  double a = v[0] + lam * fmax(v[0], 1e-12);
+  double b = v[1], c = v[2];
+  double d = v[3] + lam * fmax(v[3], 1e-12);
+  double ee = v[4];
+  double f = v[5] + lam * fmax(v[5], 1e-12);
+  double A = d * f - ee * ee, B = c * ee - b * f, C = b * ee - c * d;
+  double D = a * f - c * c, Ee = b * c - a * ee, Fm = a * d - b * b;
+  double det = a * A + b * B + c * C;
+  double inv = 1.0 / det;
+  const double i0 = A * inv, i1 = B * inv, i2 = C * inv, i3 = D * inv, i4 = Ee * inv, i5 = Fm * inv;
+  const double e0 = i0 * g[0] + i1 * g[1] + i2 * g[2];
+  const double e1 = i1 * g[0] + i3 * g[1] + i4 * g[2];
+  const double e2 = i2 * g[0] + i4 * g[1] + i5 * g[2];
+  reinterpret_cast<double2*>(o)[0] = make_double2(i0, i1);
+  reinterpret_cast<double2*>(o)[1] = make_double2(i2, i3);
+  reinterpret_cast<double2*>(o)[2] = make_double2(i4, i5);
+  reinterpret_cast<double2*>(o)[3] = make_double2(e0, e1);
+  reinterpret_cast<double2*>(o)[4] = make_double2(e2, 0.0);
+  return det > 0.0 && isfinite(inv) && isfinite(e0) && isfinite(e1) && isfinite(e2);
+}
+
 // V_i = sum Jp^T Jp, g_i = sum Jp^T r over ALL observations of the point.
 __global__ void __launch_bounds__(kBlock) k_point_lin(PointArgs a, double* __restrict__ V,
                                                       double* __restrict__ gp) {
@@ -639,6 +668,10 @@ __global__ void __launch_bounds__(kBlock) k_point_lin(PointArgs a, double* __res
     for (int k = 0; k < 6; ++k) V[p * 6 + k] = v[k];
 #pragma unroll
     for (int k = 0; k < 3; ++k) gp[p * 3 + k] = g[k];
+    // the first trial's damped point record, while V and g are in registers
+    // (k_point_prep would re-read them); its flag goes to sc_pre, which the
+    // trial's diagonal Schur kernel folds into the trial's scalars
+    if (a.pv_out && !point_prep_one(v, g, a.lam, a.pv_out + p * 12)) atomicOr(&a.sc_pre->nonfinite, 1);
     gm = fmax(fabs(g[0]), fmax(fabs(g[1]), fabs(g[2])));
     if (isnan(g[0]) || isnan(g[1]) || isnan(g[2])) gm = __longlong_as_double(0x7ff8000000000000ll);
   }
@@ -818,6 +851,7 @@ __global__ void __launch_bounds__(kCamWarps * 32, SFM_CAM_MINB) k_cam_blocks(Blk
   __shared__ double Wsum[kCamWarps][64];
   const int j = blockIdx.x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (MODE == 1 && a.pre && j == 0 && threadIdx.x == 0 && a.pre->nonfinite) atomicOr(&a.sc->nonfinite, 1);
   const int f = a.free_frame[j];
   Mat3 R; Vec3 t;
   load_cam(a.Rt, f, R, t);
@@ -1105,33 +1139,12 @@ __global__ void k_cam_post(int nf, const double* __restrict__ U, const double* _
 
 // V* = V + lam*max(diag V, 1e-12) (solver.py:217-220), V*^-1 (adjugate),
 // e = V*^-1 g_p.
+
 __global__ void k_point_prep(int64_t P, double lam, const double* __restrict__ V,
                              const double* __restrict__ gp, double* __restrict__ pv, BAScalars* sc) {
   int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= P) return;
-  const double* v = V + p * 6;
-  double a = v[0] + lam * fmax(v[0], 1e-12);
-  double b = v[1], c = v[2];
-  double d = v[3] + lam * fmax(v[3], 1e-12);
-  double ee = v[4];
-  double f = v[5] + lam * fmax(v[5], 1e-12);
-  double A = d * f - ee * ee, B = c * ee - b * f, C = b * ee - c * d;
-  double D = a * f - c * c, Ee = b * c - a * ee, Fm = a * d - b * b;
-  double det = a * A + b * B + c * C;
-  double inv = 1.0 / det;
-  double* o = pv + p * 12;
-  const double i0 = A * inv, i1 = B * inv, i2 = C * inv, i3 = D * inv, i4 = Ee * inv, i5 = Fm * inv;
-  const double* g = gp + p * 3;
-  const double e0 = i0 * g[0] + i1 * g[1] + i2 * g[2];
-  const double e1 = i1 * g[0] + i3 * g[1] + i4 * g[2];
-  const double e2 = i2 * g[0] + i4 * g[1] + i5 * g[2];
-  reinterpret_cast<double2*>(o)[0] = make_double2(i0, i1);
-  reinterpret_cast<double2*>(o)[1] = make_double2(i2, i3);
-  reinterpret_cast<double2*>(o)[2] = make_double2(i4, i5);
-  reinterpret_cast<double2*>(o)[3] = make_double2(e0, e1);
-  reinterpret_cast<double2*>(o)[4] = make_double2(e2, 0.0);
-  if (!(det > 0.0) || !isfinite(inv) || !isfinite(e0) || !isfinite(e1) || !isfinite(e2))
-    atomicOr(&sc->nonfinite, 1);
+  if (!point_prep_one(V + p * 6, gp + p * 3, lam, pv + p * 12)) atomicOr(&sc->nonfinite, 1);
 }
 
 // ---------------------------------------------------------------------------
@@ -1857,7 +1870,16 @@ void BASolver::linearize() {
   if (P_) {
     // compulsory: observation records in, points in, V/g_p and the 32-byte
     // linearisation record per observation out
-    ProfScope ps(*prof_, "point_lin", 24.0 * N_ + 24.0 * P_ + 72.0 * P_ + 32.0 * N_, s);
+    prep_ready_ = nfree_ > 0;
+    if (prep_ready_) {
+      sc_pre_.resize(1);
+      SFM_CUDA(cudaMemsetAsync(sc_pre_.get(), 0, sizeof(BAScalars), s));
+      pa.lam = lam_;
+      pa.pv_out = pv_.get();
+      pa.sc_pre = sc_pre_.get();
+      prep_lam_ = lam_;
+    }
+    ProfScope ps(*prof_, "point_lin", 24.0 * N_ + 24.0 * P_ + 72.0 * P_ + 32.0 * N_ + (prep_ready_ ? 96.0 * P_ : 0.0), s);
     k_point_lin<<<grid_for(P_, kBlock), kBlock, 0, s>>>(pa, V_.get(), gp_.get());
   }
   if (nfree_) {
@@ -1903,6 +1925,7 @@ BlkArgs BASolver::blk_args(double lam) const {
   BlkArgs ba{};
   ba.work = work_.get(); ba.nf = nfree_; ba.rank = rank_; ba.lam = lam;
   ba.offrec = offrec_.get(); ba.offk = offk_.get();
+  ba.sc = sc_.get();
   ba.ub_key = ub_key_.get(); ba.ub_pb = ub_pb_.get(); ba.ub_edge = ub_edge_.get();
   ba.pos_up = ub_pos_up_.get(); ba.pos_lo = ub_pos_lo_.get(); ba.diag_ub = diag_ub_.get();
   ba.pb_pair_ptr = pb_pair_ptr_.get(); ba.pairs = pairs_.get(); ba.op = obs_point_.get();
@@ -1917,12 +1940,15 @@ BlkArgs BASolver::blk_args(double lam) const {
 
 void BASolver::build_schur(double lam) {
   cudaStream_t s = stream_;
-  if (P_) {
+  const bool prepped = prep_ready_ && lam == prep_lam_ && nfree_ > 0;
+  prep_ready_ = false;
+  if (P_ && !prepped) {
     ProfScope ps(*prof_, "point_prep", 72.0 * P_ + 96.0 * P_, s);
     k_point_prep<<<grid_for(P_, 256), 256, 0, s>>>(P_, lam, V_.get(), gp_.get(), pv_.get(), sc_.get());
   }
   if (nfree_) {
     BlkArgs ba = blk_args(lam);
+    ba.pre = prepped ? sc_pre_.get() : nullptr;
     // compulsory: camera-major record + point id per observation, packed
     // point record (V*^-1, e), diagonal blocks and b out
     ProfScope ps(*prof_, "schur_diag", (32.0 + 4.0) * n_cm_ + 96.0 * P_ + 336.0 * nfree_, s);

@@ -124,6 +124,9 @@ class BASolver {
   DevBuf<double> edge_meas_inv_;         // [E*7] q(4) t(3) of meas^-1
   DevBuf<double> prior_init_inv_;        // [A*7]
   DevBuf<int> term_ptr_, term_list_;     // per free camera incident terms
+  DevBuf<BAScalars> sc_pre_;             // flags of the point prep done inside k_point_lin
+  bool prep_ready_ = false;              // pv holds V*^-1 at prep_lam_ for the next trial
+  double prep_lam_ = 0.0;
   DevBuf<double> term_contrib_;          // [2E+A][42] per-term J^T J | J^T r (k_terms_lin)
   DevBuf<double> edge_H_;                // [E*36] J_a^T J_b (weighted)
 
