@@ -24,6 +24,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <future>
 #include <cmath>
 #include <chrono>
 #include <cstdio>
@@ -1366,6 +1367,11 @@ BASolver::~BASolver() {
     cudaStreamSynchronize(side_);
     cudaStreamDestroy(side_);
   }
+  if (plan_stream_) {
+    cudaStreamSynchronize(plan_stream_);
+    cudaStreamDestroy(plan_stream_);
+  }
+  if (plan_ev_) cudaEventDestroy(plan_ev_);
   if (side_ready_) cudaEventDestroy(side_ready_);
   if (side_done_) cudaEventDestroy(side_done_);
 }
@@ -1652,6 +1658,45 @@ void BASolver::setup(const sfm_ba_problem& pr, const sfm_ba_options& opt) {
     diag_pos_.upload(dpos.data(), nfree_, s);
   }
   tm.mark("S pattern");
+  // Linear solver choice, then the PCG plan (host-side partition of S) on
+  // its own thread and stream: it only needs the S pattern, and overlaps
+  // the camera-major streams, the pose-term lists and the initial cost.
+  int dense_cap = opt_.dense_max_dim > 0 ? std::min(opt_.dense_max_dim, kDenseMax) : kDenseMax;
+  if (opt_.linear_solver == SFM_LINSOLVE_DENSE) {
+    SFM_REQUIRE(6 * nfree_ <= kDenseMax, "dense solver limited to 6*free_frames <= 210; use PCG");
+    use_dense_ = 1;
+  } else if (opt_.linear_solver == SFM_LINSOLVE_PCG) {
+    use_dense_ = 0;
+  } else {
+    use_dense_ = (6 * nfree_ <= dense_cap) ? 1 : 0;
+  }
+  if (use_dense_ && nfree_ > 0) {
+    const int n = 6 * nfree_;
+    size_t smem = sizeof(double) * (size_t)n * (n + 1) / 2;
+    SFM_CUDA(cudaFuncSetAttribute(k_dense_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max<size_t>(smem, 1)));
+  }
+  std::future<void> plan;
+  if (!use_dense_ && nfree_ > 0) {
+    if (!plan_stream_) {
+      SFM_CUDA(cudaStreamCreateWithFlags(&plan_stream_, cudaStreamNonBlocking));
+      SFM_CUDA(cudaEventCreateWithFlags(&plan_ev_, cudaEventDisableTiming));
+    }
+    SFM_CUDA(cudaEventRecord(plan_ev_, s));  // row_ptr / col are complete here
+    int dev = 0;
+    SFM_CUDA(cudaGetDevice(&dev));
+    const int cl = opt_.coarse_cluster == 0 ? 8 : opt_.coarse_cluster;
+    const int refresh = opt_.coarse_refresh > 0 ? opt_.coarse_refresh : 8;
+    cudaStream_t ps = plan_stream_;
+    cudaEvent_t pe = plan_ev_;
+    plan = std::async(std::launch::async, [this, dev, cl, refresh, ps, pe]() {
+      SFM_CUDA(cudaSetDevice(dev));
+      alloc_stream() = ps;  // the plan's buffers are stream-ordered on the plan stream
+      SFM_CUDA(cudaStreamWaitEvent(ps, pe, 0));
+      pcg_.setup(nfree_, cl, refresh, ps);
+      pcg_.set_pattern(row_ptr_.get(), col_idx_.get(), n_full_, ps);  // ends with a sync of ps
+    });
+  }
+
   // camera-major observation streams + off-diagonal block list
   {
     std::vector<int64_t> cptr(nfree_ + 1, 0);
@@ -1741,26 +1786,7 @@ void BASolver::setup(const sfm_ba_problem& pr, const sfm_ba_options& opt) {
   part_c_.resize(grid_for(std::max(n_edges_ + n_priors_, 1), kBlock));
   part_d_.resize(grid_for(std::max(nfree_, 1), kBlock));
 
-  int dense_cap = opt_.dense_max_dim > 0 ? std::min(opt_.dense_max_dim, kDenseMax) : kDenseMax;
-  if (opt_.linear_solver == SFM_LINSOLVE_DENSE) {
-    SFM_REQUIRE(6 * nfree_ <= kDenseMax, "dense solver limited to 6*free_frames <= 210; use PCG");
-    use_dense_ = 1;
-  } else if (opt_.linear_solver == SFM_LINSOLVE_PCG) {
-    use_dense_ = 0;
-  } else {
-    use_dense_ = (6 * nfree_ <= dense_cap) ? 1 : 0;
-  }
-  if (use_dense_ && nfree_ > 0) {
-    const int n = 6 * nfree_;
-    size_t smem = sizeof(double) * (size_t)n * (n + 1) / 2;
-    SFM_CUDA(cudaFuncSetAttribute(k_dense_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max<size_t>(smem, 1)));
-  }
-  if (!use_dense_ && nfree_ > 0) {
-    const int cl = opt_.coarse_cluster == 0 ? 8 : opt_.coarse_cluster;
-    tm.mark("buffers");
-    pcg_.setup(nfree_, cl, opt_.coarse_refresh > 0 ? opt_.coarse_refresh : 8, s);
-    pcg_.set_pattern(row_ptr_.get(), col_idx_.get(), n_full_, s);
-  }
+  if (plan.valid()) plan.get();  // the PCG plan built on its own thread (rethrows its errors)
 
   tm.mark("terms + buffers + pcg plan");
   // all_fixed (solver.py:200-203) and the initial cost (solver.py:201)

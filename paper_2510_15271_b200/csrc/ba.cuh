@@ -65,6 +65,8 @@ class BASolver {
   cudaStream_t stream_;
   cudaStream_t side_ = nullptr;          // setup: bulk H2D copies overlapped with the structure build
   cudaEvent_t side_ready_ = nullptr, side_done_ = nullptr;
+  cudaStream_t plan_stream_ = nullptr;   // setup: the PCG plan's copies, on its own host thread
+  cudaEvent_t plan_ev_ = nullptr;
   Profiler* prof_;
   Comm* comm_;
   sfm_ba_options opt_{};

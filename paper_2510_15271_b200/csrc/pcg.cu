@@ -1248,7 +1248,7 @@ void TwoLevelPcg::set_pattern(const int* row_ptr, const int* col, int nnzb, cuda
     // coarse assembly runs (row i, k0, k1) grouped by coarse pair (c(i), d),
     // rows ascending inside a pair (stable sort of the row-ordered runs)
     std::vector<std::array<int, 4>> rr;  // (pair key, i, k0, k1)
-    rr.reserve((size_t)nf_ * 8);
+    rr.reserve((size_t)nnzb / 4 + 16);
     for (int i = 0; i < nf_; ++i) {
       int k = rp[i];
       while (k < rp[i + 1]) {
