@@ -800,6 +800,9 @@ __global__ void __launch_bounds__(kPcgMaxThreads, 1) k_pcg3(Pcg3Args a) {
   __shared__ double tmp[16];
   __shared__ double e[6];
   __shared__ double sums[4];
+  __shared__ double rr_ck[2];  // stagnation test references (sums_and_zc)
+  constexpr int kStagWin = 50;
+  if (threadIdx.x == 0) { rr_ck[0] = INFINITY; rr_ck[1] = INFINITY; }
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int G = gridDim.x;
   const int row0 = a.cta_row0[blockIdx.x], row1 = a.cta_row0[blockIdx.x + 1];
@@ -817,12 +820,30 @@ __global__ void __launch_bounds__(kPcgMaxThreads, 1) k_pcg3(Pcg3Args a) {
   };
   // After the r.z / r.r barrier: the scalar sums (warps 0..nsum-1) and the
   // next SpMV's z cache (the other warps) in one L2 round trip.
-  auto sums_and_zc = [&](const double* part, int nsum) {
+  // Stagnation test (itn > 0, the loop's r.z / r.r sums): at a nearly
+  // converged LM state rtol * |b| can be below what fp64 S x resolves, and CG
+  // then wanders at the rounding floor until max_it.  Every kStagWin
+  // iterations, if |r|^2 is not below 1/4 of its value kStagWin iterations
+  // earlier, sums[2] tells every thread to stop.  One thread owns the test
+  // (rr_ck alternates read / write slots), and sums[] is read after the
+  // barrier below, so all threads of all CTAs stop at the same iteration.
+  auto sums_and_zc = [&](const double* part, int nsum, int itn) {
     if (warp < nsum) {
       double sacc = 0.0;
       sacc = lane_partial_sum(part + warp * G, G, lane);
       sacc = warp_sum(sacc);
-      if (lane == 0) sums[warp] = sacc;
+      if (lane == 0) {
+        sums[warp] = sacc;
+        if (warp == 1) {
+          double stop = 0.0;
+          if (itn > 0 && itn % kStagWin == 0) {
+            const int slot = (itn / kStagWin) & 1;
+            stop = sacc > 0.25 * rr_ck[slot] ? 1.0 : 0.0;
+            rr_ck[slot ^ 1] = sacc;
+          }
+          sums[2] = stop;
+        }
+      }
     }
     if (a.fuse_zc) fill_zc(32 * nsum);
     __syncthreads();
@@ -942,7 +963,7 @@ __global__ void __launch_bounds__(kPcgMaxThreads, 1) k_pcg3(Pcg3Args a) {
   double2 s1 = block_sum2(rz_l, 0.0, red);
   if (threadIdx.x == 0) part_rz[blockIdx.x] = s1.x;
   grid.sync();
-  sums_and_zc(part_rz, 1);
+  sums_and_zc(part_rz, 1, 0);
   double rz_old = sums[0];
   int it = 0, fail = 0;
   double beta = 0.0;
@@ -1011,12 +1032,13 @@ __global__ void __launch_bounds__(kPcgMaxThreads, 1) k_pcg3(Pcg3Args a) {
       PH(5);
       grid.sync();
       PH(6);
-      sums_and_zc(part_rz, 2);
+      sums_and_zc(part_rz, 2, it + 1);
       PH(7);
       const double rz_new = sums[0], rr = sums[1];
       ++it;
       if (!isfinite(rr) || !isfinite(rz_new)) { fail = 1; break; }
       if (sqrt(rr) <= a.rtol * bnorm) break;
+      if (sums[2] != 0.0) break;  // stagnated at the rounding floor (sums_and_zc)
       beta = rz_new / rz_old;
       rz_old = rz_new;
     }
