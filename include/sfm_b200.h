@@ -25,7 +25,7 @@
 extern "C" {
 #endif
 
-#define SFM_ABI_VERSION 3
+#define SFM_ABI_VERSION 4
 
 /* ---- error codes (mapped to sfmkit.errors classes by the Python layer) --- */
 #define SFM_OK 0
@@ -135,6 +135,10 @@ typedef struct {
                                  default 8, < 0 = block-Jacobi only)       */
   int32_t coarse_refresh;     /* rebuild the coarse operator every this many
                                  linearisations (0 = default 8)            */
+  double coarse_max_lambda;   /* coarse level only while lambda <= this
+                                 (0 = default 1e-2; above it block-Jacobi)  */
+  double coarse_drift;        /* re-assemble A_c when lambda moved by more
+                                 than this factor since (0 = default 4)    */
 } sfm_ba_options;
 
 /* SolverReport (solver.py:90-95) + device-side statistics. */
@@ -149,6 +153,9 @@ typedef struct {
   double device_ms;           /* CUDA-event time of the LM loop            */
   int64_t kernel_launches;    /* kernels launched during the call          */
   int64_t n_blocks_S;         /* stored 6x6 blocks of S (both triangles)   */
+  int32_t pcg_stagnated;      /* PCG solves stopped at the rounding floor
+                                 (within 100x of the tolerance, no progress) */
+  int32_t pcg_max_hit;        /* PCG solves that ran into pcg_max_iters    */
 } sfm_ba_report;
 
 /* ---- context ------------------------------------------------------------ */

@@ -17,7 +17,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libsfm_b200.so")
 
 # ---- constants (mirror include/sfm_b200.h) ---------------------------------
-ABI_VERSION = 3
+ABI_VERSION = 4
 SFM_OK = 0
 SFM_E_INVALID = -1
 SFM_E_NON_POSITIVE_DEPTH = -2
@@ -87,7 +87,8 @@ class BAOptionsC(ctypes.Structure):
                 ("max_lambda", ctypes.c_double), ("linear_solver", ctypes.c_int32),
                 ("pcg_max_iters", ctypes.c_int32), ("pcg_rtol", ctypes.c_double),
                 ("dense_max_dim", ctypes.c_int32), ("coarse_cluster", ctypes.c_int32),
-                ("coarse_refresh", ctypes.c_int32)]
+                ("coarse_refresh", ctypes.c_int32), ("coarse_max_lambda", ctypes.c_double),
+                ("coarse_drift", ctypes.c_double)]
 
 
 class BAReportC(ctypes.Structure):
@@ -95,7 +96,8 @@ class BAReportC(ctypes.Structure):
                 ("iterations", ctypes.c_int32), ("termination", ctypes.c_int32),
                 ("n_trials", ctypes.c_int32), ("pcg_iterations", ctypes.c_int32),
                 ("final_lambda", ctypes.c_double), ("device_ms", ctypes.c_double),
-                ("kernel_launches", ctypes.c_int64), ("n_blocks_S", ctypes.c_int64)]
+                ("kernel_launches", ctypes.c_int64), ("n_blocks_S", ctypes.c_int64),
+                ("pcg_stagnated", ctypes.c_int32), ("pcg_max_hit", ctypes.c_int32)]
 
 
 class TracksC(ctypes.Structure):

@@ -1280,7 +1280,7 @@ __global__ void k_reset_scalars(BAScalars* sc, int full) {
   sc->depth_obs = ~0ull;
   sc->gmax = 0ull;
   sc->pcg_fail = 0;
-  if (full) sc->pcg_iters = 0;
+  if (full) { sc->pcg_iters = 0; sc->pcg_stop = 0; }
 }
 
 // Locates the projection failure of one observation (message payload).
@@ -1693,6 +1693,8 @@ void BASolver::setup(const sfm_ba_problem& pr, const sfm_ba_options& opt) {
       alloc_stream() = ps;  // the plan's buffers are stream-ordered on the plan stream
       SFM_CUDA(cudaStreamWaitEvent(ps, pe, 0));
       pcg_.setup(nfree_, cl, refresh, ps);
+      pcg_.set_coarse_policy(opt_.coarse_max_lambda > 0.0 ? opt_.coarse_max_lambda : 1e-2,
+                             opt_.coarse_drift > 1.0 ? opt_.coarse_drift : 4.0);
       pcg_.set_pattern(row_ptr_.get(), col_idx_.get(), n_full_, ps);  // ends with a sync of ps
     });
   }
@@ -1802,6 +1804,8 @@ void BASolver::setup(const sfm_ba_problem& pr, const sfm_ba_options& opt) {
   iters_ = 0;
   n_trials_ = 0;
   pcg_total_ = 0;
+  pcg_stagnated_ = 0;
+  pcg_max_hit_ = 0;
   term_ = SFM_TERM_MAX_ITERATIONS;
   lam_ = opt_.initial_lambda;
   initial_cost_ = eval_cost_current();
@@ -1995,7 +1999,7 @@ void BASolver::build_schur(double lam) {
   }
 }
 
-bool BASolver::solve_reduced() {
+bool BASolver::solve_reduced(double lam) {
   cudaStream_t s = stream_;
   if (nfree_ == 0) return true;
   if (use_dense_) {
@@ -2007,7 +2011,7 @@ bool BASolver::solve_reduced() {
   }
   PcgProblem pp{};
   pp.nf = nfree_; pp.row_ptr = row_ptr_.get(); pp.col = col_idx_.get(); pp.S = S_.get(); pp.nnzb = n_full_;
-  pp.diag_pos = diag_pos_.get(); pp.b = b_.get(); pp.x = dc_.get();
+  pp.diag_pos = diag_pos_.get(); pp.b = b_.get(); pp.x = dc_.get(); pp.lam = lam;
   pcg_.solve(pp, opt_.pcg_max_iters > 0 ? opt_.pcg_max_iters : 1000, opt_.pcg_rtol > 0 ? opt_.pcg_rtol : 1e-10,
              sc_.get(), s, prof_);
   return true;
@@ -2021,7 +2025,7 @@ bool BASolver::trial(double lam, double* new_cost, double* step_norm) {
   k_reset_scalars<<<1, 1, 0, s>>>(sc_.get(), 1);
   SFM_CHECK_LAUNCH();
   build_schur(lam);
-  solve_reduced();
+  solve_reduced(lam);
   const int o = cur_ ^ 1;
   const unsigned gd = grid_for(std::max(nfree_, 1), kBlock);
   if (nfree_) {
@@ -2060,6 +2064,10 @@ bool BASolver::trial(double lam, double* new_cost, double* step_norm) {
   }
   read_scalars();
   pcg_total_ += h_sc_.pcg_iters;
+  if (!use_dense_ && nfree_) {
+    pcg_stagnated_ += h_sc_.pcg_stop == PCG_STOP_STAGNATED;
+    pcg_max_hit_ += h_sc_.pcg_stop == PCG_STOP_MAX_ITERS;
+  }
   if (!use_dense_ && nfree_)  // S read + 7 length-6nf vectors touched per PCG iteration
     prof_->add_bytes("pcg", (double)h_sc_.pcg_iters * (288.0 * n_full_ + 7.0 * 48.0 * nfree_));
   if (h_sc_.nonfinite) return false;
@@ -2092,7 +2100,11 @@ void BASolver::iterate(int n, sfm_ba_report* rep) {
     while (lam_ <= opt_.max_lambda) {  // solver.py:219-245
       double nc = 0.0, sn = 0.0;
       ++n_trials_;
-      if (!trial(lam_, &nc, &sn)) {
+      const bool ok = trial(lam_, &nc, &sn);
+      if (trace_)
+        std::fprintf(stderr, "[sfm trial] it=%d lam=%.3e pcg=%d stop=%d ok=%d cost=%.17g cur=%.17g acc=%d\n", iters_, lam_,
+                     h_sc_.pcg_iters, h_sc_.pcg_stop, (int)ok, nc, cost_, (int)(ok && std::isfinite(nc) && nc < cost_));
+      if (!ok) {
         lam_ *= 10.0;
         continue;
       }
@@ -2143,6 +2155,8 @@ void BASolver::iterate(int n, sfm_ba_report* rep) {
     rep->device_ms = ms;
     rep->kernel_launches = prof_->launches - launches0;
     rep->n_blocks_S = n_full_;
+    rep->pcg_stagnated = pcg_stagnated_;
+    rep->pcg_max_hit = pcg_max_hit_;
   }
 }
 

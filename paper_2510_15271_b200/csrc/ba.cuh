@@ -32,6 +32,7 @@ struct BAScalars {
   int nonfinite;             // delta or Schur factor not finite / not PD
   int pcg_iters;
   int pcg_fail;
+  int pcg_stop;              // PCG_STOP_* of the last solve
   int proj_code;             // PROJ_* code of depth_obs (filled on demand)
   double proj_depth;         // p_cam.z of depth_obs
 };
@@ -57,7 +58,7 @@ class BASolver {
   void linearize();
   bool trial(double lam, double* new_cost, double* step_norm);
   void build_schur(double lam);
-  bool solve_reduced();
+  bool solve_reduced(double lam);
   void raise_projection_error(bool trial_state);
   void read_scalars();
   BlkArgs blk_args(double lam) const;
@@ -85,7 +86,9 @@ class BASolver {
   bool finished_ = true;
   double initial_cost_ = 0.0, cost_ = 0.0, lam_ = 0.0;
   int iters_ = 0, term_ = SFM_TERM_MAX_ITERATIONS, n_trials_ = 0, pcg_total_ = 0;
+  int pcg_stagnated_ = 0, pcg_max_hit_ = 0;
   int use_dense_ = 0;
+  bool trace_ = std::getenv("SFM_TRACE") != nullptr;
 
   // frames / models
   DevBuf<sfm_camera_model> models_;

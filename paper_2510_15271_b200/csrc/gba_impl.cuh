@@ -839,7 +839,7 @@ bool GBASolver::trial(double lam, double* new_cost, double* step_norm) {
     } else {
       PcgProblem pp{};
       pp.nf = nf_; pp.row_ptr = row_ptr_.get(); pp.col = col_.get(); pp.S = S_.get(); pp.nnzb = n_full_;
-      pp.diag_pos = diag_pos_.get(); pp.b = b_.get(); pp.x = dc_.get();
+      pp.diag_pos = diag_pos_.get(); pp.b = b_.get(); pp.x = dc_.get(); pp.lam = lam;
       pcg_.solve(pp, opt_.pcg_max_iters > 0 ? opt_.pcg_max_iters : 1000, opt_.pcg_rtol > 0 ? opt_.pcg_rtol : 1e-10,
                  sc_.get(), s, prof_);
     }

@@ -454,6 +454,7 @@ struct Pcg3Args {
   double rtol;
   int fuse_zc;
   int warm;                // start from the energy-optimal multiple of the previous solution
+  double stag_slack;       // stagnation stop only once |r| <= stag_slack * rtol * |b|
 };
 
 __device__ __forceinline__ double warp_sum(double v) {
@@ -824,9 +825,13 @@ __global__ void __launch_bounds__(kPcgMaxThreads, 1) k_pcg3(Pcg3Args a) {
   // converged LM state rtol * |b| can be below what fp64 S x resolves, and CG
   // then wanders at the rounding floor until max_it.  Every kStagWin
   // iterations, if |r|^2 is not below 1/4 of its value kStagWin iterations
-  // earlier, sums[2] tells every thread to stop.  One thread owns the test
-  // (rr_ck alternates read / write slots), and sums[] is read after the
-  // barrier below, so all threads of all CTAs stop at the same iteration.
+  // earlier AND |r| is already within stag_slack of the target (so a slow but
+  // progressing solve far from the target is never cut short), sums[2] tells
+  // every thread to stop.  One thread owns the test (rr_ck alternates read /
+  // write slots), and sums[] is read after the barrier below, so all threads
+  // of all CTAs stop at the same iteration.  The stop is reported
+  // (PCG_STOP_STAGNATED) so the host can count it.
+  double stag_rr = 0.0;  // set once |b| is known
   auto sums_and_zc = [&](const double* part, int nsum, int itn) {
     if (warp < nsum) {
       double sacc = 0.0;
@@ -838,7 +843,7 @@ __global__ void __launch_bounds__(kPcgMaxThreads, 1) k_pcg3(Pcg3Args a) {
           double stop = 0.0;
           if (itn > 0 && itn % kStagWin == 0) {
             const int slot = (itn / kStagWin) & 1;
-            stop = sacc > 0.25 * rr_ck[slot] ? 1.0 : 0.0;
+            stop = (sacc > 0.25 * rr_ck[slot] && sacc <= stag_rr) ? 1.0 : 0.0;
             rr_ck[slot ^ 1] = sacc;
           }
           sums[2] = stop;
@@ -949,6 +954,7 @@ __global__ void __launch_bounds__(kPcgMaxThreads, 1) k_pcg3(Pcg3Args a) {
   grid.sync();
   gather_after_sync(a, part_bb, sums, 1, m.rc, two, true, nullptr, nullptr, m.cc0);
   const double bnorm = sqrt(sums[0]);
+  stag_rr = (a.stag_slack * a.rtol * bnorm) * (a.stag_slack * a.rtol * bnorm);
   if (two) coarse_apply(a, m, e, tmp);
   double rz_l = 0.0;
   for (int i = warp; i < nrows; i += kPcgWarps) {
@@ -965,10 +971,11 @@ __global__ void __launch_bounds__(kPcgMaxThreads, 1) k_pcg3(Pcg3Args a) {
   grid.sync();
   sums_and_zc(part_rz, 1, 0);
   double rz_old = sums[0];
-  int it = 0, fail = 0;
+  int it = 0, fail = 0, stop = PCG_STOP_MAX_ITERS;
   double beta = 0.0;
   if (!(bnorm > 0.0) || !isfinite(bnorm)) {
     fail = !isfinite(bnorm);
+    stop = PCG_STOP_CONVERGED;  // b = 0: x = 0 is exact
   } else {
     PH_INIT();
     for (it = 0; it < a.max_it;) {
@@ -1037,8 +1044,8 @@ __global__ void __launch_bounds__(kPcgMaxThreads, 1) k_pcg3(Pcg3Args a) {
       const double rz_new = sums[0], rr = sums[1];
       ++it;
       if (!isfinite(rr) || !isfinite(rz_new)) { fail = 1; break; }
-      if (sqrt(rr) <= a.rtol * bnorm) break;
-      if (sums[2] != 0.0) break;  // stagnated at the rounding floor (sums_and_zc)
+      if (sqrt(rr) <= a.rtol * bnorm) { stop = PCG_STOP_CONVERGED; break; }
+      if (sums[2] != 0.0) { stop = PCG_STOP_STAGNATED; break; }  // at the rounding floor (sums_and_zc)
       beta = rz_new / rz_old;
       rz_old = rz_new;
     }
@@ -1049,6 +1056,7 @@ __global__ void __launch_bounds__(kPcgMaxThreads, 1) k_pcg3(Pcg3Args a) {
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     a.sc->pcg_iters = it;
     a.sc->pcg_fail = fail;
+    a.sc->pcg_stop = fail ? PCG_STOP_FAILED : stop;
     if (fail) a.sc->nonfinite = 1;
   }
 }
@@ -1097,6 +1105,8 @@ void TwoLevelPcg::set_pattern(const int* row_ptr, const int* col, int nnzb, cuda
   }
   const int nwarps = nt_ / 32;
   if (const char* e = std::getenv("SFM_COARSE_REFRESH")) refresh_ = std::max(1, std::atoi(e));
+  if (const char* e = std::getenv("SFM_COARSE_LAMMAX")) lam_max_ = std::atof(e);
+  if (const char* e = std::getenv("SFM_COARSE_DRIFT")) drift_ = std::max(1.0, std::atof(e));
   lin_count_ = 0;
   have_prev_ = false;
   warm_ = true;
@@ -1335,10 +1345,27 @@ void TwoLevelPcg::solve(const PcgProblem& p, int max_it, double rtol, BAScalars*
     ProfScope ps(*prof, "block_jacobi", 0.0, s);
     k_block_jacobi<<<grid_for(nf_, 64), 64, 0, s>>>(nf_, p.diag_pos, p.S, Minv_.get(), sc);
   }
-  // The coarse operator is rebuilt once per linearisation (first trial);
-  // later damping trials reuse it -- any SPD coarse operator is a valid
-  // preconditioner, and lambda only rescales the diagonal.
-  if (gj_grid_ > 0 && !coarse_valid_) {
+  // The coarse operator A_c = P^T S(lam) P depends on the damping: S(lam)
+  // has lam*D_c on its diagonal and (V + lam D_p)^-1 in its point term.  An
+  // A_c assembled at lam_b and applied at lam >> lam_b over-weights the
+  // coarse correction P A_c^-1 P^T by up to lam/lam_b on the rigid-motion
+  // directions (and under-weights it for lam << lam_b), which wrecks the
+  // conditioning of the preconditioned system -- the rejected-trial tail of
+  // an LM solve climbs lam by 10x per trial up to 1e32.  So:
+  //   * lam > lam_max_: no coarse level.  There the damping makes S
+  //     block-diagonally dominant and block-Jacobi alone converges in a few
+  //     iterations;
+  //   * otherwise A_c is re-assembled and re-inverted whenever lam has moved
+  //     by more than drift_ (either way) from the lam it was built at, or the
+  //     basis was refreshed (set_basis).
+  const bool coarse_on = gj_grid_ > 0 && p.lam <= lam_max_;
+  bool stale = !coarse_valid_;
+  if (coarse_on && !stale) {
+    const double ratio = (lam_build_ > 0.0 && p.lam > 0.0) ? p.lam / lam_build_ : (p.lam == lam_build_ ? 1.0 : 1e300);
+    stale = ratio > drift_ || ratio * drift_ < 1.0;
+  }
+  if (coarse_on && stale) {
+    lam_build_ = p.lam;
     {
       ProfScope ps(*prof, "coarse_assemble", 288.0 * p.nnzb, s);
       SFM_CUDA(cudaMemsetAsync(Ac_[0].get(), 0, sizeof(double) * (size_t)npad_ * npad_, s));
@@ -1364,7 +1391,8 @@ void TwoLevelPcg::solve(const PcgProblem& p, int max_it, double rtol, BAScalars*
   Pcg3Args a{};
   a.nf = nf_; a.G = grid_; a.nc = nc_; a.npad = npad_; a.maxrows = maxrows_; a.maxsegs = maxsegs_;
   a.row_ptr = p.row_ptr; a.col = p.col; a.S = p.S; a.Minv = Minv_.get(); a.Pm = Pm_.get();
-  a.Aci = gj_grid_ > 0 ? Aci_ : nullptr;
+  a.Aci = coarse_on ? Aci_ : nullptr;
+  a.stag_slack = 100.0;
   a.cta_row0 = cta_row0_.get(); a.wchunk = wchunk_.get();
   a.wres = wres_.get(); a.resblocks = resblocks_;
   a.lcol = lcol_.get(); a.zl_ptr = zl_ptr_.get(); a.zl = zl_.get(); a.maxblk = maxblk_; a.maxdist = maxdist_; a.rowseg = rowseg_.get();

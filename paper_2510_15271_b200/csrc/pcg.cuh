@@ -18,6 +18,9 @@ namespace sfm {
 
 struct BAScalars;
 
+// Why a PCG solve stopped (BAScalars::pcg_stop).
+enum { PCG_STOP_CONVERGED = 0, PCG_STOP_MAX_ITERS = 1, PCG_STOP_STAGNATED = 2, PCG_STOP_FAILED = 3 };
+
 struct PcgProblem {
   int nf;
   const int* row_ptr;     // BSR (both triangles), [nf+1]
@@ -27,6 +30,7 @@ struct PcgProblem {
   const int* diag_pos;    // [nf] BSR slot of the diagonal block
   const double* b;        // [nf*6]
   double* x;              // [nf*6] solution
+  double lam;             // Marquardt damping S was assembled at (coarse-level consistency)
 };
 
 class TwoLevelPcg {
@@ -38,7 +42,10 @@ class TwoLevelPcg {
   // Coarse basis P_j = Adj(T_j) from the linearisation-point poses.
   void set_basis(const int* free_frame, const double* q, const double* t, const double* Rt,
                  cudaStream_t s, Profiler* prof);
-  // Solves S x = b; writes iteration count / failure into sc.
+  // Coarse level only while lam <= lam_max; rebuilt when lam has drifted by
+  // more than `drift` (either way) from the lam it was assembled at.
+  void set_coarse_policy(double lam_max, double drift) { lam_max_ = lam_max; drift_ = drift; }
+  // Solves S x = b; writes iteration count / stop reason / failure into sc.
   void solve(const PcgProblem& p, int max_it, double rtol, BAScalars* sc, cudaStream_t s,
              Profiler* prof);
   int last_grid() const { return grid_; }
@@ -49,6 +56,7 @@ class TwoLevelPcg {
   size_t smem_ = 0;
   int npairs_ = 0;
   bool coarse_valid_ = false;
+  double lam_build_ = 0.0, lam_max_ = 1e-2, drift_ = 4.0;
   bool have_prev_ = false, warm_ = true;  // warm start from the previous solution
   const double* Aci_ = nullptr;
   DevBuf<double> Minv_, Pm_, Ac_[2], gjpiv_, r_, z_, p_, q_, rpart_, part_;

@@ -217,7 +217,8 @@ def _options(loss: RobustLoss, sopt: SolverOptions, dopt: DeviceOptions) -> nat.
                           float(sopt.grad_tol), float(sopt.param_tol), float(sopt.initial_lambda),
                           float(sopt.max_lambda), nat.LINSOLVE[dopt.linear_solver],
                           int(dopt.pcg_max_iters), float(dopt.pcg_rtol), int(dopt.dense_max_dim),
-                          int(dopt.coarse_cluster), int(dopt.coarse_refresh))
+                          int(dopt.coarse_cluster), int(dopt.coarse_refresh),
+                          float(dopt.coarse_max_lambda), float(dopt.coarse_drift))
 
 
 def solve_arrays(arrays: BAArrays, loss: RobustLoss = TRIVIAL_LOSS,

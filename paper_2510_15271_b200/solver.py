@@ -59,6 +59,8 @@ class DeviceOptions:
     dense_max_dim: int = 210
     coarse_cluster: int = 8      # frames per coarse cluster; < 0 = block-Jacobi only
     coarse_refresh: int = 8      # rebuild the coarse operator every N linearisations
+    coarse_max_lambda: float = 1e-2  # above this damping: block-Jacobi only (S is diagonally dominant)
+    coarse_drift: float = 4.0    # re-assemble A_c = P^T S(lambda) P when lambda moved by more than this
 
 
 DEFAULT_DEVICE_OPTIONS = DeviceOptions()
