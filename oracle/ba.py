@@ -210,15 +210,22 @@ class BAProblem:
     def point_schur_terms(self, lin, Vinv, e):
         """The points' share of the reduced system: -sum_i W V*_i^-1 W^T and
         sum_i W e_i.  Under point sharding each rank holds only its points'
-        share; the camera blocks are added once."""
+        share; the camera blocks are added once.  Pair
+        products are batched matmuls, summed per S block with bincount (a
+        different summation order than a sequential np.add.at: rounding-level
+        differences only)."""
         nf, W, j = self.nf, lin["W"], lin["j"]
-        S4 = np.zeros((nf, nf, 6, 6))
         a, b = self._pairs()
-        CH = 1 << 18
+        key = j[a] * nf + j[b]
+        acc = np.zeros((36, nf * nf))
+        CH = 1 << 20
         for s0 in range(0, len(a), CH):
-            aa, bb = a[s0:s0 + CH], b[s0:s0 + CH]
-            C = np.einsum("nij,njk,nlk->nil", W[aa], Vinv[self.op[aa]], W[bb])
-            np.add.at(S4, (j[aa], j[bb]), -C)
+            aa, bb, kk = a[s0:s0 + CH], b[s0:s0 + CH], key[s0:s0 + CH]
+            T = np.matmul(W[aa], Vinv[self.op[aa]])
+            C = np.matmul(T, np.transpose(W[bb], (0, 2, 1))).reshape(-1, 36)
+            for q in range(36):
+                acc[q] -= np.bincount(kk, weights=C[:, q], minlength=nf * nf)
+        S4 = acc.T.reshape(nf, nf, 6, 6)
         rhs = np.zeros((nf, 6))
         fr = j >= 0
         np.add.at(rhs, j[fr], np.einsum("nij,nj->ni", W[fr], e[self.op[fr]]))

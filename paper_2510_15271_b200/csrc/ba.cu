@@ -701,6 +701,15 @@ __device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, dou
 // edge block is added on rank 0 and both BSR triangles written.
 constexpr int kOffWarps = 4;
 constexpr int kOffLd = 13;  // padded row of the staged factors (bank spread)
+#ifndef SFM_OFF_V
+#define SFM_OFF_V 0
+#endif
+#if SFM_OFF_V == 1
+constexpr int kOffRows = 64;
+#else
+constexpr int kOffRows = 32;
+#endif
+constexpr size_t kOffSmem = sizeof(double) * kOffWarps * 2 * kOffRows * kOffLd;
 
 // One packed header per off-diagonal work item (structure build): the
 // kernel's prologue is then one independent load instead of the
@@ -730,12 +739,14 @@ __global__ void k_off_records(int n, const int* __restrict__ work, const unsigne
 #define SFM_CAM_MINB 5
 #endif
 __global__ void __launch_bounds__(kOffWarps * 32, SFM_OFF_MINB) k_offdiag_blocks(BlkArgs a) {
-  __shared__ double Ast[kOffWarps][32 * kOffLd];
-  __shared__ double Bst[kOffWarps][32 * kOffLd];
+  extern __shared__ double offsm[];  // per warp: A | B staged factors [kOffRows x kOffLd] each
+
   __shared__ Mat3 Rsm[kOffWarps][2];
   __shared__ sfm_camera_model Csm[kOffWarps][2];
   const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double* Aw = offsm + (size_t)warp * 2 * kOffRows * kOffLd;
+  double* Bw = Aw + kOffRows * kOffLd;
   if (w >= a.n) return;
   const int4 hd = __ldg(a.offrec + 2 * w);
   const int4 out = __ldg(a.offrec + 2 * w + 1);
@@ -759,9 +770,91 @@ __global__ void __launch_bounds__(kOffWarps * 32, SFM_OFF_MINB) k_offdiag_blocks
     const Mat3& Rb = Rsm[warp][1];
     const sfm_camera_model& ca = Csm[warp][0];
     const sfm_camera_model& cb = Csm[warp][1];
+#if SFM_OFF_V == 1
+    // 64 pairs per round (lanes take pairs kb + lane and kb + 32 + lane):
+    // both halves' gathers are issued together, and the next round's pair
+    // records are loaded before this round's factors are computed, so a
+    // round waits for one L2 round trip instead of two
     const int64_t k0 = kr.x, k1 = kr.y;
-    double* As = &Ast[warp][lane * kOffLd];
-    double* Bs = &Bst[warp][lane * kOffLd];
+    unsigned long long prA = 0, prB = 0;
+    int ptA = 0, ptB = 0;
+    if (k0 + lane < k1) { prA = __ldg(a.pairs + k0 + lane); ptA = __ldg(a.pair_pt + k0 + lane); }
+    if (k0 + 32 + lane < k1) { prB = __ldg(a.pairs + k0 + 32 + lane); ptB = __ldg(a.pair_pt + k0 + 32 + lane); }
+    auto stage = [&](double4 ga, double4 gb, double4 pva, double2 pvb, bool has, int row) {
+      double* As = &Aw[row * kOffLd];
+      double* Bs = &Bw[row * kOffLd];
+      if (!has) {
+#pragma unroll
+        for (int i = 0; i < 12; ++i) { As[i] = 0.0; Bs[i] = 0.0; }
+        return;
+      }
+      const double v0 = pva.x, v1 = pva.y, v2 = pva.z, v3_ = pva.w, v4 = pvb.x, v5 = pvb.y;
+      double Jca[12], Jpa[6];
+      geo_jacobians(ca, Ra, ga, Jca, Jpa);
+#pragma unroll
+      for (int i = 0; i < 12; ++i) As[i] = Jca[i];
+      double Jcb[12], Jpb[6];
+      geo_jacobians(cb, Rb, gb, Jcb, Jpb);
+      const double P00 = v0 * Jpb[0] + v1 * Jpb[1] + v2 * Jpb[2];
+      const double P01 = v1 * Jpb[0] + v3_ * Jpb[1] + v4 * Jpb[2];
+      const double P02 = v2 * Jpb[0] + v4 * Jpb[1] + v5 * Jpb[2];
+      const double P10 = v0 * Jpb[3] + v1 * Jpb[4] + v2 * Jpb[5];
+      const double P11 = v1 * Jpb[3] + v3_ * Jpb[4] + v4 * Jpb[5];
+      const double P12 = v2 * Jpb[3] + v4 * Jpb[4] + v5 * Jpb[5];
+      const double m00 = Jpa[0] * P00 + Jpa[1] * P01 + Jpa[2] * P02;
+      const double m01 = Jpa[0] * P10 + Jpa[1] * P11 + Jpa[2] * P12;
+      const double m10 = Jpa[3] * P00 + Jpa[4] * P01 + Jpa[5] * P02;
+      const double m11 = Jpa[3] * P10 + Jpa[4] * P11 + Jpa[5] * P12;
+#pragma unroll
+      for (int c = 0; c < 6; ++c) {
+        Bs[c] = -(m00 * Jcb[c] + m01 * Jcb[6 + c]);
+        Bs[6 + c] = -(m10 * Jcb[c] + m11 * Jcb[6 + c]);
+      }
+    };
+    for (int64_t kb = k0; kb < k1; kb += 64) {
+      const bool hasA = kb + lane < k1, hasB = kb + 32 + lane < k1;
+      double4 gaA = make_double4(0, 0, 0, 0), gbA = gaA, pvA = gaA, gaB = gaA, gbB = gaA, pvB = gaA;
+      double2 pwA = make_double2(0, 0), pwB = pwA;
+      if (hasA) {
+        gaA = ldg256(a.geo + (int64_t)(prA >> 32));
+        gbA = ldg256(a.geo + (int64_t)(uint32_t)prA);
+        pvA = ldg256(a.pv + (int64_t)ptA * 12);
+        pwA = __ldg(reinterpret_cast<const double2*>(a.pv + (int64_t)ptA * 12 + 4));
+      }
+      if (hasB) {
+        gaB = ldg256(a.geo + (int64_t)(prB >> 32));
+        gbB = ldg256(a.geo + (int64_t)(uint32_t)prB);
+        pvB = ldg256(a.pv + (int64_t)ptB * 12);
+        pwB = __ldg(reinterpret_cast<const double2*>(a.pv + (int64_t)ptB * 12 + 4));
+      }
+      {  // next round's pair records
+        const int64_t nA = kb + 64 + lane, nB = kb + 96 + lane;
+        if (nA < k1) { prA = __ldg(a.pairs + nA); ptA = __ldg(a.pair_pt + nA); }
+        if (nB < k1) { prB = __ldg(a.pairs + nB); ptB = __ldg(a.pair_pt + nB); }
+      }
+      stage(gaA, gbA, pvA, pwA, hasA, lane);
+      stage(gaB, gbB, pvB, pwB, hasB, 32 + lane);
+      __syncwarp();
+      const int nch = (int)((min((int64_t)64, k1 - kb) + 1) >> 1);
+      const int slot = (fk & 1) * 6 + fr;
+      for (int ch = 0; ch < nch; ch += 2) {
+        const int p0 = 2 * ch + (fk >> 1);
+        const double a0 = fr < 6 ? Aw[p0 * kOffLd + slot] : 0.0;
+        const double b0 = fr < 6 ? Bw[p0 * kOffLd + slot] : 0.0;
+        dmma_8x8x4(d0, d1, a0, b0);
+        if (ch + 1 < nch) {
+          const int p1 = p0 + 2;
+          const double a1 = fr < 6 ? Aw[p1 * kOffLd + slot] : 0.0;
+          const double b1 = fr < 6 ? Bw[p1 * kOffLd + slot] : 0.0;
+          dmma_8x8x4(e0, e1, a1, b1);
+        }
+      }
+      __syncwarp();
+    }
+#else
+    const int64_t k0 = kr.x, k1 = kr.y;
+    double* As = &Aw[lane * kOffLd];
+    double* Bs = &Bw[lane * kOffLd];
     for (int64_t kb = k0; kb < k1; kb += 32) {
       const int64_t k = kb + lane;
       if (k < k1) {
@@ -801,18 +894,19 @@ __global__ void __launch_bounds__(kOffWarps * 32, SFM_OFF_MINB) k_offdiag_blocks
       const int slot = (fk & 1) * 6 + fr;
       for (int ch = 0; ch < nch; ch += 2) {
         const int p0 = 2 * ch + (fk >> 1);
-        const double a0 = fr < 6 ? Ast[warp][p0 * kOffLd + slot] : 0.0;
-        const double b0 = fr < 6 ? Bst[warp][p0 * kOffLd + slot] : 0.0;
+        const double a0 = fr < 6 ? Aw[p0 * kOffLd + slot] : 0.0;
+        const double b0 = fr < 6 ? Bw[p0 * kOffLd + slot] : 0.0;
         dmma_8x8x4(d0, d1, a0, b0);
         if (ch + 1 < nch) {
           const int p1 = p0 + 2;
-          const double a1 = fr < 6 ? Ast[warp][p1 * kOffLd + slot] : 0.0;
-          const double b1 = fr < 6 ? Bst[warp][p1 * kOffLd + slot] : 0.0;
+          const double a1 = fr < 6 ? Aw[p1 * kOffLd + slot] : 0.0;
+          const double b1 = fr < 6 ? Bw[p1 * kOffLd + slot] : 0.0;
           dmma_8x8x4(e0, e1, a1, b1);
         }
       }
       __syncwarp();
     }
+#endif
   }
   d0 += e0;
   d1 += e1;
@@ -986,6 +1080,8 @@ __global__ void __launch_bounds__(kCamWarps * 32, SFM_CAM_MINB) k_cam_blocks(Blk
   if (lane < 4) up[32 + lane] = s1;
   else if (lane < 10) a.b[j * 6 + lane - 4] = s1;
 }
+
+#include "ischur.cuh"
 
 // Camera-major observation streams (built once per bundle_adjust): the
 // diagonal pair blocks already hold each free camera's observations in point
@@ -1670,6 +1766,7 @@ void BASolver::setup(const sfm_ba_problem& pr, const sfm_ba_options& opt) {
   } else {
     use_dense_ = (6 * nfree_ <= dense_cap) ? 1 : 0;
   }
+  SFM_CUDA(cudaFuncSetAttribute(k_offdiag_blocks, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kOffSmem));
   if (use_dense_ && nfree_ > 0) {
     const int n = 6 * nfree_;
     size_t smem = sizeof(double) * (size_t)n * (n + 1) / 2;
@@ -1888,6 +1985,7 @@ double BASolver::eval_cost_current() {
 
 void BASolver::linearize() {
   cudaStream_t s = stream_;
+  last_pcg_ = -1;
   k_reset_scalars<<<1, 1, 0, s>>>(sc_.get(), 0);
   SFM_CHECK_LAUNCH();
   PointArgs pa{};
@@ -1968,14 +2066,25 @@ BlkArgs BASolver::blk_args(double lam) const {
   return ba;
 }
 
-void BASolver::build_schur(double lam) {
+// V*^-1 and e per point for this trial's lambda (skipped when k_point_lin
+// already prepared them for it).
+void BASolver::point_prep(double lam) {
   cudaStream_t s = stream_;
+  if (prep_done_lam_ == lam) return;
   const bool prepped = prep_ready_ && lam == prep_lam_ && nfree_ > 0;
   prep_ready_ = false;
+  prep_folded_ = prepped;
   if (P_ && !prepped) {
     ProfScope ps(*prof_, "point_prep", 72.0 * P_ + 96.0 * P_, s);
     k_point_prep<<<grid_for(P_, 256), 256, 0, s>>>(P_, lam, V_.get(), gp_.get(), pv_.get(), sc_.get());
   }
+  prep_done_lam_ = lam;
+}
+
+void BASolver::build_schur(double lam) {
+  cudaStream_t s = stream_;
+  point_prep(lam);
+  const bool prepped = prep_folded_;
   if (nfree_) {
     BlkArgs ba = blk_args(lam);
     ba.pre = prepped ? sc_pre_.get() : nullptr;
@@ -1991,7 +2100,7 @@ void BASolver::build_schur(double lam) {
     // observation records, point V*^-1 once; both triangles of S out
     ProfScope ps(*prof_, "schur_offdiag",
                  12.0 * (n_pairs_ - n_cm_) + 32.0 * N_ + 48.0 * P_ + 288.0 * (n_full_ - nfree_), s);
-    k_offdiag_blocks<<<grid_for((int64_t)n_off_ * 32, kOffWarps * 32), kOffWarps * 32, 0, s>>>(ba);
+    k_offdiag_blocks<<<grid_for((int64_t)n_off_ * 32, kOffWarps * 32), kOffWarps * 32, kOffSmem, s>>>(ba);
   }
   if (comm_ && comm_->active()) {
     comm_->sum(S_.get(), (size_t)n_full_ * 36, s);
@@ -2017,6 +2126,62 @@ bool BASolver::solve_reduced(double lam) {
   return true;
 }
 
+bool BASolver::solve_implicit(double lam) {
+  cudaStream_t s = stream_;
+  const int n = 6 * nfree_;
+  imp_s_.resize((size_t)P_ * 3);
+  imp_r_.resize(n); imp_z_.resize(n); imp_p_.resize(n); imp_q_.resize(n); imp_b_.resize(n);
+  imp_M_.resize((size_t)nfree_ * 36);
+  imp_st_.resize(1);
+  SFM_CUDA(cudaMemsetAsync(imp_st_.get(), 0, sizeof(ImpState), s));
+  const double rtol = opt_.pcg_rtol > 0 ? opt_.pcg_rtol : 1e-10;
+  ImpCamArgs ca{};
+  ca.nf = nfree_; ca.rank = rank_; ca.lam = lam; ca.free_frame = free_frame_.get();
+  ca.frame_model = frame_model_.get(); ca.models = models_.get(); ca.Rt = Rt_[cur_].get();
+  ca.cm_ptr = cm_ptr_.get(); ca.cm_pt = cm_pt_.get(); ca.geo_cm = geo_cm_.get();
+  ca.U = U_.get(); ca.Dc = Dc_.get(); ca.gc = gc_.get(); ca.term_ptr = term_ptr_.get();
+  ca.term_list = term_list_.get(); ca.E = n_edges_; ca.edge_ab = edge_ab_.get(); ca.free_idx = free_idx_.get();
+  ca.edge_H = edge_H_.get(); ca.st = imp_st_.get();
+  {  // b = -g_c + sum_a W_a e_i
+    ProfScope ps(*prof_, "imp_cam", 36.0 * n_cm_ + 24.0 * P_ + 96.0 * nfree_, s);
+    ca.mode = 0; ca.v = pv_.get(); ca.vstride = 12; ca.voff = 6; ca.pvec = nullptr; ca.out = imp_b_.get();
+    k_imp_cam<<<nfree_, kImpWarps * 32, 0, s>>>(ca);
+  }
+  {
+    ProfScope ps(*prof_, "imp_update", 0.0, s);
+    k_imp_precond<<<grid_for(nfree_, 64), 64, 0, s>>>(nfree_, U_.get(), Dc_.get(), lam, imp_M_.get(), imp_st_.get());
+    k_imp_init<<<1, 1024, 0, s>>>(n, imp_b_.get(), imp_M_.get(), dc_.get(), imp_r_.get(), imp_z_.get(),
+                                  imp_p_.get(), imp_st_.get());
+  }
+  constexpr int kChunk = 4, kMaxIt = 12;
+  ImpState h{};
+  for (int done_it = 0; done_it < kMaxIt; done_it += kChunk) {
+    for (int k = 0; k < kChunk; ++k) {
+      {
+        ProfScope ps(*prof_, "imp_point", 36.0 * N_ + 136.0 * P_, s);
+        k_imp_point<<<grid_for(std::max<int64_t>(P_, 1), kBlock), kBlock, 0, s>>>(
+            P_, pt_ptr_.get(), obs_frame_.get(), free_idx_.get(), frame_model_.get(), models_.get(), nmodels_,
+            Rt_[cur_].get(), geo_.get(), pv_.get(), imp_p_.get(), imp_s_.get(), imp_st_.get());
+      }
+      {
+        ProfScope ps(*prof_, "imp_cam", 60.0 * n_cm_ + 96.0 * nfree_, s);
+        ca.mode = 1; ca.v = imp_s_.get(); ca.vstride = 3; ca.voff = 0; ca.pvec = imp_p_.get(); ca.out = imp_q_.get();
+        k_imp_cam<<<nfree_, kImpWarps * 32, 0, s>>>(ca);
+      }
+      {
+        ProfScope ps(*prof_, "imp_update", 0.0, s);
+        k_imp_step<<<1, 1024, 0, s>>>(n, imp_q_.get(), imp_M_.get(), rtol, kMaxIt, dc_.get(), imp_r_.get(),
+                                      imp_z_.get(), imp_p_.get(), imp_st_.get());
+      }
+    }
+    imp_st_.download(&h, 1, s);
+    SFM_CUDA(cudaStreamSynchronize(s));
+    if (h.done) break;
+  }
+  imp_iters_ = h.it;
+  return h.done == 1;
+}
+
 // One LM trial at damping lam (solver.py:220-235).  Returns false when the
 // step is not finite (the reference then multiplies lambda by 10 without
 // evaluating the cost).
@@ -2024,8 +2189,22 @@ bool BASolver::trial(double lam, double* new_cost, double* step_norm) {
   cudaStream_t s = stream_;
   k_reset_scalars<<<1, 1, 0, s>>>(sc_.get(), 1);
   SFM_CHECK_LAUNCH();
-  build_schur(lam);
-  solve_reduced(lam);
+  prep_done_lam_ = -1.0;
+  // Matrix-free Schur PCG when the previous trial of this linearisation
+  // needed at most 3 PCG iterations (S strongly diagonally dominant at this
+  // damping); the explicit S otherwise, or if it does not converge.
+  const bool try_imp = imp_enabled_ && !use_dense_ && nfree_ > 0 && !(comm_ && comm_->active()) &&
+                       last_pcg_ >= 0 && last_pcg_ <= 3 && !(prep_ready_ && lam == prep_lam_);
+  bool imp_ok = false;
+  if (try_imp) {
+    point_prep(lam);
+    imp_ok = solve_implicit(lam);
+    ++imp_trials_;
+  }
+  if (!imp_ok) {
+    build_schur(lam);
+    solve_reduced(lam);
+  }
   const int o = cur_ ^ 1;
   const unsigned gd = grid_for(std::max(nfree_, 1), kBlock);
   if (nfree_) {
@@ -2063,13 +2242,21 @@ bool BASolver::trial(double lam, double* new_cost, double* step_norm) {
     comm_->max_i32(&sc_.get()->nonfinite, 1, s);
   }
   read_scalars();
+  if (imp_ok) {
+    h_sc_.pcg_iters = imp_iters_;
+    h_sc_.pcg_stop = PCG_STOP_CONVERGED;
+  } else if (try_imp) {
+    h_sc_.pcg_iters += imp_iters_;
+  }
+  last_pcg_ = use_dense_ ? -1 : h_sc_.pcg_iters;
   pcg_total_ += h_sc_.pcg_iters;
   if (!use_dense_ && nfree_) {
     pcg_stagnated_ += h_sc_.pcg_stop == PCG_STOP_STAGNATED;
     pcg_max_hit_ += h_sc_.pcg_stop == PCG_STOP_MAX_ITERS;
   }
-  if (!use_dense_ && nfree_)  // S read + 7 length-6nf vectors touched per PCG iteration
-    prof_->add_bytes("pcg", (double)h_sc_.pcg_iters * (288.0 * n_full_ + 7.0 * 48.0 * nfree_));
+  if (!use_dense_ && nfree_ && !imp_ok)  // S read + 7 length-6nf vectors touched per PCG iteration
+    prof_->add_bytes("pcg", (double)(h_sc_.pcg_iters - (try_imp ? imp_iters_ : 0)) *
+                                (288.0 * n_full_ + 7.0 * 48.0 * nfree_));
   if (h_sc_.nonfinite) return false;
   if (h_sc_.depth_obs != ~0ull) raise_projection_error(true);
   *new_cost = h_sc_.cost;

@@ -37,6 +37,14 @@ struct BAScalars {
   double proj_depth;         // p_cam.z of depth_obs
 };
 
+// Device state of the matrix-free Schur PCG (csrc/ischur.cuh).
+struct ImpState {
+  double rz;       // r.z
+  double bnorm;    // |b|
+  int it;          // iterations done
+  int done;        // 0 running, 1 converged, 2 failed, 3 out of iterations
+};
+
 class BASolver {
  public:
   BASolver(cudaStream_t s, Profiler* p, Comm* c) : stream_(s), prof_(p), comm_(c) {}
@@ -57,8 +65,11 @@ class BASolver {
   double eval_cost_current();
   void linearize();
   bool trial(double lam, double* new_cost, double* step_norm);
+  void point_prep(double lam);
   void build_schur(double lam);
   bool solve_reduced(double lam);
+  // Matrix-free Schur PCG (high-damping trials); false if it did not converge.
+  bool solve_implicit(double lam);
   void raise_projection_error(bool trial_state);
   void read_scalars();
   BlkArgs blk_args(double lam) const;
@@ -132,6 +143,8 @@ class BASolver {
   DevBuf<BAScalars> sc_pre_;             // flags of the point prep done inside k_point_lin
   bool prep_ready_ = false;              // pv holds V*^-1 at prep_lam_ for the next trial
   double prep_lam_ = 0.0;
+  double prep_done_lam_ = -1.0;          // pv holds this trial's V*^-1 (point_prep ran)
+  bool prep_folded_ = false;             // ... prepared inside k_point_lin (flags in sc_pre_)
   DevBuf<double> term_contrib_;          // [2E+A][42] per-term J^T J | J^T r (k_terms_lin)
   DevBuf<double> edge_H_;                // [E*36] J_a^T J_b (weighted)
 
@@ -142,6 +155,13 @@ class BASolver {
   DevBuf<double> pv_;                    // [P*12] V*^-1 (6) | e (3) | pad
   DevBuf<double> S_, b_;                 // [n_full*36], [nf*6]
   DevBuf<double> dc_;                    // [nf*6]
+  // matrix-free Schur PCG (ischur.cuh)
+  bool imp_enabled_ = std::getenv("SFM_IMPLICIT") == nullptr || std::atoi(std::getenv("SFM_IMPLICIT")) != 0;
+  int last_pcg_ = -1;                    // PCG iterations of the previous trial of this linearisation
+  int imp_iters_ = 0;
+  int imp_trials_ = 0;
+  DevBuf<double> imp_s_, imp_r_, imp_z_, imp_p_, imp_q_, imp_b_, imp_M_;
+  DevBuf<ImpState> imp_st_;
   TwoLevelPcg pcg_;
 
   // reductions

@@ -409,4 +409,54 @@ SFM_HD double loss_rho_prime(int kind, double param, double s) {
   return 1.0 / (1.0 + s / (param * param));
 }
 
+// Inverse of a symmetric positive-definite 6x6 block (row-major) through
+// its Cholesky factor, fully unrolled (block and factors stay in
+// registers).  Returns false (and a finite substitute) if A is not PD.
+__device__ __forceinline__ bool spd6_inverse(const double A[36], double* __restrict__ M) {
+  double L[36];
+#pragma unroll
+  for (int i = 0; i < 36; ++i) L[i] = 0.0;
+  bool ok = true;
+#pragma unroll
+  for (int c = 0; c < 6; ++c) {
+    double s = A[c * 6 + c];
+#pragma unroll
+    for (int k = 0; k < c; ++k) s -= L[c * 6 + k] * L[c * 6 + k];
+    if (!(s > 0.0)) { ok = false; s = 1.0; }
+    double d = sqrt(s);
+    L[c * 6 + c] = d;
+#pragma unroll
+    for (int r = c + 1; r < 6; ++r) {
+      double v = A[r * 6 + c];
+#pragma unroll
+      for (int k = 0; k < c; ++k) v -= L[r * 6 + k] * L[c * 6 + k];
+      L[r * 6 + c] = v / d;
+    }
+  }
+  double Li[36];
+#pragma unroll
+  for (int i = 0; i < 36; ++i) Li[i] = 0.0;
+#pragma unroll
+  for (int c = 0; c < 6; ++c) {
+    Li[c * 6 + c] = 1.0 / L[c * 6 + c];
+#pragma unroll
+    for (int r = c + 1; r < 6; ++r) {
+      double s = 0.0;
+#pragma unroll
+      for (int k = c; k < r; ++k) s += L[r * 6 + k] * Li[k * 6 + c];
+      Li[r * 6 + c] = -s / L[r * 6 + r];
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < 6; ++r)
+#pragma unroll
+    for (int c = 0; c < 6; ++c) {
+      double s = 0.0;
+#pragma unroll
+      for (int k = (r > c ? r : c); k < 6; ++k) s += Li[k * 6 + r] * Li[k * 6 + c];
+      M[r * 6 + c] = s;
+    }
+  return ok;
+}
+
 }  // namespace sfm

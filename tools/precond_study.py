@@ -269,3 +269,30 @@ if os.environ.get("NS") and S_hist:
     for it in range(4):
         X = X @ (2 * I - E_new @ X)
         print(f"NS step {it + 1}: ||I - E X|| = {np.linalg.norm(I - E_new @ X, 2):.3e}", flush=True)
+
+
+# --- coarse space + a per-cluster scale column: the similarity gauge's scale
+# direction of camera j is the left perturbation (0, t_j) (t -> s t), which
+# the rigid-motion columns Adj(T_j) do not span ------------------------------
+if os.environ.get("SCALE"):
+    for Cx in [int(v) for v in os.environ.get("SCALE_C", str(C)).split(",")]:
+        ncx = (nf + Cx - 1) // Cx
+        clx = np.arange(nf) // Cx
+        Pd = np.zeros((nf, 6, 7))
+        for i, f in enumerate(free):
+            qq, tt = G.pose(q[f], t[f])
+            Pd[i, :, :6] = G.adjoint((qq, tt))
+            Pd[i, 3:, 6] = tt
+        Px = sp.bsr_matrix((Pd, clx, np.arange(nf + 1)), shape=(6 * nf, 7 * ncx)).tocsr()
+        Acix = np.linalg.inv((Px.T @ (S @ Px)).toarray())
+        pcg(lambda r: jac(r) + Px @ (Acix @ (Px.T @ r)), zero, f"additive rigid+scale C={Cx}")
+        # global similarity (7 columns over all frames) on top of the rigid clusters
+    Pg = np.zeros((nf, 6, 7))
+    for i, f in enumerate(free):
+        qq, tt = G.pose(q[f], t[f])
+        Pg[i, :, :6] = G.adjoint((qq, tt))
+        Pg[i, 3:, 6] = tt
+    Pg = Pg.reshape(6 * nf, 7)
+    Pfull = sp.hstack([P, sp.csr_matrix(Pg)]).tocsr()
+    Acif = np.linalg.pinv((Pfull.T @ (S @ Pfull)).toarray())
+    pcg(lambda r: jac(r) + Pfull @ (Acif @ (Pfull.T @ r)), zero, f"additive rigid C={C} + global similarity")
