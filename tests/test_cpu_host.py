@@ -28,7 +28,7 @@ def test_library_loads_and_exports_every_symbol():
     lib = nat.load_library()
     for name in header_functions():
         assert hasattr(lib, name), name
-    assert lib.sfm_abi_version() == 3
+    assert lib.sfm_abi_version() == nat.ABI_VERSION
 
 
 def test_ctypes_struct_layout_matches_header(tmp_path):
