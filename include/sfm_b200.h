@@ -25,7 +25,7 @@
 extern "C" {
 #endif
 
-#define SFM_ABI_VERSION 4
+#define SFM_ABI_VERSION 5
 
 /* ---- error codes (mapped to sfmkit.errors classes by the Python layer) --- */
 #define SFM_OK 0
@@ -168,6 +168,9 @@ int sfm_ctx_create(int32_t device, int32_t rank, int32_t world,
 void sfm_ctx_destroy(sfm_ctx* ctx);
 const char* sfm_last_error(const sfm_ctx* ctx);
 /* Per-kernel CUDA-event timing (bench / roofline).  Off by default. */
+/* The CUDA stream (cudaStream_t) every call on ctx launches on, so a caller
+ * can bracket calls with its own CUDA events (bench.py's device timing). */
+int sfm_ctx_stream(const sfm_ctx* ctx, void** out);
 int sfm_set_profiling(sfm_ctx* ctx, int32_t enabled);
 int sfm_prof_count(const sfm_ctx* ctx);
 int sfm_prof_get(const sfm_ctx* ctx, int32_t i, const char** name,
@@ -191,10 +194,13 @@ int sfm_ba_solve(sfm_ctx* ctx, const sfm_ba_problem* prob,
 /* Stepwise form of sfm_ba_solve for device-resident benchmarking:
  * setup uploads + builds structure and evaluates the initial cost;
  * iterate runs up to n LM iterations continuing the same solve;
+ * restart begins a new solve from the entry state (poses, points, lambda_0,
+ * counters, initial cost) on the same device-resident problem and structure;
  * download copies the current state out. */
 int sfm_ba_setup(sfm_ctx* ctx, const sfm_ba_problem* prob,
                  const sfm_ba_options* opt);
 int sfm_ba_iterate(sfm_ctx* ctx, int32_t n_iters, sfm_ba_report* report);
+int sfm_ba_restart(sfm_ctx* ctx);
 int sfm_ba_download(sfm_ctx* ctx, double* out_cam_q, double* out_cam_t,
                     double* out_points);
 

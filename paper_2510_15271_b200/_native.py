@@ -17,7 +17,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libsfm_b200.so")
 
 # ---- constants (mirror include/sfm_b200.h) ---------------------------------
-ABI_VERSION = 4
+ABI_VERSION = 5
 SFM_OK = 0
 SFM_E_INVALID = -1
 SFM_E_NON_POSITIVE_DEPTH = -2
@@ -46,9 +46,9 @@ TRI_METHODS = {"dlt": 0, "midpoint": 1}
 
 EXPORTED_SYMBOLS = (
     "sfm_abi_version", "sfm_nccl_unique_id", "sfm_ctx_create", "sfm_ctx_destroy",
-    "sfm_last_error", "sfm_set_profiling", "sfm_prof_count", "sfm_prof_get",
+    "sfm_last_error", "sfm_ctx_stream", "sfm_set_profiling", "sfm_prof_count", "sfm_prof_get",
     "sfm_prof_reset", "sfm_ba_solve", "sfm_ba_setup", "sfm_ba_iterate",
-    "sfm_ba_download", "sfm_ba_eval", "sfm_ransac_triangulate", "sfm_triangulate",
+    "sfm_ba_download", "sfm_ba_restart", "sfm_ba_eval", "sfm_ransac_triangulate", "sfm_triangulate",
     "sfm_gate", "sfm_reprojection_errors", "sfm_iterative_map", "sfm_ba_solve_emulated",
     "sfm_build_tracks", "sfm_gba_solve",
 )
@@ -180,6 +180,8 @@ def load_library(path: str = None):
         lib.sfm_ba_setup.argtypes = [_p, P(BAProblemC), P(BAOptionsC)]
         lib.sfm_ba_iterate.argtypes = [_p, c_i32, P(BAReportC)]
         lib.sfm_ba_download.argtypes = [_p, _p, _p, _p]
+        lib.sfm_ba_restart.argtypes = [_p]
+        lib.sfm_ctx_stream.argtypes = [_p, P(_p)]
         lib.sfm_ba_eval.argtypes = [_p, P(BAProblemC), c_i32, c_d, _p, _p, _p, _p]
         lib.sfm_ransac_triangulate.argtypes = [_p, P(TracksC), c_d, c_d, c_i32, _p, _p, _p]
         lib.sfm_triangulate.argtypes = [_p, P(TracksC), c_d, c_i32, _p, _p]
@@ -241,6 +243,12 @@ class Context:
             raise_for_code(rc, self.last_error())
 
     # profiling ----------------------------------------------------------
+    def stream_handle(self) -> int:
+        """cudaStream_t of this context (sfm_ctx_stream) as an integer."""
+        out = _p()
+        self.check(self.lib.sfm_ctx_stream(self.handle, ctypes.byref(out)))
+        return int(out.value or 0)
+
     def set_profiling(self, on: bool):
         self.check(self.lib.sfm_set_profiling(self.handle, 1 if on else 0))
 

@@ -1917,6 +1917,53 @@ void BASolver::setup(const sfm_ba_problem& pr, const sfm_ba_options& opt) {
   }
 }
 
+void BASolver::save_entry() {
+  cudaStream_t s = stream_;
+  q0_.resize((size_t)F_ * 4);
+  t0_.resize((size_t)F_ * 3);
+  X0_.resize((size_t)P_ * 3);
+  if (F_) {
+    SFM_CUDA(cudaMemcpyAsync(q0_.get(), q_[cur_].get(), q0_.bytes(), cudaMemcpyDeviceToDevice, s));
+    SFM_CUDA(cudaMemcpyAsync(t0_.get(), t_[cur_].get(), t0_.bytes(), cudaMemcpyDeviceToDevice, s));
+  }
+  if (P_) SFM_CUDA(cudaMemcpyAsync(X0_.get(), X_[cur_].get(), X0_.bytes(), cudaMemcpyDeviceToDevice, s));
+}
+
+void BASolver::restart() {
+  SFM_REQUIRE(q0_.n == (size_t)F_ * 4 && X0_.n == (size_t)P_ * 3, "restart without a saved entry state");
+  cudaStream_t s = stream_;
+  cur_ = 0;
+  if (F_) {
+    SFM_CUDA(cudaMemcpyAsync(q_[0].get(), q0_.get(), q0_.bytes(), cudaMemcpyDeviceToDevice, s));
+    SFM_CUDA(cudaMemcpyAsync(t_[0].get(), t0_.get(), t0_.bytes(), cudaMemcpyDeviceToDevice, s));
+    k_frames_rt<<<grid_for(F_, 128), 128, 0, s>>>(F_, q_[0].get(), t_[0].get(), Rt_[0].get());
+    SFM_CHECK_LAUNCH();
+  }
+  if (P_) SFM_CUDA(cudaMemcpyAsync(X_[0].get(), X0_.get(), X0_.bytes(), cudaMemcpyDeviceToDevice, s));
+  prep_ready_ = false;
+  prep_done_lam_ = -1.0;
+  prep_folded_ = false;
+  last_pcg_ = -1;
+  imp_iters_ = 0;
+  pcg_.restart();
+  iters_ = 0;
+  n_trials_ = 0;
+  pcg_total_ = 0;
+  pcg_stagnated_ = 0;
+  pcg_max_hit_ = 0;
+  term_ = SFM_TERM_MAX_ITERATIONS;
+  lam_ = opt_.initial_lambda;
+  initial_cost_ = eval_cost_current();
+  cost_ = initial_cost_;
+  finished_ = false;
+  if (n_params_ == 0 || !has_residuals_) {
+    term_ = SFM_TERM_ALL_FIXED;
+    finished_ = true;
+  } else if (opt_.max_iters <= 0) {
+    finished_ = true;
+  }
+}
+
 void BASolver::read_scalars() {
   sc_.download(&h_sc_, 1, stream_);
   SFM_CUDA(cudaStreamSynchronize(stream_));

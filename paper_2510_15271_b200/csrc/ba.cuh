@@ -54,6 +54,11 @@ class BASolver {
   void setup(const sfm_ba_problem& prob, const sfm_ba_options& opt);
   // Runs up to n LM iterations continuing the current solve.
   void iterate(int n, sfm_ba_report* rep);
+  // Stepwise sessions: keep a device copy of the entry state (after setup)
+  // and restart the solve from it -- a fresh bundle_adjust over the same
+  // device-resident problem and structure (bench.py's per-step solves).
+  void save_entry();
+  void restart();
   void download(double* q, double* t, double* X);
   // Parity/debug evaluation of the reprojection residuals.
   static void eval(cudaStream_t s, Profiler* p, const sfm_ba_problem& prob, int loss_kind,
@@ -106,6 +111,7 @@ class BASolver {
   DevBuf<int> frame_model_, free_idx_, free_frame_;
   DevBuf<double> q_[2], t_[2], Rt_[2];  // [F*4], [F*3], [F*12]; index cur_
   DevBuf<double> X_[2];                 // [P*3]
+  DevBuf<double> q0_, t0_, X0_;         // entry state (save_entry / restart)
   int cur_ = 0;
 
   // observations (point-major)

@@ -98,6 +98,12 @@ void sfm_ctx_destroy(sfm_ctx* ctx) {
 
 const char* sfm_last_error(const sfm_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
 
+int sfm_ctx_stream(const sfm_ctx* ctx, void** out) {
+  if (!ctx || !out) return SFM_E_INVALID;
+  *out = (void*)ctx->stream;
+  return SFM_OK;
+}
+
 int sfm_set_profiling(sfm_ctx* ctx, int32_t enabled) {
   return guarded(ctx, [&] { ctx->prof.enabled = enabled != 0; });
 }
@@ -126,6 +132,7 @@ int sfm_ba_setup(sfm_ctx* ctx, const sfm_ba_problem* prob, const sfm_ba_options*
     ctx->ba.reset(new sfm::BASolver(ctx->stream, &ctx->prof, &ctx->comm));
     try {
       ctx->ba->setup(*prob, *opt);
+      ctx->ba->save_entry();
     } catch (...) {
       ctx->ba.reset();
       throw;
@@ -137,6 +144,13 @@ int sfm_ba_iterate(sfm_ctx* ctx, int32_t n_iters, sfm_ba_report* report) {
   return guarded(ctx, [&] {
     SFM_REQUIRE(ctx->ba != nullptr, "sfm_ba_iterate before sfm_ba_setup");
     ctx->ba->iterate(n_iters, report);
+  });
+}
+
+int sfm_ba_restart(sfm_ctx* ctx) {
+  return guarded(ctx, [&] {
+    SFM_REQUIRE(ctx->ba != nullptr, "sfm_ba_restart before sfm_ba_setup");
+    ctx->ba->restart();
   });
 }
 

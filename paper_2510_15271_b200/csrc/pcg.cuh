@@ -49,6 +49,8 @@ class TwoLevelPcg {
   void solve(const PcgProblem& p, int max_it, double rtol, BAScalars* sc, cudaStream_t s,
              Profiler* prof);
   int last_grid() const { return grid_; }
+  // Forget the coarse operator and the warm-start solution (a new solve).
+  void restart() { lin_count_ = 0; coarse_valid_ = false; have_prev_ = false; }
 
  private:
   int nf_ = 0, cluster_ = 0, nc_ = 0, ncp_ = 0, npad_ = 0, grid_ = 0, gj_grid_ = 0;

@@ -972,6 +972,11 @@ class DeviceBA:
         self.ctx.check(self.ctx.lib.sfm_ba_iterate(self.ctx.handle, int(n), ctypes.byref(rep)))
         return rep
 
+    def restart(self):
+        """A new solve from the entry state on the same device-resident
+        problem (sfm_ba_restart)."""
+        self.ctx.check(self.ctx.lib.sfm_ba_restart(self.ctx.handle))
+
     def download(self):
         a = self.arrays
         q = np.empty_like(a.cam_q)

@@ -154,3 +154,48 @@ def test_oracle_gate_matches_reference(golden):
     assert removed == int(d["ref_removed"])
     np.testing.assert_array_equal(mask.astype(np.uint8), d["ref_mask"])
     np.testing.assert_array_equal((inl >= 2).astype(np.int8), d["ref_triangulated"])
+
+
+@pytest.mark.parametrize("case", ["dlt", "midpoint", "kinds_dlt", "kinds_midpoint"])
+def test_oracle_batched_ransac_matches_reference(golden, case):
+    """oracle/imap.py's track-batched RANSAC (the config-sized restatement)
+    against the same sfmkit fixtures as the scalar one."""
+    from oracle import imap as OI
+    method = case.split("_")[-1]
+    d = golden("tri_" + case)
+    fr = OI.FrameArrays(d["cam_q"], d["cam_t"], d["frame_model"], models_of(d))
+    X, mask, st = OI.ransac_batch(fr, d["track_ptr"], d["obs_frame"], d["obs_uv"],
+                                  float(d["threshold_px"]), float(d["min_angle"]), method)
+    ok = d["ref_status"] == OT.OK
+    np.testing.assert_array_equal(st == OI.TRIANGULATED, ok)
+    np.testing.assert_array_equal(mask.astype(np.uint8), d["ref_mask"])
+    np.testing.assert_allclose(X[ok], d["ref_X"][ok], rtol=1e-9, atol=1e-9)
+
+
+IMAP_CASES = {"iterative_map": {},
+              "iterative_map_large": dict(stage1=(2, 1.0, 4.0), lambda_c=0.5, lambda_a=2.0,
+                                          max_solver_iters=25)}
+
+
+@pytest.mark.parametrize("case", sorted(IMAP_CASES))
+def test_oracle_iterative_map_matches_reference(golden, case):
+    """oracle/imap.py iterative_map (mapping.py:569-624) against sfmkit runs:
+    statuses, landmark order, masks and round statistics bit-exact."""
+    from oracle import imap as OI
+    d = golden(case)
+    F = len(d["cam_q"])
+    fixed = np.zeros(F, np.uint8)
+    fixed[0] = 1                               # anchor: min frame (mapping.py:583-593)
+    edges = np.stack([np.arange(F - 1), np.arange(1, F)], 1)
+    r = OI.iterative_map(d["cam_q"], d["cam_t"], np.zeros(F, int), fixed,
+                         [(0, 500.0, 500.0, 320.0, 240.0, (0.0, 0.0))], d["track_ptr"],
+                         d["obs_frame"], d["obs_uv"], edges, np.arange(1, F), **IMAP_CASES[case])
+    np.testing.assert_array_equal(r["status"], d["ref_status"])
+    np.testing.assert_array_equal(r["lm_track"], d["ref_lm_track"])
+    for key in ("added", "removed", "landmarks"):
+        np.testing.assert_array_equal([s[key] for s in r["round_stats"]], d["ref_round_" + key])
+    ptr = d["track_ptr"]
+    mask = np.concatenate([r["inlier_mask"][ptr[i]:ptr[i + 1]] for i in r["lm_track"]])
+    np.testing.assert_array_equal(mask.astype(np.uint8), d["ref_lm_mask"])
+    np.testing.assert_allclose(r["points"][r["lm_track"]], d["ref_lm_X"], atol=1e-6)
+    np.testing.assert_allclose(r["cam_q"], d["ref_cam_q"], atol=1e-7)
