@@ -488,17 +488,23 @@ def other_configs(seed, ctx, probe):
         def run():
             return iterative_map_arrays(sc.cam_q, sc.cam_t, fm, sc.frame_fixed, models, n_models,
                                         ptr, sc.obs_frame, sc.obs_uv, edges, priors, mc, ctx=ctx)
-        run()
-        ctx.set_profiling(True)
-        ctx.reset_profile()
-        t0 = time.perf_counter()
-        r = run()
-        s = time.perf_counter() - t0
+        key = f"config{cfg}_iterative_map"
+        try:
+            run()
+            ctx.set_profiling(True)
+            ctx.reset_profile()
+            t0 = time.perf_counter()
+            r = run()
+            s = time.perf_counter() - t0
+        except Exception as e:   # e.g. NonPositiveDepth out of a BA trial, as the reference raises
+            ctx.set_profiling(False)
+            out[key] = {"raised": f"{type(e).__name__}: {e}"}
+            continue
         ctx.set_profiling(False)
         prof = ctx.profile()
         ks = {k: {"launches": v["launches"], "ms": round(v["ms"], 3)}
               for k, v in sorted(prof.items(), key=lambda kv: -kv[1]["ms"])[:8]}
-        out[f"config{cfg}_iterative_map"] = {
+        out[key] = {
             "workload": "configs[%d]: %d frames / %d tracks / %d obs (5%% outliers), "
                         "iterative_map (RANSAC-DLT -> stage-1 BA -> 4 px gate rounds, stage-2 BA "
                         "-> 2 px gate), device-resident, from host arrays"
@@ -664,8 +670,14 @@ def main():
             cpu = {"value": None, "unit": "obs/s", "cores": 1, "kind": "reference",
                    "sample": str(probe)}
     if rank == 0 and world == 1 and not args.no_extra:
-        extra = other_configs(args.seed, ctx, probe)
-        extra["e2e_dropin_config3"] = dropin_e2e(sc, ctx)
+        try:
+            extra = other_configs(args.seed, ctx, probe)
+        except Exception as e:
+            extra = {"error": f"{type(e).__name__}: {e}"}
+        try:
+            extra["e2e_dropin_config3"] = dropin_e2e(sc, ctx)
+        except Exception as e:
+            extra["e2e_dropin_config3"] = {"error": f"{type(e).__name__}: {e}"}
 
     if rank == 0:
         line = {

@@ -10,8 +10,7 @@ from paper_2510_15271_b200.solver import DeviceOptions, RobustLoss, SolverOption
 cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 3
 iters = int(sys.argv[2]) if len(sys.argv) > 2 else 2
 a = scene_arrays(config_scene(cfg, seed=0))
-ba = DeviceBA(a, RobustLoss("huber", 2.0), SolverOptions(max_iters=100),
-              DeviceOptions(linear_solver="pcg", pcg_rtol=1e-8, pcg_max_iters=500))
+ba = DeviceBA(a, RobustLoss("huber", 2.0), SolverOptions(), DeviceOptions())  # bench.py's (drop-in defaults)
 prev = 0
 for i in range(iters):
     r = ba.iterate(1)

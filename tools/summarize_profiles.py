@@ -1,6 +1,6 @@
 """Turns a gpurun_out profiling directory (tools/gpu_profile.sh) into the
 committed summaries under profiles/:
-  <tag>_launches_summary.txt  every launch of `bench.py --steps 2 --warmup 3`
+  <tag>_launches_summary.txt  every launch of `bench.py --steps 1 --warmup 1 --no-extra`
                               (gpu__time_duration + DRAM bytes, cold-cache,
                               serialised: shares, not absolutes)
   <tag>_ncu_full_summary.txt  --set full metrics of the top kernels
@@ -41,8 +41,8 @@ for i, m in per.items():
 tot = sum(v[1] for v in agg.values())
 with open(f"profiles/{tag}_launches_summary.txt", "w") as f:
     f.write("# ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum "
-            "--clock-control none\n# command: python bench.py --steps 2 --warmup 3 --no-cpu-baseline "
-            "--no-e2e  (config 3, 1 B200): setup + 5 LM iterations\n# per-launch times are "
+            "--clock-control none\n# command: python bench.py --steps 1 --warmup 1 --no-cpu-baseline "
+            "--no-e2e --no-extra  (config 3, 1 B200): setup + 3 whole LM solves\n# per-launch times are "
             "cold-cache and serialised: compare shares, not absolutes\n")
     f.write(f"# total {tot / 1e3:.1f} us over {sum(v[0] for v in agg.values())} launches\n")
     f.write(f"{'launches':>8} {'total_us':>10} {'share':>6} {'DRAM_MB':>9}  kernel\n")
