@@ -302,8 +302,8 @@ def test_config3_lm_to_termination_matches_oracle(rtol):
     sample of 2,000 points.  The last iteration's decisions sit at the fp64
     rounding floor of the cost itself (decreases of 1e-16 relative, below the
     1e-14 summation-order noise of two correct evaluations), so the
-    termination has to be one of the two floor terminations on both sides
-    and the iteration count may differ by one."""
+    termination has to be one of the two floor terminations on both sides,
+    and extra accepted iterations may only be floor-level decreases."""
     from paper_2510_15271_b200 import _native as nat
     from paper_2510_15271_b200.mapping import DeviceBA
     from paper_2510_15271_b200.scenes import config_scene, scene_arrays
@@ -330,7 +330,11 @@ def test_config3_lm_to_termination_matches_oracle(rtol):
     np.testing.assert_allclose(costs[:n], ref_costs[:n], rtol=1e-9)
     assert rep.final_cost == pytest.approx(float(g["final_cost"]), rel=1e-12)
     assert term in FLOOR_TERMINATIONS and str(g["termination"]) in FLOOR_TERMINATIONS
-    assert abs(rep.iterations - int(g["iterations"])) <= 1
+    # iterations past the oracle's accepted ones only accept rounding-floor
+    # decreases: every such cost equals the oracle's final cost to 1e-12
+    extra = costs[len(ref_costs):]
+    np.testing.assert_allclose(extra, float(g["final_cost"]), rtol=1e-12)
+    assert rep.iterations >= int(g["iterations"]) - 1
     scale = max(1.0, float(np.abs(g["pt_absmean"]).max()))
     np.testing.assert_allclose(q, g["cam_q"], atol=1e-8)
     np.testing.assert_allclose(t, g["cam_t"], atol=1e-7 * scale)
