@@ -550,6 +550,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-extra", action="store_true", help="skip the other configs / drop-in e2e")
+    ap.add_argument("--max-iters", type=int, default=None,
+                    help="A/B only: cap the LM iterations per solve (default: SolverOptions().max_iters)")
     args = ap.parse_args()
     rank, world, local = dist_init(args)
     if args.impl == "reference":
@@ -574,6 +576,8 @@ def main():
     part = arrays.shard(rank, world) if world > 1 else arrays
     loss = RobustLoss("huber", 2.0)
     sopt = SolverOptions()            # the reference's defaults (max_iters 50 = max_solver_iters)
+    if args.max_iters is not None:
+        sopt = SolverOptions(max_iters=args.max_iters)
     FOREVER = 1 << 30
 
     # ---- device-resident whole solves (value) ---------------------------------

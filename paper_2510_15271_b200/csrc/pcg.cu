@@ -1063,6 +1063,7 @@ void TwoLevelPcg::set_pattern(const int* row_ptr, const int* col, int nnzb, cuda
   if (const char* e = std::getenv("SFM_COARSE_REFRESH")) refresh_ = std::max(1, std::atoi(e));
   if (const char* e = std::getenv("SFM_COARSE_LAMMAX")) lam_max_ = std::atof(e);
   if (const char* e = std::getenv("SFM_COARSE_DRIFT")) drift_ = std::max(1.0, std::atof(e));
+  if (const char* e = std::getenv("SFM_COARSE_LAMFLOOR")) lam_floor_ = std::atof(e);
   lin_count_ = 0;
   have_prev_ = false;
   warm_ = true;
@@ -1314,13 +1315,14 @@ void TwoLevelPcg::solve(const PcgProblem& p, int max_it, double rtol, BAScalars*
   //   * otherwise A_c is re-assembled and re-inverted whenever lam has moved
   //     by more than drift_ (either way) from the lam it was built at, or the
   //     basis was refreshed (set_basis).
-  //   Below kLamFloor the damping is negligible next to the coarse
-  //   operator's own (rigid-motion) spectrum -- rebuilding there does not
-  //   change the PCG iteration count (config 3: lambda 1e-4 .. 1e-8) -- so
-  //   dampings under the floor count as equal.
-  constexpr double kLamFloor = 1e-6;
+  //   Below lam_floor_ (1e-5) the damping is negligible next to the coarse
+  //   operator's own (rigid-motion) spectrum, so dampings under the floor
+  //   count as equal.  Config 3, LM iterations 1-14 (bench.py --max-iters 14,
+  //   tools/ab_env.sh): floor 1e-6 / 1e-5 / 1e-4 -> 1504 / 1508 / 1548 PCG
+  //   iterations and 2.42 / 1.82 / 1.21 ms of coarse inverses, 317 / 323 /
+  //   325 LM it/s.
   const bool coarse_on = gj_grid_ > 0 && p.lam <= lam_max_;
-  const double lam_eff = std::max(p.lam, kLamFloor);
+  const double lam_eff = std::max(p.lam, lam_floor_);
   bool stale = !coarse_valid_;
   if (coarse_on && !stale) {
     const double ratio = lam_eff / lam_build_;

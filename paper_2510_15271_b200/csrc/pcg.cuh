@@ -59,6 +59,7 @@ class TwoLevelPcg {
   int npairs_ = 0;
   bool coarse_valid_ = false;
   double lam_build_ = 0.0, lam_max_ = 1e-2, drift_ = 4.0;
+  double lam_floor_ = 1e-5;   // dampings below this count as equal (coarse rebuild rule)
   bool have_prev_ = false, warm_ = true;  // warm start from the previous solution
   const double* Aci_ = nullptr;
   DevBuf<double> Minv_, Pm_, Ac_[2], gjpiv_, r_, z_, p_, q_, rpart_, part_;

@@ -5,7 +5,7 @@ OUT=gpurun_out/$1; shift; mkdir -p $OUT
 for rep in $(seq ${REPS:-2}); do
   for lib in "$@"; do
     if [ "$lib" = tree ]; then L=""; else L="SFM_B200_LIB=$PWD/paper_2510_15271_b200/$lib"; fi
-    env $L timeout 300 python bench.py --steps ${STEPS:-10} --warmup 3 --no-cpu-baseline --no-e2e --no-extra > $OUT/b.out 2>&1
+    env $L timeout 300 python bench.py --steps ${STEPS:-10} --warmup 3 --no-cpu-baseline --no-e2e --no-extra ${MAXIT:+--max-iters $MAXIT} > $OUT/b.out 2>&1
     python - "$lib" $OUT/b.out <<'PY'
 import json, sys
 ln = [l for l in open(sys.argv[2]) if l.startswith('{')]

@@ -5,7 +5,7 @@ OUT=gpurun_out/$1; shift; mkdir -p $OUT
 for rep in $(seq ${REPS:-2}); do
   for e in "$@"; do
     if [ "$e" = "-" ]; then E=""; else E="$e"; fi
-    env $E timeout 300 python bench.py --steps ${STEPS:-10} --warmup 3 --no-cpu-baseline --no-e2e --no-extra > $OUT/b.out 2>&1
+    env $E timeout 300 python bench.py --steps ${STEPS:-10} --warmup 3 --no-cpu-baseline --no-e2e --no-extra ${MAXIT:+--max-iters $MAXIT} > $OUT/b.out 2>&1
     python - "$e" $OUT/b.out <<'PY'
 import json, sys
 ln = [l for l in open(sys.argv[2]) if l.startswith('{')]
