@@ -25,7 +25,7 @@
 extern "C" {
 #endif
 
-#define SFM_ABI_VERSION 5
+#define SFM_ABI_VERSION 6
 
 /* ---- error codes (mapped to sfmkit.errors classes by the Python layer) --- */
 #define SFM_OK 0
@@ -139,6 +139,13 @@ typedef struct {
                                  (0 = default 1e-2; above it block-Jacobi)  */
   double coarse_drift;        /* re-assemble A_c when lambda moved by more
                                  than this factor since (0 = default 4)    */
+  int32_t pcg_partition;      /* point-sharded ranks: 1 = row-partitioned
+                                 PCG (S / b reduce-scattered by block rows,
+                                 z and the dot products pushed between ranks
+                                 inside the Krylov kernel; ranks sharing a
+                                 device), 0 = replicated PCG on the
+                                 all-reduced S (NCCL ranks always)        */
+  int32_t _pad0;
 } sfm_ba_options;
 
 /* SolverReport (solver.py:90-95) + device-side statistics. */
@@ -165,6 +172,22 @@ int sfm_nccl_unique_id(uint8_t out[128]);
 /* world == 1: nccl_id may be NULL.  device = CUDA ordinal used by this rank. */
 int sfm_ctx_create(int32_t device, int32_t rank, int32_t world,
                    const uint8_t* nccl_id, sfm_ctx** out);
+/* Single-process multi-GPU context (one context owning
+ * n_gpus devices).  sfm_ba_solve on it shards the points by observation
+ * count (8(e)), one host thread per device drives its shard, and the
+ * camera-indexed sums / scalars are all-reduced over NCCL communicators
+ * created in-process with ncclCommInitAll (NVLink / NVSwitch).
+ * sfm_iterative_map keeps its track state on devices[0] and runs every
+ * bundle adjustment sharded over the devices.  A repeated device id makes
+ * the ranks on it run as shard emulation (no NCCL): the test path on one
+ * GPU.  Replaces nothing in the reference (sfmkit is single-process,
+ * single-threaded); it is how bundle_adjust / iterative_map
+ * (mapping.py:390, :569) scale without a process launcher. */
+int sfm_ctx_create_multi(int32_t n_devices, const int32_t* devices, sfm_ctx** out);
+/* devices of the context (1 unless multi) and whether NCCL carries the sums */
+int sfm_ctx_devices(const sfm_ctx* ctx, int32_t* out_n, int32_t* out_nccl);
+/* cudaGetDeviceCount (0 without a GPU / driver) */
+int sfm_device_count(int32_t* out);
 void sfm_ctx_destroy(sfm_ctx* ctx);
 const char* sfm_last_error(const sfm_ctx* ctx);
 /* Per-kernel CUDA-event timing (bench / roofline).  Off by default. */

@@ -17,7 +17,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libsfm_b200.so")
 
 # ---- constants (mirror include/sfm_b200.h) ---------------------------------
-ABI_VERSION = 5
+ABI_VERSION = 6
 SFM_OK = 0
 SFM_E_INVALID = -1
 SFM_E_NON_POSITIVE_DEPTH = -2
@@ -45,7 +45,8 @@ TERMINATIONS = ("max_iterations", "gradient_tolerance", "no_decrease",
 TRI_METHODS = {"dlt": 0, "midpoint": 1}
 
 EXPORTED_SYMBOLS = (
-    "sfm_abi_version", "sfm_nccl_unique_id", "sfm_ctx_create", "sfm_ctx_destroy",
+    "sfm_abi_version", "sfm_nccl_unique_id", "sfm_ctx_create", "sfm_ctx_create_multi",
+    "sfm_ctx_devices", "sfm_device_count", "sfm_ctx_destroy",
     "sfm_last_error", "sfm_ctx_stream", "sfm_set_profiling", "sfm_prof_count", "sfm_prof_get",
     "sfm_prof_reset", "sfm_ba_solve", "sfm_ba_setup", "sfm_ba_iterate",
     "sfm_ba_download", "sfm_ba_restart", "sfm_ba_eval", "sfm_ransac_triangulate", "sfm_triangulate",
@@ -88,7 +89,8 @@ class BAOptionsC(ctypes.Structure):
                 ("pcg_max_iters", ctypes.c_int32), ("pcg_rtol", ctypes.c_double),
                 ("dense_max_dim", ctypes.c_int32), ("coarse_cluster", ctypes.c_int32),
                 ("coarse_refresh", ctypes.c_int32), ("coarse_max_lambda", ctypes.c_double),
-                ("coarse_drift", ctypes.c_double)]
+                ("coarse_drift", ctypes.c_double), ("pcg_partition", ctypes.c_int32),
+                ("_pad0", ctypes.c_int32)]
 
 
 class BAReportC(ctypes.Structure):
@@ -182,6 +184,9 @@ def load_library(path: str = None):
         lib.sfm_ba_download.argtypes = [_p, _p, _p, _p]
         lib.sfm_ba_restart.argtypes = [_p]
         lib.sfm_ctx_stream.argtypes = [_p, P(_p)]
+        lib.sfm_ctx_create_multi.argtypes = [c_i32, P(c_i32), P(_p)]
+        lib.sfm_ctx_devices.argtypes = [_p, P(c_i32), P(c_i32)]
+        lib.sfm_device_count.argtypes = [P(c_i32)]
         lib.sfm_ba_eval.argtypes = [_p, P(BAProblemC), c_i32, c_d, _p, _p, _p, _p]
         lib.sfm_ransac_triangulate.argtypes = [_p, P(TracksC), c_d, c_d, c_i32, _p, _p, _p]
         lib.sfm_triangulate.argtypes = [_p, P(TracksC), c_d, c_i32, _p, _p]
@@ -211,17 +216,42 @@ def ptr(a):
 
 
 class Context:
-    """One sfm_ctx (one CUDA device, one stream, optional NCCL communicator)."""
+    """One sfm_ctx: one CUDA device and stream, with an optional NCCL
+    communicator (one process per GPU, `rank` of `world`) -- or, from
+    Context.multi, every device of a single-process multi-GPU context."""
 
     def __init__(self, device: int = 0, rank: int = 0, world: int = 1,
-                 nccl_id: bytes = None):
+                 nccl_id: bytes = None, _handle=None, _devices=None):
         self.lib = load_library()
         self.device, self.rank, self.world = device, rank, world
+        self.devices = list(_devices) if _devices else [device]
+        if _handle is not None:
+            self.handle = _handle
+            return
         h = _p()
         rc = self.lib.sfm_ctx_create(device, rank, world, nccl_id, ctypes.byref(h))
         if rc != SFM_OK:
             raise RuntimeError(f"sfm_ctx_create failed (code {rc}); is a CUDA device visible?")
         self.handle = h
+
+    @classmethod
+    def multi(cls, devices) -> "Context":
+        """Single-process multi-GPU context (sfm_ctx_create_multi): solves on
+        it are point-sharded over `devices`, NCCL communicators created
+        in-process; a repeated device id runs its ranks as shard emulation."""
+        lib = load_library()
+        devs = (ctypes.c_int32 * len(devices))(*[int(d) for d in devices])
+        h = _p()
+        rc = lib.sfm_ctx_create_multi(len(devices), devs, ctypes.byref(h))
+        if rc != SFM_OK:
+            raise RuntimeError(f"sfm_ctx_create_multi failed (code {rc})")
+        return cls(int(devices[0]), 0, 1, _handle=h, _devices=devices)
+
+    def topology(self):
+        """(devices driven by this context, NCCL in use)."""
+        n, nccl = ctypes.c_int32(), ctypes.c_int32()
+        self.check(self.lib.sfm_ctx_devices(self.handle, ctypes.byref(n), ctypes.byref(nccl)))
+        return n.value, bool(nccl.value)
 
     def close(self):
         if getattr(self, "handle", None):
@@ -271,6 +301,13 @@ class Context:
         self.check(self.lib.sfm_prof_reset(self.handle))
 
 
+def device_count() -> int:
+    """CUDA devices visible to the library (sfm_device_count)."""
+    n = ctypes.c_int32()
+    load_library().sfm_device_count(ctypes.byref(n))
+    return n.value
+
+
 def nccl_unique_id() -> bytes:
     lib = load_library()
     buf = ctypes.create_string_buffer(128)
@@ -285,7 +322,20 @@ _default_lock = threading.Lock()
 
 
 def default_context() -> Context:
-    """Per-process context on cuda:LOCAL_RANK (or 0), created lazily."""
+    """Per-process context, created lazily: SFM_B200_DEVICES="0,1,..,7"
+    makes it a single-process multi-GPU context (Context.multi), so the
+    sfmkit-signature entry points (bundle_adjust, iterative_map) shard over
+    those GPUs with no code change; otherwise cuda:SFM_B200_DEVICE /
+    LOCAL_RANK / 0."""
+    devs = os.environ.get("SFM_B200_DEVICES")
+    if devs:
+        key = "multi:" + devs
+        with _default_lock:
+            ctx = _default.get(key)
+            if ctx is None:
+                ctx = Context.multi([int(d) for d in devs.split(",") if d.strip()])
+                _default[key] = ctx
+            return ctx
     dev = int(os.environ.get("SFM_B200_DEVICE", os.environ.get("LOCAL_RANK", "0")))
     with _default_lock:
         ctx = _default.get(dev)

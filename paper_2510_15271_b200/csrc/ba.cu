@@ -85,6 +85,28 @@ struct BlkArgs {
 
 namespace {
 
+// PcgCollective over the solver's Comm: the row-partitioned PCG's coarse
+// operator sum and its single launch across ranks sharing a device.
+class CommPcgCollective final : public PcgCollective {
+ public:
+  explicit CommPcgCollective(Comm* c) : c_(c) {}
+  int rank() const override { return c_->rank; }
+  int world() const override { return c_->world; }
+  void sum(double* d, size_t n, cudaStream_t s) override { c_->sum(d, n, s); }
+  void launch_all(const PcgRankView& mine, cudaStream_t s,
+                  const std::function<void(const PcgRankView*)>& launch) override {
+    SFM_REQUIRE(c_->emu != nullptr, "row-partitioned PCG needs its ranks on one device");
+    c_->emu->run_root(c_->rank, &mine, s, [&](const void* const* all) {
+      std::vector<PcgRankView> v((size_t)c_->world);
+      for (int r = 0; r < c_->world; ++r) v[r] = *static_cast<const PcgRankView*>(all[r]);
+      launch(v.data());
+    });
+  }
+
+ private:
+  Comm* c_;
+};
+
 constexpr int kDenseMax = 210;    // packed lower triangle of 6*nf fits in smem
 constexpr int kBlock = 128;
 
@@ -1459,6 +1481,7 @@ struct SetupTimer {
 }  // namespace
 
 BASolver::~BASolver() {
+  if (h_pin_) cudaFreeHost(h_pin_);
   if (side_) {
     cudaStreamSynchronize(side_);
     cudaStreamDestroy(side_);
@@ -1473,6 +1496,7 @@ BASolver::~BASolver() {
 }
 
 void BASolver::setup(const sfm_ba_problem& pr, const sfm_ba_options& opt) {
+  NvtxRange nv("sfm ba setup");
   opt_ = opt;
   rank_ = comm_ ? comm_->rank : 0;
   SFM_REQUIRE(pr.n_frames >= 0 && pr.n_points >= 0 && pr.n_obs >= 0, "negative sizes");
@@ -1785,11 +1809,13 @@ void BASolver::setup(const sfm_ba_problem& pr, const sfm_ba_options& opt) {
     const int refresh = opt_.coarse_refresh > 0 ? opt_.coarse_refresh : 8;
     cudaStream_t ps = plan_stream_;
     cudaEvent_t pe = plan_ev_;
+    partitioned_ = comm_ && comm_->active() && comm_->emu != nullptr && opt_.pcg_partition != 0;
     plan = std::async(std::launch::async, [this, dev, cl, refresh, ps, pe]() {
       SFM_CUDA(cudaSetDevice(dev));
       alloc_stream() = ps;  // the plan's buffers are stream-ordered on the plan stream
       SFM_CUDA(cudaStreamWaitEvent(ps, pe, 0));
       pcg_.setup(nfree_, cl, refresh, ps);
+      if (partitioned_) pcg_.set_partition(comm_->world, comm_->rank);
       pcg_.set_coarse_policy(opt_.coarse_max_lambda > 0.0 ? opt_.coarse_max_lambda : 1e-2,
                              opt_.coarse_drift > 1.0 ? opt_.coarse_drift : 4.0);
       pcg_.set_pattern(row_ptr_.get(), col_idx_.get(), n_full_, ps);  // ends with a sync of ps
@@ -1886,6 +1912,15 @@ void BASolver::setup(const sfm_ba_problem& pr, const sfm_ba_options& opt) {
   part_d_.resize(grid_for(std::max(nfree_, 1), kBlock));
 
   if (plan.valid()) plan.get();  // the PCG plan built on its own thread (rethrows its errors)
+  if (partitioned_) {
+    coll_.reset(new CommPcgCollective(comm_));
+    const auto& rr = pcg_.rank_rows();
+    const auto& rb = pcg_.rank_blocks();
+    s_off_.assign(rb.begin(), rb.end());
+    b_off_.assign(rr.begin(), rr.end());
+    for (auto& v : s_off_) v *= 36;
+    for (auto& v : b_off_) v *= 6;
+  }
 
   tm.mark("terms + buffers + pcg plan");
   // all_fixed (solver.py:200-203) and the initial cost (solver.py:201)
@@ -1930,6 +1965,7 @@ void BASolver::save_entry() {
 }
 
 void BASolver::restart() {
+  NvtxRange nv("sfm restart");
   SFM_REQUIRE(q0_.n == (size_t)F_ * 4 && X0_.n == (size_t)P_ * 3, "restart without a saved entry state");
   cudaStream_t s = stream_;
   cur_ = 0;
@@ -1964,9 +2000,13 @@ void BASolver::restart() {
   }
 }
 
+// The one host synchronisation of a trial (the accept / reject decision is
+// the host's, solver.py:236-245): 128 bytes D2H into pinned memory.
 void BASolver::read_scalars() {
-  sc_.download(&h_sc_, 1, stream_);
+  if (!h_pin_) SFM_CUDA(cudaMallocHost(reinterpret_cast<void**>(&h_pin_), sizeof(BAScalars)));
+  SFM_CUDA(cudaMemcpyAsync(h_pin_, sc_.get(), sizeof(BAScalars), cudaMemcpyDeviceToHost, stream_));
   SFM_CUDA(cudaStreamSynchronize(stream_));
+  h_sc_ = *h_pin_;
 }
 
 // Raises NonPositiveDepth / OutOfModelDomain for the first offending
@@ -2031,6 +2071,7 @@ double BASolver::eval_cost_current() {
 }
 
 void BASolver::linearize() {
+  NvtxRange nv("sfm linearize");
   cudaStream_t s = stream_;
   last_pcg_ = -1;
   k_reset_scalars<<<1, 1, 0, s>>>(sc_.get(), 0);
@@ -2129,6 +2170,7 @@ void BASolver::point_prep(double lam) {
 }
 
 void BASolver::build_schur(double lam) {
+  NvtxRange nv("sfm schur");
   cudaStream_t s = stream_;
   point_prep(lam);
   const bool prepped = prep_folded_;
@@ -2150,8 +2192,13 @@ void BASolver::build_schur(double lam) {
     k_offdiag_blocks<<<grid_for((int64_t)n_off_ * 32, kOffWarps * 32), kOffWarps * 32, kOffSmem, s>>>(ba);
   }
   if (comm_ && comm_->active()) {
-    comm_->sum(S_.get(), (size_t)n_full_ * 36, s);
-    comm_->sum(b_.get(), (size_t)nfree_ * 6, s);
+    if (partitioned_) {  // each rank keeps only the block rows it solves for
+      comm_->reduce_ranges(S_.get(), s_off_, s);
+      comm_->reduce_ranges(b_.get(), b_off_, s);
+    } else {
+      comm_->sum(S_.get(), (size_t)n_full_ * 36, s);
+      comm_->sum(b_.get(), (size_t)nfree_ * 6, s);
+    }
   }
 }
 
@@ -2169,7 +2216,8 @@ bool BASolver::solve_reduced(double lam) {
   pp.nf = nfree_; pp.row_ptr = row_ptr_.get(); pp.col = col_idx_.get(); pp.S = S_.get(); pp.nnzb = n_full_;
   pp.diag_pos = diag_pos_.get(); pp.b = b_.get(); pp.x = dc_.get(); pp.lam = lam;
   pcg_.solve(pp, opt_.pcg_max_iters > 0 ? opt_.pcg_max_iters : 1000, opt_.pcg_rtol > 0 ? opt_.pcg_rtol : 1e-10,
-             sc_.get(), s, prof_);
+             sc_.get(), s, prof_, partitioned_ ? coll_.get() : nullptr);
+  if (partitioned_) comm_->allgather_ranges(dc_.get(), b_off_, s);  // every rank's cameras need all of dc
   return true;
 }
 
@@ -2233,6 +2281,7 @@ bool BASolver::solve_implicit(double lam) {
 // step is not finite (the reference then multiplies lambda by 10 without
 // evaluating the cost).
 bool BASolver::trial(double lam, double* new_cost, double* step_norm) {
+  NvtxRange nv("sfm trial");
   cudaStream_t s = stream_;
   k_reset_scalars<<<1, 1, 0, s>>>(sc_.get(), 1);
   SFM_CHECK_LAUNCH();

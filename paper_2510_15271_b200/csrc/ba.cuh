@@ -7,6 +7,7 @@
 // solved on device (dense Cholesky when small, block-Jacobi PCG otherwise).
 // See DESIGN.md for the data layout and the kernel/roofline inventory.
 #pragma once
+#include <memory>
 #include "comm.cuh"
 #include "common.cuh"
 #include "pcg.cuh"
@@ -169,6 +170,11 @@ class BASolver {
   DevBuf<double> imp_s_, imp_r_, imp_z_, imp_p_, imp_q_, imp_b_, imp_M_;
   DevBuf<ImpState> imp_st_;
   TwoLevelPcg pcg_;
+  // row-partitioned PCG over point-sharded ranks sharing a device
+  // (sfm_ba_options.pcg_partition): S / b reduce-scattered by block rows
+  bool partitioned_ = false;
+  std::vector<int64_t> s_off_, b_off_;    // element offsets of each rank's rows in S / b
+  std::unique_ptr<PcgCollective> coll_;
 
   // reductions
   DevBuf<double> part_a_, part_b_, part_c_, part_d_;
@@ -176,6 +182,7 @@ class BASolver {
   std::vector<int> diag_ub_host_;
   DevBuf<BAScalars> sc_;
   BAScalars h_sc_{};
+  BAScalars* h_pin_ = nullptr;          // pinned staging of the per-trial scalar read-back
 };
 
 struct GbaArgs;

@@ -18,8 +18,10 @@ struct sfm_ctx {
   cudaStream_t stream = nullptr;
   sfm::Profiler prof;
   sfm::Comm comm;
+  sfm::DeviceGroup group;  // multi-device context (sfm_ctx_create_multi): devices + in-process NCCL comms
   std::string err;
   std::unique_ptr<sfm::BASolver> ba;
+  bool multi() const { return group.size() > 1; }
 };
 
 namespace {
@@ -83,8 +85,61 @@ int sfm_ctx_create(int32_t device, int32_t rank, int32_t world, const uint8_t* n
   return SFM_OK;
 }
 
+int sfm_device_count(int32_t* out) {
+  if (!out) return SFM_E_INVALID;
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) n = 0;
+  *out = n;
+  return SFM_OK;
+}
+
+int sfm_ctx_create_multi(int32_t n_devices, const int32_t* devices, sfm_ctx** out) {
+  if (!out || n_devices < 1 || n_devices > 16 || !devices) return SFM_E_INVALID;
+  *out = nullptr;
+  auto* ctx = new sfm_ctx();
+  ctx->device = devices[0];
+  int rc = guarded(ctx, [&] {
+    SFM_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+    sfm::alloc_stream() = ctx->stream;
+    ctx->group.devices.assign(devices, devices + n_devices);
+    bool distinct = true;
+    for (int i = 0; i < n_devices; ++i) {
+      cudaMemPool_t pool;
+      SFM_CUDA(cudaDeviceGetDefaultMemPool(&pool, devices[i]));
+      uint64_t thr = UINT64_MAX;
+      SFM_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+      for (int j = 0; j < i; ++j) distinct &= devices[j] != devices[i];
+    }
+    // distinct devices: one NCCL communicator per device, created in this
+    // process (NVLink / NVSwitch); a repeated device: shard emulation
+    if (n_devices > 1 && distinct) {
+      ctx->group.comms.resize(n_devices);
+      SFM_NCCL(ncclCommInitAll(ctx->group.comms.data(), n_devices, ctx->group.devices.data()));
+    }
+    SFM_CUDA(cudaSetDevice(ctx->device));
+  });
+  if (rc != SFM_OK) {
+    std::fprintf(stderr, "sfm_ctx_create_multi: %s\n", ctx->err.c_str());
+    for (auto c : ctx->group.comms)
+      if (c) ncclCommDestroy(c);
+    delete ctx;
+    return rc;
+  }
+  *out = ctx;
+  return SFM_OK;
+}
+
+int sfm_ctx_devices(const sfm_ctx* ctx, int32_t* out_n, int32_t* out_nccl) {
+  if (!ctx || !out_n) return SFM_E_INVALID;
+  *out_n = ctx->multi() ? ctx->group.size() : 1;
+  if (out_nccl) *out_nccl = ctx->multi() ? (int32_t)!ctx->group.comms.empty() : (ctx->comm.world > 1);
+  return SFM_OK;
+}
+
 void sfm_ctx_destroy(sfm_ctx* ctx) {
   if (!ctx) return;
+  for (auto c : ctx->group.comms)
+    if (c) ncclCommDestroy(c);
   cudaSetDevice(ctx->device);
   sfm::alloc_stream() = ctx->stream;
   ctx->ba.reset();
@@ -168,6 +223,10 @@ int sfm_ba_solve(sfm_ctx* ctx, const sfm_ba_problem* prob, const sfm_ba_options*
     // a full solve ends any stepwise session: its device memory goes back
     // to the pool first, so the solve reuses it instead of growing the pool
     ctx->ba.reset();
+    if (ctx->multi()) {  // point-sharded over the context's devices
+      sfm::ba_solve_multi(ctx->group, *prob, *opt, out_cam_q, out_cam_t, out_points, report);
+      return;
+    }
     sfm::BASolver solver(ctx->stream, &ctx->prof, &ctx->comm);
     solver.setup(*prob, *opt);
     solver.iterate(opt->max_iters > 0 ? opt->max_iters : 0, report);
@@ -216,7 +275,8 @@ int sfm_iterative_map(sfm_ctx* ctx, const sfm_map_problem* prob, const sfm_map_o
                 "null argument");
     ctx->ba.reset();  // device memory back to the pool
     sfm::iterative_map(ctx->stream, &ctx->prof, *prob, *opt, out_cam_q, out_cam_t, out_X, out_mask, out_status,
-                       out_lm_track, out_n_landmarks, out_stats, out_n_stats);
+                       out_lm_track, out_n_landmarks, out_stats, out_n_stats,
+                       ctx->multi() ? &ctx->group : nullptr);
   });
 }
 

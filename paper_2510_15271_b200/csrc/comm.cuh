@@ -9,6 +9,7 @@
 #include <nccl.h>
 
 #include <condition_variable>
+#include <functional>
 #include <mutex>
 #include <vector>
 
@@ -63,12 +64,21 @@ struct EmuGroup {
   void reduce(int rank, T* d, size_t n, cudaStream_t s, int op);
   void allgather_u64(int rank, const unsigned long long* send, unsigned long long* recv, size_t n,
                      cudaStream_t s);
+  // rank q's range [off[q], off[q+1]) of every rank's d, summed in rank
+  // order, lands in rank q's d only (reduce-scatter with variable counts)
+  void reduce_ranges(int rank, double* d, const std::vector<int64_t>& off, cudaStream_t s);
+  // rank q's range of its d is copied into every rank's d (allgatherv)
+  void allgather_ranges(int rank, double* d, const std::vector<int64_t>& off, cudaStream_t s);
+  // every rank hands in `mine`; rank 0 runs fn(all ranks' pointers) on its
+  // stream, then everyone continues (one launch covering every rank)
+  void run_root(int rank, const void* mine, cudaStream_t s, const std::function<void(const void* const*)>& fn);
 };
 
 struct Comm {
   int rank = 0;
   int world = 1;
   ncclComm_t comm = nullptr;
+  bool owned = true;        // false: a communicator of a multi-device context (sfm_ctx_create_multi)
   EmuGroup* emu = nullptr;
 
   void init(int r, int w, const uint8_t* id_bytes) {
@@ -81,7 +91,7 @@ struct Comm {
     SFM_NCCL(ncclCommInitRank(&comm, w, id, r));
   }
   ~Comm() {
-    if (comm) ncclCommDestroy(comm);
+    if (comm && owned) ncclCommDestroy(comm);
   }
   bool active() const { return world > 1; }
   void sum(double* d, size_t n, cudaStream_t s) {
@@ -109,6 +119,32 @@ struct Comm {
     if (world <= 1) return;
     if (emu) return emu->allgather_u64(rank, send, recv, n_per_rank, s);
     SFM_NCCL(ncclAllGather(send, recv, n_per_rank, ncclUint64, comm, s));
+  }
+  // Reduce-scatter with variable counts: rank r ends with the sum over ranks
+  // of d[off[r] .. off[r+1]) (the block rows of S it owns); NCCL: one
+  // ncclReduce per range, rooted at its owner, in a group.
+  void reduce_ranges(double* d, const std::vector<int64_t>& off, cudaStream_t s) {
+    if (world <= 1) return;
+    if (emu) return emu->reduce_ranges(rank, d, off, s);
+    SFM_NCCL(ncclGroupStart());
+    for (int r = 0; r < world; ++r) {
+      const size_t n = (size_t)(off[r + 1] - off[r]);
+      if (n) SFM_NCCL(ncclReduce(d + off[r], d + off[r], n, ncclFloat64, ncclSum, r, comm, s));
+    }
+    SFM_NCCL(ncclGroupEnd());
+  }
+  // Allgather with variable counts: every rank receives rank r's
+  // d[off[r] .. off[r+1]) (the PCG solution rows); NCCL: one ncclBroadcast
+  // per range from its owner, in a group.
+  void allgather_ranges(double* d, const std::vector<int64_t>& off, cudaStream_t s) {
+    if (world <= 1) return;
+    if (emu) return emu->allgather_ranges(rank, d, off, s);
+    SFM_NCCL(ncclGroupStart());
+    for (int r = 0; r < world; ++r) {
+      const size_t n = (size_t)(off[r + 1] - off[r]);
+      if (n) SFM_NCCL(ncclBroadcast(d + off[r], d + off[r], n, ncclFloat64, r, comm, s));
+    }
+    SFM_NCCL(ncclGroupEnd());
   }
 };
 

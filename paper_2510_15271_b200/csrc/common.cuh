@@ -11,6 +11,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "../../include/sfm_b200.h"
 
 namespace sfm {
@@ -88,6 +90,15 @@ struct DevBuf {
   void zero(cudaStream_t s) {
     if (n) SFM_CUDA(cudaMemsetAsync(ptr, 0, n * sizeof(T), s));
   }
+};
+
+// NVTX range for Nsight timelines (setup, linearisation, trials, PCG,
+// iterative_map rounds); a no-op unless a tool is attached.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
 };
 
 // Per-kernel CUDA-event timing.  Events are recorded on the launching

@@ -22,6 +22,7 @@
 #include <vector>
 
 #include "ba.cuh"
+#include "emu.cuh"
 #include "imap.cuh"
 #include "tri.cuh"
 
@@ -140,7 +141,8 @@ struct CubScratch {
 
 void iterative_map(cudaStream_t s, Profiler* prof, const sfm_map_problem& pr, const sfm_map_options& op,
                    double* out_q, double* out_t, double* out_X, uint8_t* out_mask, int8_t* out_status,
-                   int64_t* out_lm, int64_t* out_nlm, sfm_round_stat* out_stats, int32_t* out_nstats) {
+                   int64_t* out_lm, int64_t* out_nlm, sfm_round_stat* out_stats, int32_t* out_nstats,
+                   const DeviceGroup* group) {
   SFM_REQUIRE(pr.n_frames >= 0 && pr.n_tracks >= 0 && pr.n_obs >= 0, "negative sizes");
   SFM_REQUIRE(pr.n_tracks < (1ll << 31), "n_tracks must fit in 31 bits");
   SFM_REQUIRE(op.max_outer_iters >= 0, "max_outer_iters < 0");
@@ -250,10 +252,18 @@ void iterative_map(cudaStream_t s, Profiler* prof, const sfm_map_problem& pr, co
     bo.loss_kind = loss_kind;
     bo.loss_param = loss_param;
     bo.max_iters = op.max_solver_iters;
-    BASolver solver(s, prof, nullptr);
-    solver.setup(bp, bo);
-    solver.iterate(bo.max_iters > 0 ? bo.max_iters : 0, nullptr);
-    solver.download(q.get(), t.get(), baX.get());
+    if (group && group->size() > 1) {
+      // point-sharded over the context's devices; the shards read this
+      // device's arrays and write the solution back into them
+      SFM_CUDA(cudaStreamSynchronize(s));
+      ba_solve_multi(*group, bp, bo, q.get(), t.get(), baX.get(), nullptr);
+      alloc_stream() = s;
+    } else {
+      BASolver solver(s, prof, nullptr);
+      solver.setup(bp, bo);
+      solver.iterate(bo.max_iters > 0 ? bo.max_iters : 0, nullptr);
+      solver.download(q.get(), t.get(), baX.get());
+    }
     k_lm_scatter<<<grid_for(nlm, 256), 256, 0, s>>>(nlm, lm.get(), baX.get(), X.get());
     SFM_CHECK_LAUNCH();
     tri_rt_device(s, F, q.get(), t.get(), Rt.get());
@@ -279,6 +289,7 @@ void iterative_map(cudaStream_t s, Profiler* prof, const sfm_map_problem& pr, co
   };
 
   for (int round = 0; round < op.max_outer_iters; ++round) {
+    NvtxRange nv("sfm imap round");
     // 1. RANSAC on the pending tracks (mapping.py:600-609)
     int64_t added = 0;
     if (T) {
@@ -299,6 +310,7 @@ void iterative_map(cudaStream_t s, Profiler* prof, const sfm_map_problem& pr, co
     if (added == 0 && rm == 0) break;
   }
   if (nlm) {  // mapping.py:618-622
+    NvtxRange nv("sfm imap final");
     run_ba(op.stage2_loss_kind, op.stage2_loss_param);
     const int64_t rm = gate(op.stage2_outlier_px);
     stats.push_back(sfm_round_stat{-1, 0, 0, rm, nlm});

@@ -29,10 +29,10 @@ constexpr int kPcgMaxThreads = SFM_PCG_MAXT;  // CTA size chosen at setup (512 o
 #define kPcgWarps ((int)(blockDim.x >> 5))
 
 // Block-Jacobi: inverse of each 6x6 diagonal block of S (Cholesky).
-__global__ void k_block_jacobi(int nf, const int* __restrict__ diag_pos, const double* __restrict__ S,
+__global__ void k_block_jacobi(int r0, int r1, const int* __restrict__ diag_pos, const double* __restrict__ S,
                                double* __restrict__ Minv, BAScalars* sc) {
-  int j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= nf) return;
+  int j = r0 + blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= r1) return;
   const double* Ag = S + (int64_t)diag_pos[j] * 36;
   double A[36];
 #pragma unroll
@@ -382,10 +382,7 @@ struct Pcg3Args {
   int nf, G, nc, npad, maxrows, maxsegs;
   const int* row_ptr;
   const int* col;
-  const double* S;
-  const double* Minv;
-  const double* Pm;
-  const double* Aci;       // coarse inverse [npad x npad] (nullptr: one level)
+  int two;                 // coarse level on (every rank's view has Aci)
   const int* cta_row0;     // [G+1]
   const int4* wchunk;      // [G*kPcgWarps] (k_begin, k_end, first row, first segment)
   const int2* wres;        // [G*kPcgWarps] (resident blocks at the chunk head, smem slot)
@@ -397,15 +394,9 @@ struct Pcg3Args {
   const int2* rowseg;      // [nf] (first segment local to the CTA, count)
   const int* cta_cluster;  // [G]
   const int* cluster_cta0; // [nc+1]
-  const double* b;
-  double* x;
-  double* r;
-  double* z;
-  double* p;
-  double* q;
-  double* rpart;           // [G*6] per-CTA restriction partials
-  double* part;            // [4*G]
-  BAScalars* sc;
+  int R;                   // ranks (1: single device)
+  int rcta0[kPcgMaxRanks + 1];  // first CTA of each rank
+  PcgRankView v[kPcgMaxRanks];  // per-rank buffers (pcg.cuh)
   int max_it;
   double rtol;
   int fuse_zc;
@@ -456,8 +447,9 @@ __device__ __forceinline__ double dot6_ss(const double* s, const double* v) {  /
 // the loop is the S stream itself: independent loads, no index -> z chain.
 // The head of every warp's chunk (wres.x blocks) is resident in shared
 // memory for the whole solve (Ssm).
-__device__ __forceinline__ void spmv_segments(const Pcg3Args& a, const double* zc, const int* lc, int kc0,
-                                              double* seg, const double* Ssm, const int* rpl) {
+__device__ __forceinline__ void spmv_segments(const Pcg3Args& a, const double* __restrict__ S, const double* zc,
+                                              const int* lc, int kc0, double* seg, const double* Ssm,
+                                              const int* rpl) {
   const unsigned full = 0xffffffffu;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int grp = lane / 6, comp = lane % 6;
@@ -465,6 +457,9 @@ __device__ __forceinline__ void spmv_segments(const Pcg3Args& a, const double* z
   const int2 wr = a.wres[blockIdx.x * kPcgWarps + warp];
   int kb = ch.x, r = ch.z, sidx = ch.w;
   const int ke = ch.y;
+  // an empty chunk (a CTA with fewer blocks than warps) owns no segment:
+  // its sidx is the next warp's (compute-sanitizer racecheck)
+  if (kb >= ke) return;
   const int kres = ch.x + wr.x;                    // first non-resident block
   const double* Sres = Ssm + ((int64_t)wr.y - ch.x) * 36 + comp * 6;  // Sres + k*36 for resident k
   const int* lcb = lc - kc0;                       // lcb[k] for global block k
@@ -479,7 +474,7 @@ __device__ __forceinline__ void spmv_segments(const Pcg3Args& a, const double* z
     if (lane < 30) {
       int k = kb + grp;
       for (; k + 15 < ke; k += 20) {
-        const double* s0 = a.S + (int64_t)k * 36 + comp * 6;
+        const double* s0 = S + (int64_t)k * 36 + comp * 6;
         const double d0 = dot6_sg(s0, zc + lcb[k] * 6);
         const double d1 = dot6_sg(s0 + 5 * 36, zc + lcb[k + 5] * 6);
         const double d2 = dot6_sg(s0 + 10 * 36, zc + lcb[k + 10] * 6);
@@ -490,7 +485,7 @@ __device__ __forceinline__ void spmv_segments(const Pcg3Args& a, const double* z
         if (k + 15 < bnd) a3 += d3; else b3 += d3;
       }
       for (; k < ke; k += 5) {
-        const double d = dot6_sg(a.S + (int64_t)k * 36 + comp * 6, zc + lcb[k] * 6);
+        const double d = dot6_sg(S + (int64_t)k * 36 + comp * 6, zc + lcb[k] * 6);
         if (k < bnd) a0 += d; else b0 += d;
       }
     }
@@ -525,13 +520,13 @@ __device__ __forceinline__ void spmv_segments(const Pcg3Args& a, const double* z
       }
       for (; k < rs; k += 5) acc0 += dot6_ss(Sres + (int64_t)k * 36, zc + lcb[k] * 6);
       for (; k + 15 < re; k += 20) {
-        const double* s0 = a.S + (int64_t)k * 36 + comp * 6;
+        const double* s0 = S + (int64_t)k * 36 + comp * 6;
         acc0 += dot6_sg(s0, zc + lcb[k] * 6);
         acc1 += dot6_sg(s0 + 5 * 36, zc + lcb[k + 5] * 6);
         acc2 += dot6_sg(s0 + 10 * 36, zc + lcb[k + 10] * 6);
         acc3 += dot6_sg(s0 + 15 * 36, zc + lcb[k + 15] * 6);
       }
-      for (; k < re; k += 5) acc0 += dot6_sg(a.S + (int64_t)k * 36 + comp * 6, zc + lcb[k] * 6);
+      for (; k < re; k += 5) acc0 += dot6_sg(S + (int64_t)k * 36 + comp * 6, zc + lcb[k] * 6);
     }
     double acc = (acc0 + acc1) + (acc2 + acc3);
     const double v1 = __shfl_sync(full, acc, comp + 6);
@@ -625,7 +620,8 @@ __device__ __forceinline__ double lane_partial_sum(const double* __restrict__ p,
 // (warp 0, fixed order) and, for the two-level preconditioner, the cluster
 // restriction sums (other warps), in one round trip.
 //   rc[t] = sum_c rpart (assign) or rc[t] -= scale * sum_c rpart.
-__device__ __forceinline__ void gather_after_sync(const Pcg3Args& a, const double* part, double* out, int nsum,
+__device__ __forceinline__ void gather_after_sync(const Pcg3Args& a, const double* __restrict__ rpart,
+                                                  const double* part, double* out, int nsum,
                                                   double* rc, bool two, bool assign, const double* scale_num,
                                                   const double* scale_den, const int* cc0) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -647,7 +643,7 @@ __device__ __forceinline__ void gather_after_sync(const Pcg3Args& a, const doubl
     for (int j = 0; j < 4; ++j) {
       const int t = t0 + j * tstride;
       if (t < 6 * a.nc) {
-        qs[j] = __ldcg(a.rpart + cc0[t / 6] * 6 + t % 6);
+        qs[j] = __ldcg(rpart + cc0[t / 6] * 6 + t % 6);
         nq = j + 1;
       }
     }
@@ -655,7 +651,7 @@ __device__ __forceinline__ void gather_after_sync(const Pcg3Args& a, const doubl
     for (int j = 0; j < 4; ++j) {
       const int t = t0 + j * tstride;
       if (j < nq)
-        for (int c = cc0[t / 6] + 1; c < cc0[t / 6 + 1]; ++c) qs[j] += __ldcg(a.rpart + c * 6 + t % 6);
+        for (int c = cc0[t / 6] + 1; c < cc0[t / 6 + 1]; ++c) qs[j] += __ldcg(rpart + c * 6 + t % 6);
     }
   }
   __syncthreads();
@@ -669,7 +665,7 @@ __device__ __forceinline__ void gather_after_sync(const Pcg3Args& a, const doubl
          t += kPcgThreads - 32 * nsum) {
       const int k = t / 6, mm = t % 6;
       double s = 0.0;
-      for (int c = cc0[k]; c < cc0[k + 1]; ++c) s += __ldcg(a.rpart + c * 6 + mm);
+      for (int c = cc0[k]; c < cc0[k + 1]; ++c) s += __ldcg(rpart + c * 6 + mm);
       rc[t] = assign ? s : rc[t] - alpha * s;
     }
   }
@@ -762,6 +758,17 @@ __global__ void __launch_bounds__(kPcgMaxThreads, 1) k_pcg3(Pcg3Args a) {
   if (threadIdx.x == 0) { rr_ck[0] = INFINITY; rr_ck[1] = INFINITY; }
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int G = gridDim.x;
+  // this CTA's rank and its buffers; the pushes go to every rank's replica
+  int rk = 0;
+  while (rk + 1 < a.R && (int)blockIdx.x >= a.rcta0[rk + 1]) ++rk;
+  const PcgRankView& V = a.v[rk];
+  const double* __restrict__ Sr = V.S;
+  auto push_z = [&](int64_t i, double val) {
+    for (int q = 0; q < a.R; ++q) a.v[q].z[i] = val;
+  };
+  auto push_part = [&](int64_t i, double val) {
+    for (int q = 0; q < a.R; ++q) a.v[q].part[i] = val;
+  };
   const int row0 = a.cta_row0[blockIdx.x], row1 = a.cta_row0[blockIdx.x + 1];
   const int nrows = row1 - row0;
   const int kc0 = __ldg(a.row_ptr + row0);
@@ -772,7 +779,7 @@ __global__ void __launch_bounds__(kPcgMaxThreads, 1) k_pcg3(Pcg3Args a) {
   auto fill_zc = [&](int first) {
     for (int t = threadIdx.x - first; t < 3 * ndist && t >= 0; t += kPcgThreads - first) {
       const int c = __ldg(a.zl + zl0 + t / 3);
-      reinterpret_cast<double2*>(m.zc)[t] = ldcg2(a.z + c * 6 + 2 * (t % 3));
+      reinterpret_cast<double2*>(m.zc)[t] = ldcg2(V.z + c * 6 + 2 * (t % 3));
     }
   };
   // After the r.z / r.r barrier: the scalar sums (warps 0..nsum-1) and the
@@ -813,20 +820,19 @@ __global__ void __launch_bounds__(kPcgMaxThreads, 1) k_pcg3(Pcg3Args a) {
       __syncthreads();
     }
   };
-  double* part_pq = a.part;          // [G]
-  double* part_rz = a.part + G;      // [G] followed by part_rr [G]
-  double* part_bb = a.part + 3 * G;  // [G]
-  const bool two = a.Aci != nullptr;
+  // partial-sum slots (offsets into every replica of `part`); reads use V.part
+  const int part_pq = 0, part_rz = G, part_bb = 3 * G;
+  const bool two = a.two != 0;
 
   // ---- stage the constant operators -----------------------------------------
   for (int t = threadIdx.x; t < 36 * nrows; t += kPcgThreads) {
-    m.Mi[t] = a.Minv[(int64_t)row0 * 36 + t];
-    if (two) m.Pc[t] = a.Pm[(int64_t)row0 * 36 + t];
+    m.Mi[t] = V.Minv[(int64_t)row0 * 36 + t];
+    if (two) m.Pc[t] = V.Pm[(int64_t)row0 * 36 + t];
   }
   if (two) {
     const int k = a.cta_cluster[blockIdx.x];
     for (int t = threadIdx.x; t < 6 * n6; t += kPcgThreads)
-      m.Ae[t] = a.Aci[(int64_t)(6 * k + t / n6) * a.npad + t % n6];
+      m.Ae[t] = V.Aci[(int64_t)(6 * k + t / n6) * a.npad + t % n6];
   }
   for (int t = threadIdx.x; t < nblk; t += kPcgThreads) m.lc[t] = __ldg(a.lcol + kc0 + t);
   for (int t = threadIdx.x; t < nrows; t += kPcgThreads) m.rs[t] = a.rowseg[row0 + t];
@@ -837,7 +843,7 @@ __global__ void __launch_bounds__(kPcgMaxThreads, 1) k_pcg3(Pcg3Args a) {
   for (int w = 0; w < kPcgWarps; ++w) {
     const int4 ch = a.wchunk[blockIdx.x * kPcgWarps + w];
     const int2 wr = a.wres[blockIdx.x * kPcgWarps + w];
-    const double2* src = reinterpret_cast<const double2*>(a.S + (int64_t)ch.x * 36);
+    const double2* src = reinterpret_cast<const double2*>(Sr + (int64_t)ch.x * 36);
     double2* dst = reinterpret_cast<double2*>(m.Ssm + (int64_t)wr.y * 36);
     for (int t = threadIdx.x; t < wr.x * 18; t += kPcgThreads) dst[t] = __ldg(src + t);
   }
@@ -848,7 +854,7 @@ __global__ void __launch_bounds__(kPcgMaxThreads, 1) k_pcg3(Pcg3Args a) {
     if (threadIdx.x < 6) {
       double s = 0.0;
       for (int i = 0; i < nrows; ++i) s += m.y[i * 6 + threadIdx.x];
-      a.rpart[blockIdx.x * 6 + threadIdx.x] = s;
+      for (int q = 0; q < a.R; ++q) a.v[q].rpart[blockIdx.x * 6 + threadIdx.x] = s;
     }
   };
 
@@ -860,11 +866,11 @@ __global__ void __launch_bounds__(kPcgMaxThreads, 1) k_pcg3(Pcg3Args a) {
   double gamma = 0.0;
   if (a.warm) {
     for (int i = warp; i < nrows; i += kPcgWarps)
-      if (lane < 6) a.z[(row0 + i) * 6 + lane] = a.x[(row0 + i) * 6 + lane];
+      if (lane < 6) push_z((row0 + i) * 6 + lane, V.x[(row0 + i) * 6 + lane]);
     grid.sync();
     fill_zc(0);
     __syncthreads();
-    spmv_segments(a, m.zc, m.lc, kc0, m.seg, m.Ssm, rpl);
+    spmv_segments(a, Sr, m.zc, m.lc, kc0, m.seg, m.Ssm, rpl);
     __syncthreads();
     double xb = 0.0, xw = 0.0;
     for (int i = warp; i < nrows; i += kPcgWarps)
@@ -873,14 +879,14 @@ __global__ void __launch_bounds__(kPcgMaxThreads, 1) k_pcg3(Pcg3Args a) {
         double w = 0.0;
         for (int sg = 0; sg < rs.y; ++sg) w += m.seg[(rs.x + sg) * 6 + lane];
         m.q[i * 6 + lane] = w;  // S x0, consumed by the prologue below
-        const double x0 = a.x[(row0 + i) * 6 + lane];
-        xb += x0 * a.b[(row0 + i) * 6 + lane];
+        const double x0 = V.x[(row0 + i) * 6 + lane];
+        xb += x0 * V.b[(row0 + i) * 6 + lane];
         xw += x0 * w;
       }
     const double2 t = block_sum2(xb, xw, red);
-    if (threadIdx.x == 0) { part_rz[blockIdx.x] = t.x; part_rz[G + blockIdx.x] = t.y; }
+    if (threadIdx.x == 0) { push_part(part_rz + blockIdx.x, t.x); push_part(part_rz + G + blockIdx.x, t.y); }
     grid.sync();
-    gather_after_sync(a, part_rz, sums, 2, m.rc, false, true, nullptr, nullptr, m.cc0);
+    gather_after_sync(a, V.rpart, V.part + part_rz, sums, 2, m.rc, false, true, nullptr, nullptr, m.cc0);
     const double g = sums[0] / sums[1];
     gamma = (sums[1] > 0.0 && isfinite(g)) ? g : 0.0;
   }
@@ -890,10 +896,10 @@ __global__ void __launch_bounds__(kPcgMaxThreads, 1) k_pcg3(Pcg3Args a) {
   for (int i = warp; i < nrows; i += kPcgWarps) {
     double ri = 0.0;
     if (lane < 6) {
-      const double bi = a.b[(row0 + i) * 6 + lane];
+      const double bi = V.b[(row0 + i) * 6 + lane];
       const bool ws = gamma != 0.0;
       ri = ws ? bi - gamma * m.q[i * 6 + lane] : bi;
-      m.x[i * 6 + lane] = ws ? gamma * a.x[(row0 + i) * 6 + lane] : 0.0;
+      m.x[i * 6 + lane] = ws ? gamma * V.x[(row0 + i) * 6 + lane] : 0.0;
       m.r[i * 6 + lane] = ri;
       m.p[i * 6 + lane] = 0.0;
       m.q[i * 6 + lane] = 0.0;
@@ -906,9 +912,9 @@ __global__ void __launch_bounds__(kPcgMaxThreads, 1) k_pcg3(Pcg3Args a) {
   }
   if (two) write_rpart();
   double2 sb = block_sum2(bb_l, 0.0, red);
-  if (threadIdx.x == 0) part_bb[blockIdx.x] = sb.x;
+  if (threadIdx.x == 0) push_part(part_bb + blockIdx.x, sb.x);
   grid.sync();
-  gather_after_sync(a, part_bb, sums, 1, m.rc, two, true, nullptr, nullptr, m.cc0);
+  gather_after_sync(a, V.rpart, V.part + part_bb, sums, 1, m.rc, two, true, nullptr, nullptr, m.cc0);
   const double bnorm = sqrt(sums[0]);
   stag_rr = (a.stag_slack * a.rtol * bnorm) * (a.stag_slack * a.rtol * bnorm);
   if (two) coarse_apply(a, m, e, tmp);
@@ -918,14 +924,14 @@ __global__ void __launch_bounds__(kPcgMaxThreads, 1) k_pcg3(Pcg3Args a) {
     const double zi = precond_row(m, two, i, ri, e);
     if (lane < 6) {
       m.z[i * 6 + lane] = zi;
-      a.z[(row0 + i) * 6 + lane] = zi;
+      push_z((row0 + i) * 6 + lane, zi);
       rz_l += ri * zi;
     }
   }
   double2 s1 = block_sum2(rz_l, 0.0, red);
-  if (threadIdx.x == 0) part_rz[blockIdx.x] = s1.x;
+  if (threadIdx.x == 0) push_part(part_rz + blockIdx.x, s1.x);
   grid.sync();
-  sums_and_zc(part_rz, 1, 0);
+  sums_and_zc(V.part + part_rz, 1, 0);
   double rz_old = sums[0];
   int it = 0, fail = 0, stop = PCG_STOP_MAX_ITERS;
   double beta = 0.0;
@@ -936,7 +942,7 @@ __global__ void __launch_bounds__(kPcgMaxThreads, 1) k_pcg3(Pcg3Args a) {
     PH_INIT();
     for (it = 0; it < a.max_it;) {
       // ---- phase 1: w = S z; p = z + beta p; q = w + beta q; P^T q --------
-      spmv_segments(a, m.zc, m.lc, kc0, m.seg, m.Ssm, rpl);
+      spmv_segments(a, Sr, m.zc, m.lc, kc0, m.seg, m.Ssm, rpl);
       __syncthreads();
       PH(0);
       double pq_l = 0.0;
@@ -961,13 +967,13 @@ __global__ void __launch_bounds__(kPcgMaxThreads, 1) k_pcg3(Pcg3Args a) {
       if (two) write_rpart();
       PH(9);
       const double2 s = block_sum2(pq_l, 0.0, red);
-      if (threadIdx.x == 0) part_pq[blockIdx.x] = s.x;
+      if (threadIdx.x == 0) push_part(part_pq + blockIdx.x, s.x);
       PH(10);
       PH(1);
       grid.sync();
       PH(2);
       // ---- phase 2: x += alpha p; r -= alpha q; rc -= alpha P^T q; z = M^-1 r
-      gather_after_sync(a, part_pq, sums, 1, m.rc, two, false, &rz_old, &sums[0], m.cc0);
+      gather_after_sync(a, V.rpart, V.part + part_pq, sums, 1, m.rc, two, false, &rz_old, &sums[0], m.cc0);
       const double pq = sums[0];
       if (!(pq > 0.0) || !isfinite(pq)) { fail = 1; break; }
       const double alpha = rz_old / pq;
@@ -985,17 +991,17 @@ __global__ void __launch_bounds__(kPcgMaxThreads, 1) k_pcg3(Pcg3Args a) {
         const double zi = precond_row(m, two, i, ri, e);
         if (lane < 6) {
           m.z[i * 6 + lane] = zi;
-          a.z[(row0 + i) * 6 + lane] = zi;
+          push_z((row0 + i) * 6 + lane, zi);
           rz_n += ri * zi;
           rr_n += ri * ri;
         }
       }
       const double2 t = block_sum2(rz_n, rr_n, red);
-      if (threadIdx.x == 0) { part_rz[blockIdx.x] = t.x; part_rz[G + blockIdx.x] = t.y; }
+      if (threadIdx.x == 0) { push_part(part_rz + blockIdx.x, t.x); push_part(part_rz + G + blockIdx.x, t.y); }
       PH(5);
       grid.sync();
       PH(6);
-      sums_and_zc(part_rz, 2, it + 1);
+      sums_and_zc(V.part + part_rz, 2, it + 1);
       PH(7);
       const double rz_new = sums[0], rr = sums[1];
       ++it;
@@ -1008,12 +1014,12 @@ __global__ void __launch_bounds__(kPcgMaxThreads, 1) k_pcg3(Pcg3Args a) {
     PH_DUMP(it);
   }
   for (int i = warp; i < nrows; i += kPcgWarps)
-    if (lane < 6) a.x[(row0 + i) * 6 + lane] = m.x[i * 6 + lane];
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    a.sc->pcg_iters = it;
-    a.sc->pcg_fail = fail;
-    a.sc->pcg_stop = fail ? PCG_STOP_FAILED : stop;
-    if (fail) a.sc->nonfinite = 1;
+    if (lane < 6) V.x[(row0 + i) * 6 + lane] = m.x[i * 6 + lane];
+  if ((int)blockIdx.x == a.rcta0[rk] && threadIdx.x == 0) {  // every rank's scalars
+    V.sc->pcg_iters = it;
+    V.sc->pcg_fail = fail;
+    V.sc->pcg_stop = fail ? PCG_STOP_FAILED : stop;
+    if (fail) V.sc->nonfinite = 1;
   }
 }
 
@@ -1074,24 +1080,42 @@ void TwoLevelPcg::set_pattern(const int* row_ptr, const int* col, int nnzb, cuda
   per_sm = std::max(1, std::min(per_sm, 1024 / nt_));
   if (const char* e = std::getenv("SFM_PCG_PERSM")) per_sm = std::max(1, std::min(per_sm, std::atoi(e)));
   int G = std::min(per_sm * nsm, nf_);
-  std::vector<int> row0;
-  for (;;) {
-    row0.assign(1, 0);
-    for (int c = 1; c < G; ++c) {
-      const int64_t target = total * c / G;
-      int lo = row0.back() + 1, hi = nf_ - (G - c);  // keep >= 1 row per CTA
-      int r = lo;
-      // first row whose prefix cost reaches target
-      int a0 = lo, b0 = hi;
-      while (a0 < b0) {
-        int m = (a0 + b0) / 2;
-        if (cost_upto(m) < target) a0 = m + 1; else b0 = m;
-      }
-      r = std::min(std::max(a0, lo), hi);
-      row0.push_back(r);
+  // first row in [lo, hi] whose prefix cost reaches target
+  auto row_at = [&](int64_t target, int lo, int hi) {
+    int a0 = lo, b0 = hi;
+    while (a0 < b0) {
+      int m = (a0 + b0) / 2;
+      if (cost_upto(m) < target) a0 = m + 1; else b0 = m;
     }
-    row0.push_back(nf_);
-    break;
+    return std::min(std::max(a0, lo), hi);
+  };
+  // ranks (row-partitioned solve): contiguous row ranges balanced by cost,
+  // then CTAs per rank in proportion, each rank's rows split over its CTAs
+  const int R = std::max(1, std::min(world_, G));
+  SFM_REQUIRE(R == world_, "row-partitioned PCG: fewer block rows than ranks");
+  rank_row0_.assign(1, 0);
+  for (int r = 1; r < R; ++r) rank_row0_.push_back(row_at(total * r / R, rank_row0_.back() + 1, nf_ - (R - r)));
+  rank_row0_.push_back(nf_);
+  rank_cta0_.assign(1, 0);
+  for (int r = 1; r < R; ++r) {
+    const int64_t c0 = cost_upto(rank_row0_[r]);
+    int cr = (int)((G * c0 + total / 2) / std::max<int64_t>(total, 1));
+    cr = std::max(cr, rank_cta0_.back() + 1);
+    cr = std::min(cr, rank_row0_[r]);                 // <= rows before it
+    cr = std::max(cr, G - (nf_ - rank_row0_[r]));     // >= 1 row per CTA after it
+    cr = std::min(cr, G - (R - r));                   // >= 1 CTA per later rank
+    rank_cta0_.push_back(cr);
+  }
+  rank_cta0_.push_back(G);
+  rank_blk0_.resize(R + 1);
+  for (int r = 0; r <= R; ++r) rank_blk0_[r] = rp[rank_row0_[r]];
+  std::vector<int> row0(1, 0);
+  for (int r = 0; r < R; ++r) {
+    const int ca = rank_cta0_[r], cb = rank_cta0_[r + 1], ra = rank_row0_[r], rb = rank_row0_[r + 1];
+    const int64_t ta = cost_upto(ra), tb = cost_upto(rb);
+    for (int c = ca + 1; c < cb; ++c)
+      row0.push_back(row_at(ta + (tb - ta) * (c - ca) / (cb - ca), row0.back() + 1, rb - (cb - c)));
+    row0.push_back(rb);
   }
   mark("partition");
   // ---- per-warp chunks and segments ----------------------------------------
@@ -1156,8 +1180,20 @@ void TwoLevelPcg::set_pattern(const int* row_ptr, const int* col, int nnzb, cuda
   // ---- coarse clusters = groups of consecutive CTAs -------------------------
   const bool two = cluster_ > 0;
   nc_ = two ? std::min(G, std::max(1, (nf_ + cluster_ - 1) / cluster_)) : 1;
+  // clusters never straddle a rank: each rank gets its share of them
+  std::vector<int> rank_nc0(1, 0);
+  for (int r = 0; r < R; ++r) {
+    const int gr = rank_cta0_[r + 1] - rank_cta0_[r];
+    int nr = R == 1 ? nc_ : std::max(1, std::min(gr, (int)(((int64_t)nc_ * gr + G / 2) / G)));
+    rank_nc0.push_back(rank_nc0.back() + nr);
+  }
+  nc_ = rank_nc0.back();
   std::vector<int> cta_cluster(G), cluster_cta0(nc_ + 1), frame_cluster(nf_);
-  for (int k = 0; k <= nc_; ++k) cluster_cta0[k] = (int)((int64_t)G * k / nc_);
+  for (int r = 0; r < R; ++r) {
+    const int ca = rank_cta0_[r], gr = rank_cta0_[r + 1] - ca, k0 = rank_nc0[r], nr = rank_nc0[r + 1] - k0;
+    for (int k = 0; k < nr; ++k) cluster_cta0[k0 + k] = ca + (int)((int64_t)gr * k / nr);
+  }
+  cluster_cta0[nc_] = G;
   for (int k = 0; k < nc_; ++k)
     for (int c = cluster_cta0[k]; c < cluster_cta0[k + 1]; ++c) {
       cta_cluster[c] = k;
@@ -1269,6 +1305,13 @@ void TwoLevelPcg::set_pattern(const int* row_ptr, const int* col, int nnzb, cuda
     }
     if (!rr.empty()) ptr.push_back((int)runs.size());
     npairs_ = (int)cd.size();
+    rank_pair0_.assign(R + 1, npairs_);
+    for (int r = R - 1; r >= 0; --r) {
+      int q = 0;
+      while (q < npairs_ && cd[q].x < rank_nc0[r]) ++q;
+      rank_pair0_[r] = q;
+    }
+    rank_pair0_[R] = npairs_;
     mark("coarse runs");
     pair_cd_.upload(cd.data(), cd.size(), s);
     pair_ptr_.upload(ptr.data(), ptr.size(), s);
@@ -1296,11 +1339,18 @@ void TwoLevelPcg::set_basis(const int* free_frame, const double* q, const double
 }
 
 void TwoLevelPcg::solve(const PcgProblem& p, int max_it, double rtol, BAScalars* sc, cudaStream_t s,
-                        Profiler* prof) {
+                        Profiler* prof, PcgCollective* coll) {
   if (nf_ <= 0) return;
+  NvtxRange nv("sfm pcg");
+  // row-partitioned over the ranks of `coll` (the caller reduce-scattered S
+  // and b by rank_rows()); otherwise every row is this rank's
+  const bool parted = coll && world_ > 1;
+  SFM_REQUIRE(!parted || (coll->world() == world_ && coll->rank() == rank_), "PCG partition / collective mismatch");
+  const int my = parted ? rank_ : 0;
+  const int r0 = parted ? rank_row0_[my] : 0, r1 = parted ? rank_row0_[my + 1] : nf_;
   {
     ProfScope ps(*prof, "block_jacobi", 0.0, s);
-    k_block_jacobi<<<grid_for(nf_, 64), 64, 0, s>>>(nf_, p.diag_pos, p.S, Minv_.get(), sc);
+    if (r1 > r0) k_block_jacobi<<<grid_for(r1 - r0, 64), 64, 0, s>>>(r0, r1, p.diag_pos, p.S, Minv_.get(), sc);
   }
   // The coarse operator A_c = P^T S(lam) P depends on the damping: S(lam)
   // has lam*D_c on its diagonal and (V + lam D_p)^-1 in its point term.  An
@@ -1333,11 +1383,15 @@ void TwoLevelPcg::solve(const PcgProblem& p, int max_it, double rtol, BAScalars*
     {
       ProfScope ps(*prof, "coarse_assemble", 288.0 * p.nnzb, s);
       SFM_CUDA(cudaMemsetAsync(Ac_[0].get(), 0, sizeof(double) * (size_t)npad_ * npad_, s));
-      if (npairs_)
-        k_coarse_assemble<<<grid_for((int64_t)npairs_ * 32, 128), 128, 0, s>>>(
-            npairs_, npad_, pair_cd_.get(), pair_ptr_.get(), runs_.get(), p.col, p.S, Pm_.get(), Ac_[0].get());
-      if (npad_ > 6 * nc_)
+      // the coarse blocks (c, d) of this rank's clusters (rows of S it holds)
+      const int q0 = parted ? rank_pair0_[my] : 0, q1 = parted ? rank_pair0_[my + 1] : npairs_;
+      if (q1 > q0)
+        k_coarse_assemble<<<grid_for((int64_t)(q1 - q0) * 32, 128), 128, 0, s>>>(
+            q1 - q0, npad_, pair_cd_.get() + q0, pair_ptr_.get() + q0, runs_.get(), p.col, p.S, Pm_.get(),
+            Ac_[0].get());
+      if (npad_ > 6 * nc_ && my == 0)
         k_pad_identity<<<1, 256, 0, s>>>(6 * nc_, npad_, Ac_[0].get());
+      if (parted) coll->sum(Ac_[0].get(), (size_t)npad_ * npad_, s);  // disjoint rows: exact
     }
     double* A0 = Ac_[0].get();
     double* A1 = Ac_[1].get();
@@ -1354,22 +1408,32 @@ void TwoLevelPcg::solve(const PcgProblem& p, int max_it, double rtol, BAScalars*
   }
   Pcg3Args a{};
   a.nf = nf_; a.G = grid_; a.nc = nc_; a.npad = npad_; a.maxrows = maxrows_; a.maxsegs = maxsegs_;
-  a.row_ptr = p.row_ptr; a.col = p.col; a.S = p.S; a.Minv = Minv_.get(); a.Pm = Pm_.get();
-  a.Aci = coarse_on ? Aci_ : nullptr;
+  a.row_ptr = p.row_ptr; a.col = p.col;
+  a.two = coarse_on ? 1 : 0;
   a.stag_slack = 100.0;
   a.cta_row0 = cta_row0_.get(); a.wchunk = wchunk_.get();
   a.wres = wres_.get(); a.resblocks = resblocks_;
   a.lcol = lcol_.get(); a.zl_ptr = zl_ptr_.get(); a.zl = zl_.get(); a.maxblk = maxblk_; a.maxdist = maxdist_; a.rowseg = rowseg_.get();
   a.cta_cluster = cta_cluster_.get(); a.cluster_cta0 = cluster_cta0_.get();
-  a.b = p.b; a.x = p.x; a.r = r_.get(); a.z = z_.get(); a.p = p_.get(); a.q = q_.get();
-  a.rpart = rpart_.get(); a.part = part_.get(); a.sc = sc; a.max_it = max_it; a.rtol = rtol;
+  a.max_it = max_it; a.rtol = rtol;
   a.fuse_zc = 1;
   a.warm = have_prev_ && warm_ ? 1 : 0;
   have_prev_ = true;
   if (const char* e = std::getenv("SFM_PCG_FUSEZC")) a.fuse_zc = std::atoi(e);
-  void* args[] = {&a};
+  PcgRankView mine{};
+  mine.S = p.S; mine.b = p.b; mine.x = p.x; mine.Minv = Minv_.get(); mine.Pm = Pm_.get();
+  mine.Aci = coarse_on ? Aci_ : nullptr; mine.z = z_.get(); mine.part = part_.get(); mine.rpart = rpart_.get();
+  mine.sc = sc;
   ProfScope ps(*prof, "pcg", 0.0, s);
-  SFM_CUDA(cudaLaunchCooperativeKernel((void*)k_pcg3, grid_, nt_, args, smem_, s));
+  auto launch = [&](const PcgRankView* views) {
+    a.R = parted ? world_ : 1;
+    for (int r = 0; r < a.R; ++r) a.v[r] = views[r];
+    for (int r = 0; r <= a.R; ++r) a.rcta0[r] = parted ? rank_cta0_[r] : (r ? grid_ : 0);
+    void* args[] = {&a};
+    SFM_CUDA(cudaLaunchCooperativeKernel((void*)k_pcg3, grid_, nt_, args, smem_, s));
+  };
+  if (parted) coll->launch_all(mine, s, launch);
+  else launch(&mine);
 }
 
 }  // namespace sfm

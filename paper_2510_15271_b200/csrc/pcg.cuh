@@ -12,11 +12,52 @@
 // The Krylov loop is one persistent cooperative kernel with two grid
 // barriers per iteration; every reduction has a fixed order.
 #pragma once
+#include <functional>
+#include <vector>
+
 #include "common.cuh"
 
 namespace sfm {
 
 struct BAScalars;
+
+// ---- row-partitioned PCG over R ranks (north-star variant)
+// Rank r owns the block rows [row0[r], row0[r+1]) of S (reduce-scattered by
+// the caller) and the CTAs of those rows.  Inside the persistent kernel a CTA
+// reads S, b, x, M^-1 and A_c^-1 from its own rank's buffers and PUSHES what
+// the other ranks need -- its rows of z and its partial sums -- into every
+// rank's replica before each grid barrier (the allgather of z and the
+// allreduce of the dot products, fused into the Krylov loop), so every read
+// after a barrier is rank-local.
+constexpr int kPcgMaxRanks = 16;
+
+struct PcgRankView {       // one rank's buffers for one solve
+  const double* S;         // [nnzb*36]  valid in the rank's rows
+  const double* b;         // [nf*6]     valid in the rank's rows
+  double* x;               // [nf*6]     written in the rank's rows (warm start read there)
+  const double* Minv;      // [nf*36]    block-Jacobi inverses of the rank's rows
+  const double* Pm;        // [nf*36]    coarse basis (all rows)
+  const double* Aci;       // [npad^2]   coarse inverse (replicated), null = one level
+  double* z;               // [nf*6]     replica of z (every CTA pushes its rows here)
+  double* part;            // [4G]       replica of the per-CTA scalar partials
+  double* rpart;           // [6G]       replica of the per-CTA restriction partials
+  BAScalars* sc;           // the rank's scalars (iterations, stop reason, failure)
+};
+
+// How a rank's TwoLevelPcg meets the others (implemented over Comm in ba.cu).
+class PcgCollective {
+ public:
+  virtual ~PcgCollective() = default;
+  virtual int rank() const = 0;
+  virtual int world() const = 0;
+  // sum over ranks, result on every rank (the coarse operator A_c)
+  virtual void sum(double* d, size_t n, cudaStream_t s) = 0;
+  // every rank hands in its view; `launch` runs once with all R views
+  // (shard emulation: rank 0 launches one cooperative kernel covering every
+  // rank's CTAs on the shared device)
+  virtual void launch_all(const PcgRankView& mine, cudaStream_t s,
+                          const std::function<void(const PcgRankView*)>& launch) = 0;
+};
 
 // Why a PCG solve stopped (BAScalars::pcg_stop).
 enum { PCG_STOP_CONVERGED = 0, PCG_STOP_MAX_ITERS = 1, PCG_STOP_STAGNATED = 2, PCG_STOP_FAILED = 3 };
@@ -37,6 +78,13 @@ class TwoLevelPcg {
  public:
   // cluster <= 0 disables the coarse level (plain block-Jacobi).
   void setup(int nf, int cluster, int refresh, cudaStream_t s);
+  // Row-partitioned solve over `world` ranks (call before set_pattern):
+  // the CTA partition and the coarse clusters are cut at the rank row
+  // boundaries, which rank_rows() / rank_blocks() then report.
+  void set_partition(int world, int rank) { world_ = std::max(1, world); rank_ = rank; }
+  int world() const { return world_; }
+  const std::vector<int>& rank_rows() const { return rank_row0_; }    // [world+1]
+  const std::vector<int>& rank_blocks() const { return rank_blk0_; }  // [world+1]
   // Coarse assembly runs from the (fixed) BSR pattern of S.
   void set_pattern(const int* row_ptr, const int* col, int nnzb, cudaStream_t s);
   // Coarse basis P_j = Adj(T_j) from the linearisation-point poses.
@@ -47,7 +95,7 @@ class TwoLevelPcg {
   void set_coarse_policy(double lam_max, double drift) { lam_max_ = lam_max; drift_ = drift; }
   // Solves S x = b; writes iteration count / stop reason / failure into sc.
   void solve(const PcgProblem& p, int max_it, double rtol, BAScalars* sc, cudaStream_t s,
-             Profiler* prof);
+             Profiler* prof, PcgCollective* coll = nullptr);
   int last_grid() const { return grid_; }
   // Forget the coarse operator and the warm-start solution (a new solve).
   void restart() { lin_count_ = 0; coarse_valid_ = false; have_prev_ = false; }
@@ -57,6 +105,8 @@ class TwoLevelPcg {
   int maxrows_ = 0, maxsegs_ = 0, nt_ = 512, refresh_ = 1, lin_count_ = 0, resblocks_ = 0, maxdist_ = 1, maxblk_ = 1;
   size_t smem_ = 0;
   int npairs_ = 0;
+  int world_ = 1, rank_ = 0;
+  std::vector<int> rank_row0_, rank_blk0_, rank_cta0_, rank_pair0_;
   bool coarse_valid_ = false;
   double lam_build_ = 0.0, lam_max_ = 1e-2, drift_ = 4.0;
   double lam_floor_ = 1e-5;   // dampings below this count as equal (coarse rebuild rule)

@@ -262,19 +262,23 @@ def test_dropin_bundle_adjust_objects(golden):
     np.testing.assert_allclose(X, d["ref_points"], atol=1e-8)
 
 
-@pytest.mark.parametrize("n_shards", [2, 3, 4])
-def test_point_sharded_solve_matches_single_rank(n_shards):
+@pytest.mark.parametrize("partition", [True, False])
+@pytest.mark.parametrize("n_shards", [2, 3, 4, 8])
+def test_point_sharded_solve_matches_single_rank(n_shards, partition):
     """SURVEY.md §8(e) on one B200: n logical ranks run the multi-GPU
     control flow (point shards balanced by observation count, partial Schur
-    complements reduced, replicated PCG, reduced scalars); the result equals
-    the single-rank solve and the oracle's."""
+    complements reduced -- reduce-scattered by block rows into the
+    row-partitioned PCG (partition=True: z and the dot products pushed
+    between the ranks inside the Krylov kernel, the solution allgathered) or
+    all-reduced into the replicated PCG -- reduced scalars); the result
+    equals the single-rank solve and the oracle's."""
     from oracle import ba as OB
     from paper_2510_15271_b200.mapping import solve_arrays, solve_sharded_emulated
     from paper_2510_15271_b200.scenes import make_scene, scene_arrays
     from paper_2510_15271_b200.solver import DeviceOptions, RobustLoss, SolverOptions
     a = scene_arrays(make_scene(120, 12000, 60000, shape="venice", seed=8))
     loss, sopt = RobustLoss("huber", 2.0), SolverOptions(max_iters=5)
-    dopt = DeviceOptions(linear_solver="pcg", pcg_rtol=1e-12)
+    dopt = DeviceOptions(linear_solver="pcg", pcg_rtol=1e-12, pcg_partition=partition)
     q1, t1, X1, r1, _ = solve_arrays(a, loss, sopt, dopt)
     qs, ts, Xs, rs, raw = solve_sharded_emulated(a, loss, sopt, dopt, n_shards)
     assert raw.kernel_launches > 0
