@@ -34,6 +34,7 @@ extern "C" {
 #define SFM_E_OUT_OF_MODEL_DOMAIN (-3)/* OutOfModelDomain   cameras.py:68-69   */
 #define SFM_E_SOLVER_DIVERGED (-4)    /* SolverDiverged     solver.py:247-248  */
 #define SFM_E_UNDISTORT_DIVERGED (-5) /* UndistortDiverged  cameras.py:119-125 */
+#define SFM_E_NO_GAUGE (-6)           /* NoGauge            mapping.py:408-409 (iterative_map's BA) */
 #define SFM_E_CUDA (-10)              /* CUDA runtime failure                  */
 #define SFM_E_NCCL (-11)              /* NCCL failure                          */
 #define SFM_E_OOM (-12)               /* device allocation failure             */
@@ -44,9 +45,10 @@ extern "C" {
 #define SFM_TRI_CHEIRALITY 2            /* CheiralityViolation  mapping.py:186-191 */
 #define SFM_TRI_PARALLEL_RAYS 3         /* ParallelRays         mapping.py:236-237 */
 #define SFM_TRI_TOO_FEW_OBS 4           /* ValueError           mapping.py:202-203 */
-#define SFM_TRI_CAMERA_ERROR 5          /* unproject raised (UndistortDiverged / OutOfModelDomain) */
+#define SFM_TRI_CAMERA_ERROR 5          /* unproject raised UndistortDiverged cameras.py:119-125 */
 #define SFM_TRI_FAILED 6                /* ransac: track.status = FAILED mapping.py:286-303 */
 #define SFM_TRI_SKIPPED 7               /* track not active (not PENDING)       */
+#define SFM_TRI_CAMERA_DOMAIN 8         /* unproject raised OutOfModelDomain cameras.py:106-108 */
 
 /* ---- camera models: cameras.py:35-54 -------------------------------------- */
 #define SFM_CAM_PINHOLE 0

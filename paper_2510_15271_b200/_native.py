@@ -24,6 +24,7 @@ SFM_E_NON_POSITIVE_DEPTH = -2
 SFM_E_OUT_OF_MODEL_DOMAIN = -3
 SFM_E_SOLVER_DIVERGED = -4
 SFM_E_UNDISTORT_DIVERGED = -5
+SFM_E_NO_GAUGE = -6
 SFM_E_CUDA = -10
 SFM_E_NCCL = -11
 SFM_E_OOM = -12
@@ -36,6 +37,7 @@ TRI_TOO_FEW_OBS = 4
 TRI_CAMERA_ERROR = 5
 TRI_FAILED = 6
 TRI_SKIPPED = 7
+TRI_CAMERA_DOMAIN = 8
 
 CAM_KINDS = {"pinhole": 0, "pinhole_radial": 1, "equidistant_fisheye": 2}
 LOSS_KINDS = {"trivial": 0, "huber": 1, "cauchy": 2}
@@ -43,6 +45,12 @@ LINSOLVE = {"auto": 0, "dense": 1, "pcg": 2}
 TERMINATIONS = ("max_iterations", "gradient_tolerance", "no_decrease",
                 "parameter_tolerance", "cost_zero", "all_fixed")
 TRI_METHODS = {"dlt": 0, "midpoint": 1}
+
+
+def tri_method(method: str) -> int:
+    """ransac_triangulate's `method` (mapping.py:270-278): "dlt" is the DLT,
+    every other value the midpoint method."""
+    return 0 if method == "dlt" else 1
 
 EXPORTED_SYMBOLS = (
     "sfm_abi_version", "sfm_nccl_unique_id", "sfm_ctx_create", "sfm_ctx_create_multi",

@@ -218,8 +218,13 @@ void iterative_map(cudaStream_t s, Profiler* prof, const sfm_map_problem& pr, co
     return h;
   };
 
+  // bundle_adjust's gauge check (mapping.py:408-409): it runs only once
+  // there are landmarks, so an empty map never raises
+  bool gauge = pr.n_priors > 0 && pr.prior_weight > 0.0;
+  for (int f = 0; f < F && !gauge; ++f) gauge = pr.frame_fixed[f] != 0;
   auto run_ba = [&](int loss_kind, double loss_param) {
     if (nlm == 0) return;
+    if (!gauge) throw SfmError(SFM_E_NO_GAUGE, "no fixed pose and no absolute prior");
     cnt.resize(nlm + 1);
     off.resize(nlm + 1);
     k_lm_count<<<grid_for(nlm + 1, 256), 256, 0, s>>>(nlm, lm.get(), ptr.get(), mask.get(), cnt.get());

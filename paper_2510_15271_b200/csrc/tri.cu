@@ -241,7 +241,7 @@ __device__ int tri_solve(const TriData& d, const Sel& s, int method, double min_
   for (int64_t o = s.b0; o < s.b1; ++o) {
     if (!s(o)) continue;
     ++n;
-    if (d.ray_st[o] != PROJ_OK) return SFM_TRI_CAMERA_ERROR;
+    if (d.ray_st[o] != PROJ_OK) return d.ray_st[o] == PROJ_DOMAIN ? SFM_TRI_CAMERA_DOMAIN : SFM_TRI_CAMERA_ERROR;
   }
   if (n < 2) return SFM_TRI_TOO_FEW_OBS;
   if (check_angle && max_ray_angle(d, s) < min_angle) return SFM_TRI_INSUFFICIENT_PARALLAX;

@@ -75,6 +75,8 @@ def raise_for_code(code: int, message: str):
         raise UndistortDiverged(message)
     if code == n.SFM_E_SOLVER_DIVERGED:
         raise SolverDiverged(message)
+    if code == n.SFM_E_NO_GAUGE:
+        raise NoGauge(message)
     if code == n.SFM_E_INVALID:
         raise ValueError(message)
     if code == n.SFM_E_OOM:
@@ -97,4 +99,6 @@ def raise_for_tri_status(status: int):
         raise ValueError("need at least two observations")
     if status == n.TRI_CAMERA_ERROR:
         raise UndistortDiverged("unprojection failed")
+    if status == n.TRI_CAMERA_DOMAIN:
+        raise OutOfModelDomain("distorted radius beyond 90 deg")
     raise RuntimeError(f"triangulation status {status}")

@@ -635,7 +635,7 @@ def _tri_call(observations, poses, cameras, method, min_angle, ctx):
     st = np.empty(1, dtype=np.int8)
     s = ta.struct()
     ctx.check(ctx.lib.sfm_triangulate(ctx.handle, ctypes.byref(s), float(min_angle),
-                                      nat.TRI_METHODS[method], nat.ptr(X), nat.ptr(st)))
+                                      nat.tri_method(method), nat.ptr(X), nat.ptr(st)))
     raise_for_tri_status(int(st[0]))
     return X[0].copy()
 
@@ -664,7 +664,7 @@ def ransac_triangulate_batch(tracks, poses, cameras, threshold_px=4.0,
     st = np.empty(T, dtype=np.int8)
     s = ta.struct()
     ctx.check(ctx.lib.sfm_ransac_triangulate(ctx.handle, ctypes.byref(s), float(threshold_px),
-                                             float(min_angle), nat.TRI_METHODS[method], nat.ptr(X),
+                                             float(min_angle), nat.tri_method(method), nat.ptr(X),
                                              nat.ptr(mask), nat.ptr(st)))
     out = []
     for i, tr in enumerate(tracks):
@@ -755,7 +755,7 @@ def _map_options(config: MappingConfig, device: DeviceOptions) -> nat.MapOptions
         nat.LOSS_KINDS[config.stage1.loss.kind], nat.LOSS_KINDS[config.stage2.loss.kind],
         float(config.stage1.loss.param), float(config.stage2.loss.param),
         float(config.stage1.outlier_px), float(config.stage2.outlier_px),
-        float(config.min_triangulation_angle), nat.TRI_METHODS[config.triangulation], 0,
+        float(config.min_triangulation_angle), nat.tri_method(config.triangulation), 0,
         _options(TRIVIAL_LOSS, SolverOptions(max_iters=config.max_solver_iters), dev))
 
 
@@ -861,8 +861,8 @@ def iterative_map(keyframes, tracks, cameras, config: MappingConfig = None, rig=
     fixed = set(sparse_map.fixed_frames)
     if mode == LOCALIZATION_FIXED:
         fixed |= {f for f in frames if sparse_map.provenance.get(f) == "prior"}
-    if mode != RIG_EXTRINSIC and not fixed and config.lambda_a <= 0:
-        raise NoGauge("no fixed pose and no absolute prior")
+    # NoGauge comes out of the first bundle_adjust that has landmarks
+    # (mapping.py:408-409 via :611), raised by the device loop (SFM_E_NO_GAUGE)
     fidx = {f: i for i, f in enumerate(frames)}
     cam_q = np.array([kf_map[f].cam_from_world.quat for f in frames]).reshape(-1, 4)
     cam_t = np.array([kf_map[f].cam_from_world.t for f in frames]).reshape(-1, 3)

@@ -277,3 +277,42 @@ def test_dropin_map_writes_reference_map_bin(tmp_path, golden):
     back = RIO.read_map(tmp_path / "ours.bin")
     assert len(back.landmarks) == len(ours.landmarks)
     np.testing.assert_array_equal(np.array([lm.position for lm in back.landmarks]), d["ref_lm_X"])
+
+
+def _io_map(golden):
+    """The map of tests/golden/make_io_golden.py in this package's objects."""
+    from paper_2510_15271_b200 import (CameraModel, Keyframe, Landmark, Observation, Pose,
+                                       SparseMap, Track)
+    d = golden("iterative_map")
+    ptr, lm_track = d["track_ptr"], d["ref_lm_track"]
+    masks = np.split(d["ref_lm_mask"].astype(bool),
+                     np.cumsum([ptr[t + 1] - ptr[t] for t in lm_track])[:-1])
+    cams = {0: CameraModel("pinhole", 500.0, 500.0, 320.0, 240.0, 640, 480),
+            1: CameraModel("pinhole_radial", 480.0, 490.0, 321.5, 239.5, 640, 480, (-0.05, 0.01))}
+    F = len(d["cam_q"])
+    kfs = {f: Keyframe(f, 0.1 * f, f % 2, Pose(d["ref_cam_q"][f], d["ref_cam_t"][f]),
+                       image_path=f"img/{f:04d}.jpg" if f % 3 else "") for f in range(F)}
+    lms = []
+    for i, t in enumerate(lm_track):
+        obs = [Observation(int(d["obs_frame"][o]), int(o), d["obs_uv"][o]) for o in range(ptr[t], ptr[t + 1])]
+        lms.append(Landmark(d["ref_lm_X"][i], Track(obs, status="triangulated"), masks[i]))
+    return SparseMap(kfs, cams, lms, None, {1: "prior"}, {0})
+
+
+def test_map_bin_writer_matches_reference_bytes(tmp_path, golden):
+    """paper_2510_15271_b200.io.write_map: the same bytes as sfmkit's
+    write_map (io.py:508-537, CRC32 container io.py:348-361) on the same map
+    (tests/golden/io_writers.npz from tests/golden/make_io_golden.py), and
+    read_map round-trips it."""
+    from paper_2510_15271_b200 import io as SIO
+    g = golden("io_writers")
+    m = _io_map(golden)
+    SIO.write_map(m, tmp_path / "map.bin")
+    assert (tmp_path / "map.bin").read_bytes() == g["map_bin"].tobytes()
+    back = SIO.read_map(tmp_path / "map.bin")
+    assert SIO.map_bytes(back) == g["map_bin"].tobytes()
+    bad = bytearray(g["map_bin"].tobytes())
+    bad[40] ^= 1
+    (tmp_path / "bad.bin").write_bytes(bytes(bad))
+    with pytest.raises(SIO.ChecksumMismatch):
+        SIO.read_map(tmp_path / "bad.bin")

@@ -92,3 +92,51 @@ def test_bundle_adjust_points_only(golden):
     assert rep.iterations == int(d["e6_iters"])
     assert rep.final_cost == pytest.approx(float(d["e6_cost"]), rel=1e-6)
     np.testing.assert_allclose([lm.position for lm in smap.landmarks], d["e6_X"], rtol=1e-7, atol=1e-8)
+
+
+def test_iterative_map_empty_without_gauge():
+    """sfmkit raises NoGauge only from a bundle_adjust that has landmarks
+    (mapping.py:408-409, reached through :611): with no keyframes and
+    lambda_a = 0 it returns an empty map with one empty round (sfmkit:
+    [{'round': 0, 'added': 0, 'removed': 0, 'landmarks': 0}])."""
+    smap = iterative_map([], [], {}, MappingConfig(lambda_a=0.0))
+    assert smap.round_stats == [{"round": 0, "added": 0, "removed": 0, "landmarks": 0}]
+    assert smap.landmarks == [] and smap.fixed_frames == set()
+
+
+def test_triangulate_fisheye_beyond_model_domain():
+    """unproject of a fisheye pixel whose distorted radius is beyond 90 deg
+    raises OutOfModelDomain (cameras.py:106-108), not UndistortDiverged --
+    sfmkit's triangulate_dlt on these inputs: OutOfModelDomain('distorted
+    radius beyond 90 deg')."""
+    from paper_2510_15271_b200 import OutOfModelDomain, triangulate_dlt, triangulate_midpoint
+    cam = CameraModel("equidistant_fisheye", 300.0, 300.0, 320.0, 240.0, 640, 480)
+    poses = {0: Pose(), 1: Pose(np.array([1, 0, 0, 0.0]), np.array([-1.0, 0, 0]))}
+    cams = {0: cam, 1: cam}
+    obs = [Observation(0, 0, np.array([320 + 300 * 1.7, 240.0])), Observation(1, 0, np.array([300.0, 240.0]))]
+    with pytest.raises(OutOfModelDomain):
+        triangulate_dlt(obs, poses, cams)
+    with pytest.raises(OutOfModelDomain):
+        triangulate_midpoint(obs, poses, cams)
+
+
+def test_ransac_unknown_method_is_midpoint(golden):
+    """ransac_triangulate treats every method other than "dlt" as the
+    midpoint method (mapping.py:270-278)."""
+    from paper_2510_15271_b200 import ransac_triangulate
+    d = golden("tri_midpoint")
+    cam = CameraModel("pinhole", 500.0, 500.0, 320.0, 240.0, 640, 480)
+    F = len(d["cam_q"])
+    poses = {f: Pose(d["cam_q"][f], d["cam_t"][f]) for f in range(F)}
+    cams = {f: cam for f in range(F)}
+    ptr = d["track_ptr"]
+    for i in range(min(20, len(ptr) - 1)):
+        obs = [Observation(int(d["obs_frame"][o]), 0, d["obs_uv"][o]) for o in range(ptr[i], ptr[i + 1])]
+        a = ransac_triangulate(Track(list(obs)), poses, cams, threshold_px=float(d["threshold_px"]),
+                               min_angle=float(d["min_angle"]), method="midpoint")
+        b = ransac_triangulate(Track(list(obs)), poses, cams, threshold_px=float(d["threshold_px"]),
+                               min_angle=float(d["min_angle"]), method="anything-else")
+        assert (a is None) == (b is None)
+        if a is not None:
+            assert np.array_equal(a.position, b.position)
+            assert np.array_equal(a.inlier_mask, b.inlier_mask)

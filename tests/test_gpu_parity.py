@@ -368,3 +368,18 @@ def test_rig_and_rolling_shutter_ba_match_reference(golden, case):
         ids = [int(c) for c in d["rig_ids"]]
         np.testing.assert_allclose([smap.rig.extrinsic(c).quat for c in ids], d["ref_rig_q"], atol=1e-7)
         np.testing.assert_allclose([smap.rig.extrinsic(c).t for c in ids], d["ref_rig_t"], atol=1e-6)
+
+
+def test_colmap_writer_matches_reference_bytes(tmp_path, golden):
+    """paper_2510_15271_b200.io.write_colmap_sparse (reprojection errors from
+    the device) writes the same three files as sfmkit's write_colmap_sparse
+    (io.py:271-337) on the same map (tests/golden/make_io_golden.py)."""
+    import sys
+    sys.path.insert(0, __import__("os").path.dirname(__file__))
+    from test_cpu_host import _io_map
+    from paper_2510_15271_b200 import io as SIO
+    g = golden("io_writers")
+    SIO.write_colmap_sparse(_io_map(golden), tmp_path)
+    for name, key in (("cameras.txt", "cameras_txt"), ("images.txt", "images_txt"),
+                      ("points3D.txt", "points3d_txt")):
+        assert (tmp_path / name).read_bytes() == g[key].tobytes(), name
