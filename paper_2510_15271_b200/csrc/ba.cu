@@ -982,16 +982,23 @@ __global__ void __launch_bounds__(kCamWarps * 32, SFM_CAM_MINB) k_cam_blocks(Blk
   // next point id (the packed point record load then does not wait on it)
   const int64_t kfirst = k0 + (int64_t)warp * 32 + lane;
   double4 g_nx = make_double4(0.0, 0.0, 0.0, 0.0);
+  double2 uv_nx = make_double2(0.0, 0.0);
   int pt_nx = 0;
-  if (MODE == 0 && kfirst < k1) g_nx = ldg256(a.geo_cm + kfirst);
+  const double2* cm_uv2 = reinterpret_cast<const double2*>(a.cm_uv);
+  if (MODE == 0 && kfirst < k1) { g_nx = ldg256(a.geo_cm + kfirst); uv_nx = __ldg(cm_uv2 + kfirst); }
   if (MODE == 1 && kfirst < k1) pt_nx = __ldg(a.cm_pt + kfirst);
   for (int64_t kb = k0 + (int64_t)warp * 32; kb < k1; kb += kCamWarps * 32) {
     const int64_t k = kb + lane;
     const double4 g_pf = g_nx;
+    const double2 uv_pf = uv_nx;
     const int pt_cur = pt_nx;
     if (k + kCamWarps * 32 < k1) {
-      if (MODE == 0) g_nx = ldg256(a.geo_cm + k + kCamWarps * 32);
-      else pt_nx = __ldg(a.cm_pt + k + kCamWarps * 32);
+      if (MODE == 0) {
+        g_nx = ldg256(a.geo_cm + k + kCamWarps * 32);
+        uv_nx = __ldg(cm_uv2 + k + kCamWarps * 32);  // the pixel too (its load was the top stall)
+      } else {
+        pt_nx = __ldg(a.cm_pt + k + kCamWarps * 32);
+      }
     }
     if (k < k1) {
       const double4 g = MODE == 0 ? g_pf : ldg256(a.geo_cm + k);
@@ -1000,7 +1007,7 @@ __global__ void __launch_bounds__(kCamWarps * 32, SFM_CAM_MINB) k_cam_blocks(Blk
 #pragma unroll
       for (int i = 0; i < 12; ++i) As[i] = Jc[i];
       if (MODE == 0) {
-        const double2 uv = reinterpret_cast<const double2*>(a.cm_uv)[k];
+        const double2 uv = uv_pf;
         double xd, yd;
         distort(cm, g.x, g.y, xd, yd);
         const double r0 = g.w * (cm.fx * xd + cm.cx - uv.x);

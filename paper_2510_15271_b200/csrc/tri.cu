@@ -371,21 +371,11 @@ __device__ __forceinline__ void pair_of(int k, int pi, int& i, int& j) {
   j = i + 1 + rem;
 }
 
-// Warp per track: ransac_triangulate (mapping.py:255-305).
-__global__ void __launch_bounds__(128) k_ransac(TrackArgs a) {
-  const int64_t t = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (t >= a.T) return;
+// Warp per track, observations read from global memory: ransac_triangulate
+// (mapping.py:255-305) for tracks longer than the staged kernel takes.
+__device__ void ransac_track_global(const TrackArgs& a, int64_t t, int lane) {
   const int64_t b0 = a.ptr[t], b1 = a.ptr[t + 1];
   const int k = (int)(b1 - b0);
-  if (a.active && !a.active[t]) {
-    for (int64_t o = b0 + lane; o < b1; o += 32) a.mask[o] = 0;
-    if (lane == 0) {
-      a.status[t] = SFM_TRI_SKIPPED;
-      a.X[t * 3] = a.X[t * 3 + 1] = a.X[t * 3 + 2] = NAN;
-    }
-    return;
-  }
   const int npairs = k * (k - 1) / 2;
   int bcnt = -1, bidx = 0x7fffffff;
   double bneg = -INFINITY;
@@ -446,6 +436,227 @@ __global__ void __launch_bounds__(128) k_ransac(TrackArgs a) {
   }
   a.status[t] = (int8_t)status;
   a.X[t * 3] = X.x; a.X[t * 3 + 1] = X.y; a.X[t * 3 + 2] = X.z;
+}
+
+// ---- staged RANSAC: a track's observations (camera record, ray, world
+// direction, pixel, model, unproject status) copied into the warp's shared
+// memory once, lane o <- observation o, so every hypothesis of the track
+// reads them from shared memory instead of re-gathering camera records from
+// L2 for each of its ~k^2 uses.  Same arithmetic, in the same order, as
+// tri_solve / reproj_err / score_hyp above -- the masks, statuses and
+// positions are bit-identical -- plus: a pair hypothesis touches only its two
+// observations (no filtered loop over the track), and the refinement's
+// per-observation errors run across the lanes.
+constexpr int kRansacMaxK = 32;
+constexpr int kRansacWarps = 4;
+
+struct ObsSm {
+  double R[9], t[3], ray[3], w[3], uv[2];
+  int model, st;
+};
+
+__device__ __forceinline__ double reproj_sm(const ObsSm& ob, const sfm_camera_model* models, Vec3 X) {
+  Mat3 R;
+#pragma unroll
+  for (int i = 0; i < 9; ++i) R.m[i] = ob.R[i];
+  const Vec3 pc = add(mul(R, X), v3(ob.t[0], ob.t[1], ob.t[2]));
+  double u, v;
+  if (project_point(models[ob.model], pc, u, v) != PROJ_OK) return INFINITY;
+  const double du = u - ob.uv[0], dv = v - ob.uv[1];
+  return sqrt(du * du + dv * dv);
+}
+
+__device__ __forceinline__ void dlt_rows_sm(const ObsSm& ob, double Rm[10]) {
+  const double dx = ob.ray[0], dy = ob.ray[1], dz = ob.ray[2];
+  double P[3][4];
+  for (int i = 0; i < 3; ++i) {
+    P[i][0] = ob.R[i * 3]; P[i][1] = ob.R[i * 3 + 1]; P[i][2] = ob.R[i * 3 + 2];
+  }
+  P[0][3] = ob.t[0]; P[1][3] = ob.t[1]; P[2][3] = ob.t[2];
+  double row[4];
+  for (int c = 0; c < 4; ++c) row[c] = -dz * P[1][c] + dy * P[2][c];
+  givens_add(Rm, row);
+  for (int c = 0; c < 4; ++c) row[c] = dz * P[0][c] - dx * P[2][c];
+  givens_add(Rm, row);
+  for (int c = 0; c < 4; ++c) row[c] = -dy * P[0][c] + dx * P[1][c];
+  givens_add(Rm, row);
+}
+
+__device__ __forceinline__ void midpoint_add_sm(const ObsSm& ob, double A[9], double b[3]) {
+  Mat3 R;
+#pragma unroll
+  for (int i = 0; i < 9; ++i) R.m[i] = ob.R[i];
+  Vec3 c = mulT(R, v3(ob.t[0], ob.t[1], ob.t[2]));
+  c = v3(-c.x, -c.y, -c.z);
+  const double wv[3] = {ob.w[0], ob.w[1], ob.w[2]}, cv[3] = {c.x, c.y, c.z};
+  for (int i = 0; i < 3; ++i) {
+    double bi = 0.0;
+    for (int j = 0; j < 3; ++j) {
+      double m = (i == j ? 1.0 : 0.0) - wv[i] * wv[j];
+      A[i * 3 + j] += m;
+      bi += m * cv[j];
+    }
+    b[i] += bi;
+  }
+}
+
+// tri_solve over the observations in `sel` (bit o = observation o of the
+// track, visited in ascending order), from the staged records.
+__device__ int tri_solve_sm(const ObsSm* ob, unsigned sel, const sfm_camera_model* models, int method,
+                            double min_angle, bool check_angle, Vec3& X) {
+  (void)models;
+  const int n = __popc(sel);
+  for (unsigned m = sel; m; m &= m - 1) {
+    const int o = __ffs(m) - 1;
+    if (ob[o].st != PROJ_OK) return ob[o].st == PROJ_DOMAIN ? SFM_TRI_CAMERA_DOMAIN : SFM_TRI_CAMERA_ERROR;
+  }
+  if (n < 2) return SFM_TRI_TOO_FEW_OBS;
+  if (check_angle) {  // max_ray_angle: arccos of the smallest |da.db| over pairs
+    double mind = 2.0;
+    for (unsigned ma = sel; ma; ma &= ma - 1) {
+      const int oa = __ffs(ma) - 1;
+      const Vec3 da = v3(ob[oa].w[0], ob[oa].w[1], ob[oa].w[2]);
+      for (unsigned mb = ma & (ma - 1); mb; mb &= mb - 1) {
+        const int b = __ffs(mb) - 1;
+        mind = fmin(mind, fabs(dot(da, v3(ob[b].w[0], ob[b].w[1], ob[b].w[2]))));
+      }
+    }
+    if (mind > 1.0) mind = 1.0;
+    if (acos(mind) < min_angle) return SFM_TRI_INSUFFICIENT_PARALLAX;
+  }
+  if (method == SFM_TRI_DLT) {
+    double Rm[10];
+    for (int i = 0; i < 10; ++i) Rm[i] = 0.0;
+    for (unsigned m = sel; m; m &= m - 1) dlt_rows_sm(ob[__ffs(m) - 1], Rm);
+    double Xh[4];
+    smallest_right_sv(Rm, Xh);
+    if (fabs(Xh[3]) < 1e-12) return SFM_TRI_INSUFFICIENT_PARALLAX;
+    X = v3(Xh[0] / Xh[3], Xh[1] / Xh[3], Xh[2] / Xh[3]);
+  } else {
+    double A[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0}, b[3] = {0, 0, 0};
+    for (unsigned m = sel; m; m &= m - 1) midpoint_add_sm(ob[__ffs(m) - 1], A, b);
+    if (sym3_cond(A) > 1e10) return SFM_TRI_PARALLEL_RAYS;
+    double x[3];
+    if (!solve3(A, b, x)) return SFM_TRI_PARALLEL_RAYS;
+    X = v3(x[0], x[1], x[2]);
+  }
+  for (unsigned m = sel; m; m &= m - 1) {  // cheirality (mapping.py:186-191)
+    const ObsSm& o = ob[__ffs(m) - 1];
+    Mat3 R;
+#pragma unroll
+    for (int i = 0; i < 9; ++i) R.m[i] = o.R[i];
+    const Vec3 pc = add(mul(R, X), v3(o.t[0], o.t[1], o.t[2]));
+    if (dot(pc, v3(o.ray[0], o.ray[1], o.ray[2])) <= 0.0) return SFM_TRI_CHEIRALITY;
+  }
+  if (!(isfinite(X.x) && isfinite(X.y) && isfinite(X.z))) return SFM_TRI_INSUFFICIENT_PARALLAX;
+  return SFM_TRI_OK;
+}
+
+// Warp per track: ransac_triangulate (mapping.py:255-305).
+__global__ void __launch_bounds__(kRansacWarps * 32) k_ransac(TrackArgs a) {
+  __shared__ ObsSm obs[kRansacWarps][kRansacMaxK];
+  const int64_t t = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (t >= a.T) return;
+  const int64_t b0 = a.ptr[t], b1 = a.ptr[t + 1];
+  const int k = (int)(b1 - b0);
+  if (a.active && !a.active[t]) {
+    for (int64_t o = b0 + lane; o < b1; o += 32) a.mask[o] = 0;
+    if (lane == 0) {
+      a.status[t] = SFM_TRI_SKIPPED;
+      a.X[t * 3] = a.X[t * 3 + 1] = a.X[t * 3 + 2] = NAN;
+    }
+    return;
+  }
+  if (k > kRansacMaxK) {
+    ransac_track_global(a, t, lane);
+    return;
+  }
+  ObsSm* ob = obs[warp];
+  if (lane < k) {  // stage observation lane
+    const int64_t o = b0 + lane;
+    const int f = a.d.of[o];
+    ObsSm& m = ob[lane];
+    const double* p = a.d.Rt + (int64_t)f * 12;
+#pragma unroll
+    for (int i = 0; i < 9; ++i) m.R[i] = p[i];
+    m.t[0] = p[9]; m.t[1] = p[10]; m.t[2] = p[11];
+    m.ray[0] = a.d.ray[o * 3]; m.ray[1] = a.d.ray[o * 3 + 1]; m.ray[2] = a.d.ray[o * 3 + 2];
+    Mat3 R;
+#pragma unroll
+    for (int i = 0; i < 9; ++i) R.m[i] = m.R[i];
+    const Vec3 w = mulT(R, v3(m.ray[0], m.ray[1], m.ray[2]));  // world_dir
+    m.w[0] = w.x; m.w[1] = w.y; m.w[2] = w.z;
+    m.uv[0] = a.d.uv[o * 2]; m.uv[1] = a.d.uv[o * 2 + 1];
+    m.model = a.d.fm[f];
+    m.st = a.d.ray_st[o];
+  }
+  __syncwarp();
+  const sfm_camera_model* models = a.d.models;
+  const int npairs = k * (k - 1) / 2;
+  int bcnt = -1, bidx = 0x7fffffff;
+  double bneg = -INFINITY;
+  for (int pi = lane; pi < npairs; pi += 32) {
+    int i, j;
+    pair_of(k, pi, i, j);
+    Vec3 X;
+    if (tri_solve_sm(ob, (1u << i) | (1u << j), models, a.method, a.min_angle, true, X) != SFM_TRI_OK) continue;
+    // score_hyp: inlier count, then numpy's pairwise sum of their errors
+    int cnt = 0;
+    for (int o = 0; o < k; ++o) cnt += reproj_sm(ob[o], models, X) < a.thr;
+    NpSum acc(cnt);
+    for (int o = 0; o < k; ++o) {
+      const double e = reproj_sm(ob[o], models, X);
+      if (e < a.thr) acc.add(e);
+    }
+    const double neg = -acc.value();
+    if (cnt >= 2 && (cnt > bcnt || (cnt == bcnt && neg > bneg))) {
+      bcnt = cnt; bneg = neg; bidx = pi;
+    }
+  }
+  // warp arg-max: (count, -sum) lexicographic, lowest pair index on ties
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    int oc = __shfl_down_sync(0xffffffffu, bcnt, off);
+    double on = __shfl_down_sync(0xffffffffu, bneg, off);
+    int oi = __shfl_down_sync(0xffffffffu, bidx, off);
+    bool take = oc > bcnt || (oc == bcnt && (on > bneg || (on == bneg && oi < bidx)));
+    if (take) { bcnt = oc; bneg = on; bidx = oi; }
+  }
+  bcnt = __shfl_sync(0xffffffffu, bcnt, 0);
+  bidx = __shfl_sync(0xffffffffu, bidx, 0);
+  int status = SFM_TRI_FAILED;
+  Vec3 X = v3(NAN, NAN, NAN);
+  unsigned inl = 0;
+  if (bcnt >= 2) {
+    // the winning hypothesis again (lane 0), its inlier set across lanes
+    Vec3 Xb = v3(0.0, 0.0, 0.0);
+    if (lane == 0) {
+      int i, j;
+      pair_of(k, bidx, i, j);
+      tri_solve_sm(ob, (1u << i) | (1u << j), models, a.method, a.min_angle, true, Xb);
+    }
+    Xb = v3(__shfl_sync(0xffffffffu, Xb.x, 0), __shfl_sync(0xffffffffu, Xb.y, 0), __shfl_sync(0xffffffffu, Xb.z, 0));
+    const unsigned sel = __ballot_sync(0xffffffffu, lane < k && reproj_sm(ob[lane < k ? lane : 0], models, Xb) < a.thr);
+    // refinement on the inliers (midpoint has no parallax gate, :295)
+    int st = SFM_TRI_FAILED;
+    if (lane == 0) st = tri_solve_sm(ob, sel, models, a.method, a.min_angle, a.method == SFM_TRI_DLT, X);
+    st = __shfl_sync(0xffffffffu, st, 0);
+    if (st == SFM_TRI_OK) {
+      X = v3(__shfl_sync(0xffffffffu, X.x, 0), __shfl_sync(0xffffffffu, X.y, 0), __shfl_sync(0xffffffffu, X.z, 0));
+      inl = __ballot_sync(0xffffffffu, lane < k && reproj_sm(ob[lane < k ? lane : 0], models, X) < a.thr);
+      if (__popc(inl) >= 2) status = SFM_TRI_OK;
+    }
+  }
+  if (status != SFM_TRI_OK) {
+    inl = 0;
+    X = v3(NAN, NAN, NAN);
+  }
+  if (lane < k) a.mask[b0 + lane] = (inl >> lane) & 1u;
+  if (lane == 0) {
+    a.status[t] = (int8_t)status;
+    a.X[t * 3] = X.x; a.X[t * 3 + 1] = X.y; a.X[t * 3 + 2] = X.z;
+  }
 }
 
 __global__ void k_direct(TrackArgs a) {
@@ -551,7 +762,7 @@ void tri_ransac(cudaStream_t s, Profiler* prof, const sfm_tracks& tr, double thr
   a.thr = thr; a.min_angle = min_angle; a.method = method; a.X = X.get(); a.mask = mask.get(); a.status = st.get();
   if (tr.n_tracks) {
     ProfScope ps(*prof, "tri_ransac", 24.0 * tr.n_obs + 24.0 * tr.n_tracks + tr.n_obs, s);
-    k_ransac<<<grid_for(tr.n_tracks * 32, 128), 128, 0, s>>>(a);
+    k_ransac<<<grid_for(tr.n_tracks * 32, kRansacWarps * 32), kRansacWarps * 32, 0, s>>>(a);
   }
   X.download(out_X, (size_t)tr.n_tracks * 3, s);
   mask.download(out_mask, tr.n_obs, s);
@@ -634,7 +845,7 @@ void tri_ransac_device(cudaStream_t s, Profiler* prof, const TriDeviceTracks& tr
   a.T = tr.n_tracks; a.ptr = tr.ptr; a.active = active; a.d = tri_data(tr);
   a.thr = thr; a.min_angle = min_angle; a.method = method; a.X = X; a.mask = mask; a.status = status;
   ProfScope ps(*prof, "tri_ransac", 24.0 * tr.n_obs + 24.0 * tr.n_tracks + tr.n_obs, s);
-  k_ransac<<<grid_for(tr.n_tracks * 32, 128), 128, 0, s>>>(a);
+  k_ransac<<<grid_for(tr.n_tracks * 32, kRansacWarps * 32), kRansacWarps * 32, 0, s>>>(a);
 }
 
 void tri_gate_device(cudaStream_t s, Profiler* prof, const TriDeviceTracks& tr, const double* P, double thr,

@@ -15,8 +15,8 @@ ptr = np.searchsorted(sc.obs_point, np.arange(sc.n_points + 1)).astype(np.int64)
 F = sc.n_frames
 edges = np.stack([np.arange(F - 1), np.arange(1, F)], 1).astype(np.int32)
 priors = np.flatnonzero(sc.frame_fixed == 0).astype(np.int32)
-dev = DeviceOptions(linear_solver="pcg", pcg_rtol=1e-8)
-for rep in range(2):
+dev = DeviceOptions()  # drop-in defaults, as bench.py
+for rep in range(int(sys.argv[2]) if len(sys.argv) > 2 else 2):
     t0 = time.perf_counter()
     try:
         r = iterative_map_arrays(sc.cam_q, sc.cam_t, fm, sc.frame_fixed, models, n_models, ptr,
