@@ -318,16 +318,26 @@ def flatten_ba(sparse_map, config, stage=1, mode=PURE):
                                         for f in frames])
     fixed_arr = np.array([1 if f in fixed else 0 for f in frames], dtype=np.uint8)
     lms = [li for li, lm in enumerate(sparse_map.landmarks) if lm.track.status == TRIANGULATED]
-    points = np.array([sparse_map.landmarks[li].position for li in lms],
-                      dtype=np.float64).reshape(-1, 3)
-    of, op, uv = [], [], []
-    for pi, li in enumerate(lms):
-        lm = sparse_map.landmarks[li]
-        for o, ok in zip(lm.track.observations, lm.inlier_mask):
-            if ok:
-                of.append(fidx[o.frame_id])
-                op.append(pi)
-                uv.append(o.pixel)
+    sel = [sparse_map.landmarks[li] for li in lms]
+    points = np.array([lm.position for lm in sel], dtype=np.float64).reshape(-1, 3)
+    # inlier observations, landmark-major in track order (mapping.py:452-475),
+    # gathered with one pass over the objects and numpy for the rest
+    allobs = [o for lm in sel for o in lm.track.observations]
+    counts = np.fromiter((len(lm.track.observations) for lm in sel), dtype=np.int64, count=len(sel))
+    keep = (np.concatenate([np.asarray(lm.inlier_mask, dtype=bool) for lm in sel])
+            if sel else np.zeros(0, bool))
+    fids = np.fromiter((o.frame_id for o in allobs), dtype=np.int64, count=len(allobs))
+    frame_arr = np.asarray(frames, dtype=np.int64)
+    at = np.searchsorted(frame_arr, fids)
+    bad = (at >= len(frame_arr)) | (frame_arr[np.minimum(at, max(len(frame_arr) - 1, 0))] != fids) \
+        if len(frame_arr) else np.ones(len(fids), bool)
+    if np.any(bad & keep):
+        raise KeyError(int(fids[np.flatnonzero(bad & keep)[0]]))
+    pix = (np.concatenate([o.pixel for o in allobs]).reshape(-1, 2) if allobs
+           else np.zeros((0, 2)))
+    of = at[keep]
+    op = np.repeat(np.arange(len(sel), dtype=np.int64), counts)[keep]
+    uv = pix[keep]
     edges = []
     if config.lambda_c > 0:
         by_cam = {}
