@@ -8,4 +8,4 @@ for cfg in 2 4; do
   timeout 900 ncu --metrics $M --clock-control none -k "regex:k_ransac|k_gate|k_rays" --csv --log-file $OUT/tri_cfg$cfg.csv \
      python tools/imap_run.py $cfg 1 > $OUT/tri_cfg$cfg.log 2>&1
 done
-tail -2 $OUT/tri_cfg*.log
+for f in $OUT/tri_cfg*.log; do tail -n 2 $f; done
