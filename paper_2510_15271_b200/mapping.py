@@ -223,16 +223,25 @@ def _options(loss: RobustLoss, sopt: SolverOptions, dopt: DeviceOptions) -> nat.
 
 
 def solve_arrays(arrays: BAArrays, loss: RobustLoss = TRIVIAL_LOSS,
-                 options: SolverOptions = None, device: DeviceOptions = None, ctx=None):
-    """sfm_ba_solve on flattened arrays -> (cam_q, cam_t, points, report, raw)."""
+                 options: SolverOptions = None, device: DeviceOptions = None, ctx=None,
+                 out=None):
+    """sfm_ba_solve on flattened arrays -> (cam_q, cam_t, points, report, raw).
+    `out` = (cam_q, cam_t, points) C-contiguous fp64 arrays to write the
+    result into (e.g. pinned host memory); fresh arrays otherwise.  The
+    library writes every entry (fixed frames copied bit-identically)."""
     ctx = ctx or nat.default_context()
     options = options or SolverOptions()
     device = device or DEFAULT_DEVICE_OPTIONS
     prob = arrays.struct()
     opt = _options(loss, options, device)
-    q = np.array(arrays.cam_q, dtype=np.float64, copy=True)
-    t = np.array(arrays.cam_t, dtype=np.float64, copy=True)
-    X = np.array(arrays.points, dtype=np.float64, copy=True)
+    if out is not None:
+        q, t, X = out
+        assert q.shape == arrays.cam_q.shape and t.shape == arrays.cam_t.shape
+        assert X.shape == arrays.points.shape
+    else:
+        q = np.empty(arrays.cam_q.shape, dtype=np.float64)
+        t = np.empty(arrays.cam_t.shape, dtype=np.float64)
+        X = np.empty(arrays.points.shape, dtype=np.float64)
     rep = nat.BAReportC()
     ctx.check(ctx.lib.sfm_ba_solve(ctx.handle, ctypes.byref(prob), ctypes.byref(opt),
                                    nat.ptr(q), nat.ptr(t), nat.ptr(X), ctypes.byref(rep)))

@@ -373,3 +373,25 @@ def test_config2_iterative_map_matches_oracle():
     np.testing.assert_allclose(r.cam_t, g["cam_t"], atol=1e-6)
     X = r.points[r.lm_track[g["lm_sample"]]]
     np.testing.assert_allclose(X, g["lm_sample_X"], atol=1e-5)
+
+
+@pytest.mark.parametrize("n_shards", [2, 4])
+def test_config3_sharded_matches_single_rank(n_shards):
+    """The benchmarked scene (configs[2], 5M observations) point-sharded over
+    emulated ranks with the row-partitioned PCG (S / b reduce-scattered by
+    block rows, z and the dot products pushed between ranks inside the
+    Krylov kernel): five LM iterations equal the single-rank solve."""
+    from paper_2510_15271_b200.mapping import solve_arrays, solve_sharded_emulated
+    from paper_2510_15271_b200.scenes import config_scene, scene_arrays
+    from paper_2510_15271_b200.solver import DeviceOptions, RobustLoss, SolverOptions
+    a = scene_arrays(config_scene(3, seed=0))
+    loss, sopt = RobustLoss("huber", 2.0), SolverOptions(max_iters=5)
+    dopt = DeviceOptions(pcg_rtol=1e-10)
+    q1, t1, X1, r1, _ = solve_arrays(a, loss, sopt, dopt)
+    qs, ts, Xs, rs, _ = solve_sharded_emulated(a, loss, sopt, dopt, n_shards)
+    assert rs.iterations == r1.iterations == 5
+    assert rs.initial_cost == pytest.approx(r1.initial_cost, rel=1e-13)
+    assert rs.final_cost == pytest.approx(r1.final_cost, rel=1e-10)
+    scale = np.abs(X1).max()
+    np.testing.assert_allclose(Xs, X1, atol=1e-9 * scale)
+    np.testing.assert_allclose(qs, q1, atol=1e-10)
