@@ -25,7 +25,7 @@
 extern "C" {
 #endif
 
-#define SFM_ABI_VERSION 6
+#define SFM_ABI_VERSION 7
 
 /* ---- error codes (mapped to sfmkit.errors classes by the Python layer) --- */
 #define SFM_OK 0
@@ -376,6 +376,14 @@ int sfm_reprojection_errors(sfm_ctx* ctx, const sfm_tracks* tracks,
  * pointers): tracks as CSR (out_track_ptr, out_obs_frame, out_obs_feature),
  * in the reference's track and observation order.  Needs no GPU.
  */
+/* Host-only helpers of the multi-GPU partition (no context, no GPU):
+ * the point shards -- contiguous point ranges balanced by observation
+ * count, out_bounds[world+1] -- and the rank row ranges
+ * of the row-partitioned PCG over a BSR pattern, out_row0[world+1]. */
+int sfm_shard_points(int64_t n_obs, const int32_t* obs_point, int64_t n_points, int32_t world,
+                     int64_t* out_bounds);
+int sfm_pcg_rank_rows(int32_t n_rows, const int32_t* row_ptr, int32_t world, int32_t* out_row0);
+
 int sfm_build_tracks(int64_t n_pairs, const int32_t* pair_frames, const int64_t* pair_ptr,
                      const int32_t* match_index, int64_t* out_track_ptr, int32_t* out_obs_frame,
                      int32_t* out_obs_feature, int64_t* out_n_tracks, int64_t* out_n_obs);

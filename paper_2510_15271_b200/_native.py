@@ -17,7 +17,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libsfm_b200.so")
 
 # ---- constants (mirror include/sfm_b200.h) ---------------------------------
-ABI_VERSION = 6
+ABI_VERSION = 7
 SFM_OK = 0
 SFM_E_INVALID = -1
 SFM_E_NON_POSITIVE_DEPTH = -2
@@ -59,7 +59,7 @@ EXPORTED_SYMBOLS = (
     "sfm_prof_reset", "sfm_ba_solve", "sfm_ba_setup", "sfm_ba_iterate",
     "sfm_ba_download", "sfm_ba_restart", "sfm_ba_eval", "sfm_ransac_triangulate", "sfm_triangulate",
     "sfm_gate", "sfm_reprojection_errors", "sfm_iterative_map", "sfm_ba_solve_emulated",
-    "sfm_build_tracks", "sfm_gba_solve",
+    "sfm_build_tracks", "sfm_gba_solve", "sfm_shard_points", "sfm_pcg_rank_rows",
 )
 
 TRACK_PENDING, TRACK_TRIANGULATED, TRACK_FAILED = 0, 1, 2
@@ -202,6 +202,8 @@ def load_library(path: str = None):
         lib.sfm_reprojection_errors.argtypes = [_p, P(TracksC), _p, _p]
         lib.sfm_gba_solve.argtypes = [_p, P(GbaProblemC), P(BAOptionsC), _p, _p, _p, P(BAReportC)]
         lib.sfm_build_tracks.argtypes = [c_i64, _p, _p, _p, _p, _p, _p, P(c_i64), P(c_i64)]
+        lib.sfm_shard_points.argtypes = [c_i64, _p, c_i64, c_i32, _p]
+        lib.sfm_pcg_rank_rows.argtypes = [c_i32, _p, c_i32, _p]
         lib.sfm_ba_solve_emulated.argtypes = [_p, c_i32, _p, P(BAOptionsC), _p, _p, _p,
                                               P(BAReportC)]
         lib.sfm_iterative_map.argtypes = [_p, P(MapProblemC), P(MapOptionsC), _p, _p, _p, _p, _p,
@@ -307,6 +309,28 @@ class Context:
 
     def reset_profile(self):
         self.check(self.lib.sfm_prof_reset(self.handle))
+
+
+def shard_points(obs_point, n_points: int, world: int) -> np.ndarray:
+    """sfm_shard_points: point boundaries [world+1] of the observation-balanced
+    point shards (host-only, no GPU)."""
+    op = np.ascontiguousarray(obs_point, dtype=np.int32)
+    out = np.empty(world + 1, np.int64)
+    rc = load_library().sfm_shard_points(len(op), ptr(op), int(n_points), int(world), ptr(out))
+    if rc != SFM_OK:
+        raise ValueError(f"sfm_shard_points failed ({rc})")
+    return out
+
+
+def pcg_rank_rows(row_ptr, world: int) -> np.ndarray:
+    """sfm_pcg_rank_rows: block-row boundaries [world+1] of the row-partitioned
+    PCG over a BSR row pointer (host-only, no GPU)."""
+    rp = np.ascontiguousarray(row_ptr, dtype=np.int32)
+    out = np.empty(world + 1, np.int32)
+    rc = load_library().sfm_pcg_rank_rows(len(rp) - 1, ptr(rp), int(world), ptr(out))
+    if rc != SFM_OK:
+        raise ValueError(f"sfm_pcg_rank_rows failed ({rc})")
+    return out
 
 
 def device_count() -> int:

@@ -280,6 +280,31 @@ int sfm_iterative_map(sfm_ctx* ctx, const sfm_map_problem* prob, const sfm_map_o
   });
 }
 
+int sfm_shard_points(int64_t n_obs, const int32_t* obs_point, int64_t n_points, int32_t world,
+                     int64_t* out_bounds) {
+  // host-only: no context
+  try {
+    if (n_obs < 0 || n_points < 0 || world < 1 || !out_bounds || (n_obs && !obs_point)) return SFM_E_INVALID;
+    const auto b = sfm::shard_bounds(obs_point, n_obs, n_points, world);
+    for (int r = 0; r <= world; ++r) out_bounds[r] = b[r];
+    return SFM_OK;
+  } catch (...) {
+    return SFM_E_INVALID;
+  }
+}
+
+int sfm_pcg_rank_rows(int32_t n_rows, const int32_t* row_ptr, int32_t world, int32_t* out_row0) {
+  // host-only: no context
+  try {
+    if (n_rows < 1 || world < 1 || world > n_rows || !row_ptr || !out_row0) return SFM_E_INVALID;
+    const auto r = sfm::pcg_rank_rows(row_ptr, n_rows, world);
+    for (int q = 0; q <= world; ++q) out_row0[q] = r[q];
+    return SFM_OK;
+  } catch (...) {
+    return SFM_E_INVALID;
+  }
+}
+
 int sfm_build_tracks(int64_t n_pairs, const int32_t* pair_frames, const int64_t* pair_ptr,
                      const int32_t* match_index, int64_t* out_track_ptr, int32_t* out_obs_frame,
                      int32_t* out_obs_feature, int64_t* out_n_tracks, int64_t* out_n_obs) {

@@ -133,12 +133,30 @@ void EmuGroup::allgather_u64(int rank, const unsigned long long* send, unsigned 
   barrier();
 }
 
+std::vector<int64_t> shard_bounds(const int* op, int64_t N, int64_t P, int world) {
+  // first observation of every point (obs_point is non-decreasing)
+  auto first_obs = [&](int64_t p) { return (int64_t)(std::lower_bound(op, op + N, (int)p) - op); };
+  std::vector<int64_t> bounds(1, 0);
+  for (int r = 1; r < world; ++r) {
+    // first point whose observations start at or after r*N/world (the point
+    // straddling the target stays whole on the lower rank)
+    const int64_t target = N * r / world;
+    int64_t p = P;
+    if (target < N) {
+      const int64_t q = op[target];
+      p = first_obs(q) >= target ? q : q + 1;
+    }
+    bounds.push_back(std::max(bounds.back(), std::min(p, P)));
+  }
+  bounds.push_back(P);
+  return bounds;
+}
+
 ShardSet shard_problem(const sfm_ba_problem& full, int world) {
   SFM_REQUIRE(world >= 1, "world must be >= 1");
   const int64_t N = full.n_obs, P = full.n_points;
   std::vector<int> op((size_t)N);
   if (N) SFM_CUDA(cudaMemcpy(op.data(), full.obs_point, sizeof(int) * N, cudaMemcpyDefault));
-  // first observation of every point (obs_point is non-decreasing)
   auto first_obs = [&](int64_t p) {
     return (int64_t)(std::lower_bound(op.begin(), op.end(), (int)p) - op.begin());
   };
@@ -150,20 +168,7 @@ ShardSet shard_problem(const sfm_ba_problem& full, int world) {
     for (uint8_t v : fx) n_free += v == 0;
   }
   ShardSet ss;
-  std::vector<int64_t> bounds(1, 0);
-  for (int r = 1; r < world; ++r) {
-    // first point whose observations start at or after r*N/world (the point
-    // straddling the target stays whole on the lower rank)
-    const int64_t target = N * r / world;
-    int64_t p = P;
-    if (target < N) {
-      const int64_t q = op[(size_t)target];
-      p = first_obs(q) >= target ? q : q + 1;
-    }
-    p = std::max(bounds.back(), std::min(p, P));
-    bounds.push_back(p);
-  }
-  bounds.push_back(P);
+  const std::vector<int64_t> bounds = shard_bounds(op.data(), N, P, world);
   ss.shards.resize(world);
   ss.local_op.resize(world);
   ss.p0.resize(world);

@@ -27,6 +27,9 @@ struct ShardSet {
   std::vector<int64_t> p0;
 };
 ShardSet shard_problem(const sfm_ba_problem& full, int world);
+// The point boundaries of that split from host obs_point (world+1 entries):
+// rank r owns points [b[r], b[r+1]).
+std::vector<int64_t> shard_bounds(const int* obs_point, int64_t n_obs, int64_t n_points, int world);
 
 void ba_solve_group(const DeviceGroup& g, const sfm_ba_problem* shards, const sfm_ba_options& opt,
                     double* out_q, double* out_t, double* const* out_points, sfm_ba_report* report);

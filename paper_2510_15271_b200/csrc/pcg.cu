@@ -1032,6 +1032,25 @@ void TwoLevelPcg::setup(int nf, int cluster, int refresh, cudaStream_t s) {
   (void)s;
 }
 
+std::vector<int> pcg_rank_rows(const int* rp, int nf, int world) {
+  constexpr int64_t kRowCost = 4;
+  auto cost_upto = [&](int r) { return (int64_t)rp[r] + kRowCost * r; };
+  const int64_t total = cost_upto(nf);
+  std::vector<int> out(1, 0);
+  for (int r = 1; r < world; ++r) {
+    const int64_t target = total * r / world;
+    int a0 = out.back() + 1, b0 = nf - (world - r);
+    const int lo = a0, hi = b0;
+    while (a0 < b0) {
+      const int m = (a0 + b0) / 2;
+      if (cost_upto(m) < target) a0 = m + 1; else b0 = m;
+    }
+    out.push_back(std::min(std::max(a0, lo), hi));
+  }
+  out.push_back(nf);
+  return out;
+}
+
 void TwoLevelPcg::set_pattern(const int* row_ptr, const int* col, int nnzb, cudaStream_t s) {
   if (nf_ <= 0) return;
   const bool timing = std::getenv("SFM_TIMING") != nullptr;
@@ -1093,9 +1112,7 @@ void TwoLevelPcg::set_pattern(const int* row_ptr, const int* col, int nnzb, cuda
   // then CTAs per rank in proportion, each rank's rows split over its CTAs
   const int R = std::max(1, std::min(world_, G));
   SFM_REQUIRE(R == world_, "row-partitioned PCG: fewer block rows than ranks");
-  rank_row0_.assign(1, 0);
-  for (int r = 1; r < R; ++r) rank_row0_.push_back(row_at(total * r / R, rank_row0_.back() + 1, nf_ - (R - r)));
-  rank_row0_.push_back(nf_);
+  rank_row0_ = pcg_rank_rows(rp.data(), nf_, R);
   rank_cta0_.assign(1, 0);
   for (int r = 1; r < R; ++r) {
     const int64_t c0 = cost_upto(rank_row0_[r]);

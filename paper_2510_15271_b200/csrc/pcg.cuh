@@ -74,6 +74,11 @@ struct PcgProblem {
   double lam;             // Marquardt damping S was assembled at (coarse-level consistency)
 };
 
+// Rank row ranges of the row-partitioned PCG: block rows split into `world`
+// contiguous ranges balanced by stored blocks + 4 per row (the same cost the
+// CTA partition balances).  Host-only; row_ptr has nf+1 entries.
+std::vector<int> pcg_rank_rows(const int* row_ptr, int nf, int world);
+
 class TwoLevelPcg {
  public:
   // cluster <= 0 disables the coarse level (plain block-Jacobi).

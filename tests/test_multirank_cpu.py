@@ -2,11 +2,17 @@
 (SURVEY.md §8(e)): the host-side sharding, the camera-indexed reductions
 that csrc/comm.cuh performs with NCCL, and the gather of the sharded points.
 
-Each rank takes its shard (`BAArrays.shard`), computes its partial
+Each rank takes its shard (`BAArrays.shard`, boundaries checked against the
+library's own host-side split, sfm_shard_points), computes its partial
 linearisation / reduced camera system with the oracle, and the partials are
 all-reduced over gloo, exactly where libsfm_b200 all-reduces over NCCL
 (linearize(): U, g_c, grad max; build_schur(): S, b_S; trial(): cost).  The
-sum must equal the unsharded system.  No GPU is needed.
+sum must equal the unsharded system.  The row-partitioned variant is then
+replayed with the library's rank row ranges (sfm_pcg_rank_rows): S and b
+reduce-scattered by block rows, a CG in which every rank updates only its
+rows, exchanging z (all_gather) and the dot products (all_reduce) each
+iteration, the solution allgathered -- and it equals the unsharded step.  No
+GPU is needed (the two helpers are host-only).
 """
 
 from __future__ import annotations
@@ -38,6 +44,11 @@ def _oracle(a):
                         [(0, 500.0, 500.0, 320.0, 240.0, (0.0, 0.0))], a.points, a.obs_frame,
                         a.obs_point, a.obs_uv, a.edge_ab, a.prior_frame, a.edge_weight,
                         a.prior_weight)
+
+
+def allsum_off(lin, world, dist, nf):
+    """The off-diagonal pose-term blocks (rank 0's; empty elsewhere)."""
+    return lin["Hoff"]
 
 
 def _worker(rank, world, port, out_dir):
@@ -73,10 +84,77 @@ def _worker(rank, world, port, out_dir):
         # _solve_sharded: gather of the sharded points in rank order
         gathered = [None] * world
         dist.all_gather_object(gathered, X)
+        # row-partitioned solve (pcg_partition): the full camera blocks on
+        # rank 0, the library's rank row ranges over the S block pattern
+        from paper_2510_15271_b200 import _native as nat
+        nf = p.nf
+        S4 = np.zeros((nf, nf, 6, 6))
+        if rank == 0:
+            dU = np.maximum(np.einsum("cii->ci", U), 1e-12)
+            S4[np.arange(nf), np.arange(nf)] = U + lam * np.einsum("ci,ij->cij", dU, np.eye(6))
+            for (ja, jb), H in allsum_off(lin, world, dist, nf).items():
+                S4[ja, jb] += H
+                S4[jb, ja] += H.T
+        else:
+            allsum_off(lin, world, dist, nf)
+        S_pt, b_pt = p.point_schur_terms(lin, Vinv, e)   # this rank's partials (allsum above summed in place)
+        Sp = S4.transpose(0, 2, 1, 3).reshape(6 * nf, 6 * nf) + S_pt
+        bp = (-gc.reshape(-1) if rank == 0 else np.zeros(6 * nf)) + b_pt
+        blk_nz = np.abs(allsum(Sp.copy())).reshape(nf, 6, nf, 6).max(axis=(1, 3)) > 0
+        row_ptr = np.concatenate([[0], np.cumsum(blk_nz.sum(1))]).astype(np.int32)
+        rows = nat.pcg_rank_rows(row_ptr, world)
+        lo, hi = 6 * rows[rank], 6 * rows[rank + 1]
+        # reduce-scatter by block rows: rank r keeps the summed rows it owns
+        S_own, b_own = None, None
+        for q in range(world):
+            a0, a1 = 6 * rows[q], 6 * rows[q + 1]
+            tS = torch.from_numpy(np.ascontiguousarray(Sp[a0:a1]))
+            tb = torch.from_numpy(np.ascontiguousarray(bp[a0:a1]))
+            dist.reduce(tS, dst=q)
+            dist.reduce(tb, dst=q)
+            if q == rank:
+                S_own, b_own = tS.numpy().copy(), tb.numpy().copy()
+        # CG with block-Jacobi, each rank updating its rows only
+        Minv = np.zeros((hi - lo, hi - lo))
+        for i in range(0, hi - lo, 6):
+            Minv[i:i + 6, i:i + 6] = np.linalg.inv(S_own[i:i + 6, lo + i:lo + i + 6])
+
+        width = 6 * int(np.max(np.diff(rows)))
+
+        def gather_vec(v):
+            # allgather with variable counts (gloo wants equal sizes: pad)
+            buf = np.zeros(width)
+            buf[:len(v)] = v
+            parts = [torch.zeros(width, dtype=torch.float64) for _ in range(world)]
+            dist.all_gather(parts, torch.from_numpy(buf))
+            return np.concatenate([parts[q].numpy()[:6 * (rows[q + 1] - rows[q])] for q in range(world)])
+
+        def dot(u, v):
+            return float(allsum(np.array([u @ v]))[0])
+
+        x = np.zeros(hi - lo)
+        r_ = b_own.copy()
+        z = Minv @ r_
+        pv = z.copy()
+        rz = dot(r_, z)
+        bn = np.sqrt(dot(b_own, b_own))
+        for _ in range(500):
+            q_ = S_own @ gather_vec(pv)
+            alpha = rz / dot(pv, q_)
+            x += alpha * pv
+            r_ -= alpha * q_
+            if np.sqrt(dot(r_, r_)) <= 1e-13 * bn:
+                break
+            z = Minv @ r_
+            rz_new = dot(r_, z)
+            pv = z + (rz_new / rz) * pv
+            rz = rz_new
+        dc_part = gather_vec(x)
         np.savez(os.path.join(out_dir, f"rank{rank}.npz"), cost=cost, U=U, gc=gc, S=S, b=b,
                  X=np.concatenate(gathered, axis=0), n_edges=len(part.edge_ab),
                  n_priors=len(part.prior_frame), n_obs=len(part.obs_frame),
-                 obs_offset=part.obs_offset, n_params=part.n_params_global)
+                 obs_offset=part.obs_offset, n_params=part.n_params_global, dc_part=dc_part,
+                 rank_rows=rows)
     finally:
         dist.destroy_process_group()
 
@@ -142,3 +220,36 @@ def test_sharded_sums_equal_unsharded_system(sharded):
     dc = scipy.linalg.cho_solve(scipy.linalg.cho_factor(S, lower=True), b)
     dc_ref = scipy.linalg.cho_solve(scipy.linalg.cho_factor(S_ref, lower=True), b_ref)
     np.testing.assert_allclose(dc, dc_ref, rtol=1e-8, atol=1e-10 * np.abs(dc_ref).max())
+
+
+def test_library_point_shards_match_host_split():
+    """sfm_shard_points (the split libsfm_b200 uses for a multi-device
+    context) == mapping.shard_ranges (BAArrays.shard), and every point's
+    observations stay on one rank."""
+    from paper_2510_15271_b200 import _native as nat
+    from paper_2510_15271_b200.mapping import shard_ranges
+    from paper_2510_15271_b200.scenes import make_scene
+    sc = make_scene(40, 3000, 15000, shape="venice", seed=4)
+    for world in (1, 2, 3, 5, 8):
+        b = nat.shard_points(sc.obs_point, sc.n_points, world)
+        ref = shard_ranges(sc.obs_point, sc.n_points, world)
+        assert [(int(b[r]), int(b[r + 1])) for r in range(world)] == [tuple(map(int, x)) for x in ref]
+        assert b[0] == 0 and b[-1] == sc.n_points and np.all(np.diff(b) >= 0)
+
+
+def test_row_partitioned_solve_equals_unsharded(sharded):
+    """The replayed row-partitioned PCG data flow (reduce-scatter by the
+    library's rank rows, per-rank row updates, z allgather, dot-product
+    allreduce, solution allgather) gives the unsharded step, identically on
+    both ranks."""
+    import scipy.linalg
+    full = _scene()
+    p = _oracle(full)
+    lin = p.linearize(full.cam_q, full.cam_t, full.points, 1, 2.0)
+    S_ref, b_ref, *_ = p.reduced_system(lin, 1e-3)
+    dc_ref = scipy.linalg.cho_solve(scipy.linalg.cho_factor(S_ref, lower=True), b_ref)
+    assert sharded[0]["dc_part"].tobytes() == sharded[1]["dc_part"].tobytes()
+    rows = sharded[0]["rank_rows"]
+    assert rows[0] == 0 and rows[-1] == p.nf and np.all(np.diff(rows) >= 1)
+    np.testing.assert_allclose(sharded[0]["dc_part"], dc_ref, rtol=1e-8,
+                               atol=1e-9 * np.abs(dc_ref).max())
