@@ -672,9 +672,10 @@ __device__ __forceinline__ void gather_after_sync(const Pcg3Args& a, const doubl
   __syncthreads();
 }
 
-// e[0..5] = A_c^-1[6k.., :] . rc for this CTA's cluster k (rows in smem).
-// Warps 0..11: two warps per output row, halves summed in a fixed order.
-__device__ __forceinline__ void coarse_apply(const Pcg3Args& a, const PcgSmem& m, double* e, double* tmp) {
+// The two halves of e[0..5] = A_c^-1[6k.., :] . rc for this CTA's cluster k
+// (rows in smem) into tmp[12]; a reader forms e[j] = tmp[2j] + tmp[2j+1]
+// (coarse_e).  Warps 0..11: two warps per output row.
+__device__ __forceinline__ void coarse_apply(const Pcg3Args& a, const PcgSmem& m, double* tmp) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n = 6 * a.nc;
   if (warp < 12) {
@@ -688,8 +689,24 @@ __device__ __forceinline__ void coarse_apply(const Pcg3Args& a, const PcgSmem& m
     if (lane == 0) tmp[warp] = s;
   }
   __syncthreads();
-  if (threadIdx.x < 6) e[threadIdx.x] = tmp[2 * threadIdx.x] + tmp[2 * threadIdx.x + 1];
+}
+
+__device__ __forceinline__ void coarse_e(const double* tmp, double e[6]) {
+#pragma unroll
+  for (int j = 0; j < 6; ++j) e[j] = tmp[2 * j] + tmp[2 * j + 1];
+}
+
+// block_sum2 for a point where `red` is known to be free (right after a
+// grid barrier): one CTA barrier instead of two.
+__device__ __forceinline__ double2 block_sum2_free(double u, double v, double2* red) {
+  u = warp_sum(u);
+  v = warp_sum(v);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = make_double2(u, v);
   __syncthreads();
+  double2 r = make_double2(0.0, 0.0);
+  if (threadIdx.x == 0)
+    for (int w = 0; w < kPcgWarps; ++w) { r.x += red[w].x; r.y += red[w].y; }
+  return r;
 }
 
 // Deterministic block sum of two values (fixed shuffle tree + warp order).
@@ -751,7 +768,6 @@ __global__ void __launch_bounds__(kPcgMaxThreads, 1) k_pcg3(Pcg3Args a) {
   m.cc0 = m.rp + a.maxrows + 1;
   __shared__ double2 red[32];
   __shared__ double tmp[16];
-  __shared__ double e[6];
   __shared__ double sums[4];
   __shared__ double rr_ck[2];  // stagnation test references (sums_and_zc)
   constexpr int kStagWin = 50;
@@ -917,11 +933,15 @@ __global__ void __launch_bounds__(kPcgMaxThreads, 1) k_pcg3(Pcg3Args a) {
   gather_after_sync(a, V.rpart, V.part + part_bb, sums, 1, m.rc, two, true, nullptr, nullptr, m.cc0);
   const double bnorm = sqrt(sums[0]);
   stag_rr = (a.stag_slack * a.rtol * bnorm) * (a.stag_slack * a.rtol * bnorm);
-  if (two) coarse_apply(a, m, e, tmp);
+  double ev[6] = {0, 0, 0, 0, 0, 0};
+  if (two) {
+    coarse_apply(a, m, tmp);
+    coarse_e(tmp, ev);
+  }
   double rz_l = 0.0;
   for (int i = warp; i < nrows; i += kPcgWarps) {
     const double ri = (lane < 6) ? m.r[i * 6 + lane] : 0.0;
-    const double zi = precond_row(m, two, i, ri, e);
+    const double zi = precond_row(m, two, i, ri, ev);
     if (lane < 6) {
       m.z[i * 6 + lane] = zi;
       push_z((row0 + i) * 6 + lane, zi);
@@ -964,10 +984,23 @@ __global__ void __launch_bounds__(kPcgMaxThreads, 1) k_pcg3(Pcg3Args a) {
         }
       }
       PH(8);
-      if (two) write_rpart();
+      {  // p.q partial (thread 0) and the restriction partial P^T q (warp 1),
+         // one CTA barrier: same sums, same order as block_sum2 / write_rpart
+        const double u = warp_sum(pq_l);
+        if (lane == 0) red[warp] = make_double2(u, 0.0);
+        __syncthreads();
+        if (threadIdx.x == 0) {
+          double sx = 0.0;
+          for (int w = 0; w < kPcgWarps; ++w) sx += red[w].x;
+          push_part(part_pq + blockIdx.x, sx);
+        } else if (two && threadIdx.x >= 32 && threadIdx.x < 38) {
+          const int c = threadIdx.x - 32;
+          double sr = 0.0;
+          for (int i = 0; i < nrows; ++i) sr += m.y[i * 6 + c];
+          for (int q = 0; q < a.R; ++q) a.v[q].rpart[blockIdx.x * 6 + c] = sr;
+        }
+      }
       PH(9);
-      const double2 s = block_sum2(pq_l, 0.0, red);
-      if (threadIdx.x == 0) push_part(part_pq + blockIdx.x, s.x);
       PH(10);
       PH(1);
       grid.sync();
@@ -978,7 +1011,10 @@ __global__ void __launch_bounds__(kPcgMaxThreads, 1) k_pcg3(Pcg3Args a) {
       if (!(pq > 0.0) || !isfinite(pq)) { fail = 1; break; }
       const double alpha = rz_old / pq;
       PH(3);
-      if (two) coarse_apply(a, m, e, tmp);
+      if (two) {
+        coarse_apply(a, m, tmp);
+        coarse_e(tmp, ev);
+      }
       PH(4);
       double rz_n = 0.0, rr_n = 0.0;
       for (int i = warp; i < nrows; i += kPcgWarps) {
@@ -988,7 +1024,7 @@ __global__ void __launch_bounds__(kPcgMaxThreads, 1) k_pcg3(Pcg3Args a) {
           ri = m.r[i * 6 + lane] - alpha * m.q[i * 6 + lane];
           m.r[i * 6 + lane] = ri;
         }
-        const double zi = precond_row(m, two, i, ri, e);
+        const double zi = precond_row(m, two, i, ri, ev);
         if (lane < 6) {
           m.z[i * 6 + lane] = zi;
           push_z((row0 + i) * 6 + lane, zi);
@@ -996,7 +1032,7 @@ __global__ void __launch_bounds__(kPcgMaxThreads, 1) k_pcg3(Pcg3Args a) {
           rr_n += ri * ri;
         }
       }
-      const double2 t = block_sum2(rz_n, rr_n, red);
+      const double2 t = block_sum2_free(rz_n, rr_n, red);  // red last read before the grid barrier
       if (threadIdx.x == 0) { push_part(part_rz + blockIdx.x, t.x); push_part(part_rz + G + blockIdx.x, t.y); }
       PH(5);
       grid.sync();
