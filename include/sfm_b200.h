@@ -141,12 +141,18 @@ typedef struct {
                                  (0 = default 1e-2; above it block-Jacobi)  */
   double coarse_drift;        /* re-assemble A_c when lambda moved by more
                                  than this factor since (0 = default 4)    */
-  int32_t pcg_partition;      /* point-sharded ranks: 1 = row-partitioned
-                                 PCG (S / b reduce-scattered by block rows,
-                                 z and the dot products pushed between ranks
-                                 inside the Krylov kernel; ranks sharing a
-                                 device), 0 = replicated PCG on the
-                                 all-reduced S (NCCL ranks always)        */
+  int32_t pcg_partition;      /* point-sharded ranks: 0 = replicated PCG on
+                                 the all-reduced S; 1 = row-partitioned PCG
+                                 (S / b reduce-scattered by block rows, z and
+                                 the dot products pushed between ranks inside
+                                 the Krylov kernel): ranks sharing a device
+                                 run one launch over all their CTAs, the
+                                 devices of a multi-device context (peer
+                                 access) one launch each meeting at a
+                                 cross-launch barrier; 2 = per-rank launches
+                                 also for ranks sharing a device (the test of
+                                 that barrier).  Ranks in separate processes
+                                 always use 0.                              */
   int32_t _pad0;
 } sfm_ba_options;
 

@@ -95,8 +95,18 @@ class CommPcgCollective final : public PcgCollective {
   void sum(double* d, size_t n, cudaStream_t s) override { c_->sum(d, n, s); }
   void launch_all(const PcgRankView& mine, cudaStream_t s,
                   const std::function<void(const PcgRankView*)>& launch) override {
-    SFM_REQUIRE(c_->emu != nullptr, "row-partitioned PCG needs its ranks on one device");
+    SFM_REQUIRE(c_->emu != nullptr, "a single PCG launch needs its ranks on one device");
     c_->emu->run_root(c_->rank, &mine, s, [&](const void* const* all) {
+      std::vector<PcgRankView> v((size_t)c_->world);
+      for (int r = 0; r < c_->world; ++r) v[r] = *static_cast<const PcgRankView*>(all[r]);
+      launch(v.data());
+    });
+  }
+  bool separate_launches() const override { return c_->emu == nullptr || c_->pcg_partition == 2; }
+  void launch_each(const PcgRankView& mine, cudaStream_t s, const std::function<void()>& root_prep,
+                   const std::function<void(const PcgRankView*)>& launch) override {
+    SFM_REQUIRE(c_->host != nullptr, "per-rank PCG launches need the ranks in one process");
+    c_->host->run_each(c_->rank, &mine, s, root_prep, [&](const void* const* all) {
       std::vector<PcgRankView> v((size_t)c_->world);
       for (int r = 0; r < c_->world; ++r) v[r] = *static_cast<const PcgRankView*>(all[r]);
       launch(v.data());
@@ -1816,7 +1826,11 @@ void BASolver::setup(const sfm_ba_problem& pr, const sfm_ba_options& opt) {
     const int refresh = opt_.coarse_refresh > 0 ? opt_.coarse_refresh : 8;
     cudaStream_t ps = plan_stream_;
     cudaEvent_t pe = plan_ev_;
-    partitioned_ = comm_ && comm_->active() && comm_->emu != nullptr && opt_.pcg_partition != 0;
+    // row-partitioned PCG: ranks sharing a device, or the devices of one
+    // process with peer access (NCCL ranks of separate processes: replicated)
+    partitioned_ = comm_ && comm_->active() && opt_.pcg_partition != 0 &&
+                   (comm_->emu != nullptr || (comm_->host != nullptr && comm_->peer));
+    if (comm_) comm_->pcg_partition = opt_.pcg_partition;
     plan = std::async(std::launch::async, [this, dev, cl, refresh, ps, pe]() {
       SFM_CUDA(cudaSetDevice(dev));
       alloc_stream() = ps;  // the plan's buffers are stream-ordered on the plan stream

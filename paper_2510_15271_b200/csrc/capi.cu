@@ -115,6 +115,21 @@ int sfm_ctx_create_multi(int32_t n_devices, const int32_t* devices, sfm_ctx** ou
     if (n_devices > 1 && distinct) {
       ctx->group.comms.resize(n_devices);
       SFM_NCCL(ncclCommInitAll(ctx->group.comms.data(), n_devices, ctx->group.devices.data()));
+      // peer access between every pair: the row-partitioned PCG pushes z and
+      // its partial sums straight into the other devices' replicas
+      bool peer = true;
+      for (int i = 0; i < n_devices && peer; ++i)
+        for (int j = 0; j < n_devices && peer; ++j) {
+          if (i == j) continue;
+          int ok = 0;
+          SFM_CUDA(cudaDeviceCanAccessPeer(&ok, devices[i], devices[j]));
+          if (!ok) { peer = false; break; }
+          SFM_CUDA(cudaSetDevice(devices[i]));
+          const cudaError_t e = cudaDeviceEnablePeerAccess(devices[j], 0);
+          if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+          else if (e != cudaSuccess) { cudaGetLastError(); peer = false; }
+        }
+      ctx->group.peer = peer;
     }
     SFM_CUDA(cudaSetDevice(ctx->device));
   });

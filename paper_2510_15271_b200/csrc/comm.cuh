@@ -72,6 +72,10 @@ struct EmuGroup {
   // every rank hands in `mine`; rank 0 runs fn(all ranks' pointers) on its
   // stream, then everyone continues (one launch covering every rank)
   void run_root(int rank, const void* mine, cudaStream_t s, const std::function<void(const void* const*)>& fn);
+  // every rank hands in `mine` and gets everyone's; rank 0 runs root_prep;
+  // then every rank runs fn on its own stream and waits for it
+  void run_each(int rank, const void* mine, cudaStream_t s, const std::function<void()>& root_prep,
+                const std::function<void(const void* const*)>& fn);
 };
 
 struct Comm {
@@ -79,7 +83,10 @@ struct Comm {
   int world = 1;
   ncclComm_t comm = nullptr;
   bool owned = true;        // false: a communicator of a multi-device context (sfm_ctx_create_multi)
-  EmuGroup* emu = nullptr;
+  EmuGroup* emu = nullptr;  // ranks sharing a device: every collective through this host group
+  EmuGroup* host = nullptr; // ranks of one process (multi-device context): host-side exchanges / barriers
+  bool peer = false;        // every device pair of the process has peer access
+  int pcg_partition = 0;    // sfm_ba_options.pcg_partition (set by the solver)
 
   void init(int r, int w, const uint8_t* id_bytes) {
     rank = r;

@@ -97,6 +97,32 @@ void EmuGroup::run_root(int rank, const void* mine, cudaStream_t s,
   barrier();
 }
 
+void EmuGroup::run_each(int rank, const void* mine, cudaStream_t s, const std::function<void()>& root_prep,
+                        const std::function<void(const void* const*)>& fn) {
+  SFM_CUDA(cudaStreamSynchronize(s));
+  ptr_a[rank] = const_cast<void*>(mine);
+  barrier();
+  std::vector<const void*> all(ptr_a.begin(), ptr_a.end());
+  if (rank == 0) {
+    try {
+      root_prep();
+      SFM_CUDA(cudaStreamSynchronize(s));
+    } catch (...) {
+      abort();
+      throw;
+    }
+  }
+  barrier();
+  try {
+    fn(all.data());
+    SFM_CUDA(cudaStreamSynchronize(s));
+  } catch (...) {
+    abort();
+    throw;
+  }
+  barrier();
+}
+
 template <typename T>
 void EmuGroup::reduce(int rank, T* d, size_t n, cudaStream_t s, int op) {
   SFM_CUDA(cudaStreamSynchronize(s));
@@ -220,9 +246,11 @@ void ba_solve_group(const DeviceGroup& g, const sfm_ba_problem* shards, const sf
         if (!g.comms.empty()) {
           comm.comm = g.comms[r];
           comm.owned = false;
+          comm.peer = g.peer;
         } else {
           comm.emu = &grp;
         }
+        comm.host = &grp;
         {
           BASolver solver(s, &prof, &comm);
           solver.setup(shards[r], opt);

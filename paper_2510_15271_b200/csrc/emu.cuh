@@ -14,6 +14,7 @@ namespace sfm {
 struct DeviceGroup {
   std::vector<int> devices;        // device of each rank
   std::vector<ncclComm_t> comms;   // one per rank (ncclCommInitAll), empty = shard emulation
+  bool peer = false;               // peer access enabled between every pair of devices
   int size() const { return (int)devices.size(); }
 };
 

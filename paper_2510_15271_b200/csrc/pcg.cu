@@ -396,6 +396,9 @@ struct Pcg3Args {
   const int* cluster_cta0; // [nc+1]
   int R;                   // ranks (1: single device)
   int rcta0[kPcgMaxRanks + 1];  // first CTA of each rank
+  int cta_base;            // global index of this launch's first CTA (per-rank launches)
+  unsigned* xbar;          // [2] cross-launch barrier counter | abort flag (null: grid.sync)
+  long long xbar_limit;    // spin budget of one cross-launch barrier, in clock64 cycles
   PcgRankView v[kPcgMaxRanks];  // per-rank buffers (pcg.cuh)
   int max_it;
   double rtol;
@@ -447,14 +450,14 @@ __device__ __forceinline__ double dot6_ss(const double* s, const double* v) {  /
 // the loop is the S stream itself: independent loads, no index -> z chain.
 // The head of every warp's chunk (wres.x blocks) is resident in shared
 // memory for the whole solve (Ssm).
-__device__ __forceinline__ void spmv_segments(const Pcg3Args& a, const double* __restrict__ S, const double* zc,
-                                              const int* lc, int kc0, double* seg, const double* Ssm,
-                                              const int* rpl) {
+__device__ __forceinline__ void spmv_segments(const Pcg3Args& a, int cta, const double* __restrict__ S,
+                                              const double* zc, const int* lc, int kc0, double* seg,
+                                              const double* Ssm, const int* rpl) {
   const unsigned full = 0xffffffffu;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int grp = lane / 6, comp = lane % 6;
-  const int4 ch = a.wchunk[blockIdx.x * kPcgWarps + warp];
-  const int2 wr = a.wres[blockIdx.x * kPcgWarps + warp];
+  const int4 ch = a.wchunk[cta * kPcgWarps + warp];
+  const int2 wr = a.wres[cta * kPcgWarps + warp];
   int kb = ch.x, r = ch.z, sidx = ch.w;
   const int ke = ch.y;
   // an empty chunk (a CTA with fewer blocks than warps) owns no segment:
@@ -744,6 +747,38 @@ __device__ __forceinline__ double2 block_sum2(double u, double v, double2* red) 
 #define PH_DUMP(it) do {} while (0)
 #endif
 
+// Barrier across several cooperative launches (one per rank: per-device
+// launches of a multi-GPU context, or per-rank launches sharing a device):
+// the launch's own grid barrier, then one system-scope arrival per launch
+// on a shared counter and a spin until every launch has arrived, then the
+// grid barrier again.  A spin that outlives xbar_limit cycles sets the abort
+// flag, which releases every later barrier at once (the solve then reports a
+// failure instead of hanging the device).
+__device__ __forceinline__ unsigned ld_acquire_sys(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void xlaunch_barrier(cg::grid_group& grid, const Pcg3Args& a, unsigned& epoch) {
+  __threadfence_system();  // this CTA's pushes into other ranks' replicas, system-wide
+  grid.sync();
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    epoch += 1;
+    const unsigned target = epoch * (unsigned)a.R;
+    atomicAdd_system(a.xbar, 1u);
+    const long long t0 = clock64();
+    while (ld_acquire_sys(a.xbar) < target) {
+      if (ld_acquire_sys(a.xbar + 1) != 0u) break;
+      if (clock64() - t0 > a.xbar_limit) {
+        atomicExch_system(a.xbar + 1, 1u);
+        break;
+      }
+    }
+  }
+  grid.sync();
+}
+
 __global__ void __launch_bounds__(kPcgMaxThreads, 1) k_pcg3(Pcg3Args a) {
   cg::grid_group grid = cg::this_grid();
   extern __shared__ double psm[];
@@ -773,10 +808,16 @@ __global__ void __launch_bounds__(kPcgMaxThreads, 1) k_pcg3(Pcg3Args a) {
   constexpr int kStagWin = 50;
   if (threadIdx.x == 0) { rr_ck[0] = INFINITY; rr_ck[1] = INFINITY; }
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int G = gridDim.x;
+  const int G = a.G;                        // CTAs over every launch
+  const int cta = a.cta_base + (int)blockIdx.x;
+  unsigned xepoch = 0;
+  auto gsync = [&]() {
+    if (a.xbar) xlaunch_barrier(grid, a, xepoch);
+    else grid.sync();
+  };
   // this CTA's rank and its buffers; the pushes go to every rank's replica
   int rk = 0;
-  while (rk + 1 < a.R && (int)blockIdx.x >= a.rcta0[rk + 1]) ++rk;
+  while (rk + 1 < a.R && cta >= a.rcta0[rk + 1]) ++rk;
   const PcgRankView& V = a.v[rk];
   const double* __restrict__ Sr = V.S;
   auto push_z = [&](int64_t i, double val) {
@@ -785,11 +826,11 @@ __global__ void __launch_bounds__(kPcgMaxThreads, 1) k_pcg3(Pcg3Args a) {
   auto push_part = [&](int64_t i, double val) {
     for (int q = 0; q < a.R; ++q) a.v[q].part[i] = val;
   };
-  const int row0 = a.cta_row0[blockIdx.x], row1 = a.cta_row0[blockIdx.x + 1];
+  const int row0 = a.cta_row0[cta], row1 = a.cta_row0[cta + 1];
   const int nrows = row1 - row0;
   const int kc0 = __ldg(a.row_ptr + row0);
   const int nblk = __ldg(a.row_ptr + row1) - kc0;
-  const int zl0 = a.zl_ptr[blockIdx.x], ndist = a.zl_ptr[blockIdx.x + 1] - zl0;
+  const int zl0 = a.zl_ptr[cta], ndist = a.zl_ptr[cta + 1] - zl0;
   // z cache fill: 3 double2 per distinct column, straight from L2
   // (threads from `first` on; the first warps are busy with the scalar sums)
   auto fill_zc = [&](int first) {
@@ -846,7 +887,7 @@ __global__ void __launch_bounds__(kPcgMaxThreads, 1) k_pcg3(Pcg3Args a) {
     if (two) m.Pc[t] = V.Pm[(int64_t)row0 * 36 + t];
   }
   if (two) {
-    const int k = a.cta_cluster[blockIdx.x];
+    const int k = a.cta_cluster[cta];
     for (int t = threadIdx.x; t < 6 * n6; t += kPcgThreads)
       m.Ae[t] = V.Aci[(int64_t)(6 * k + t / n6) * a.npad + t % n6];
   }
@@ -857,8 +898,8 @@ __global__ void __launch_bounds__(kPcgMaxThreads, 1) k_pcg3(Pcg3Args a) {
   const int* rpl = m.rp - row0;  // rpl[r] = row_ptr[r] for the CTA's rows
   // resident S blocks: the head of every warp's chunk (18 double2 per block)
   for (int w = 0; w < kPcgWarps; ++w) {
-    const int4 ch = a.wchunk[blockIdx.x * kPcgWarps + w];
-    const int2 wr = a.wres[blockIdx.x * kPcgWarps + w];
+    const int4 ch = a.wchunk[cta * kPcgWarps + w];
+    const int2 wr = a.wres[cta * kPcgWarps + w];
     const double2* src = reinterpret_cast<const double2*>(Sr + (int64_t)ch.x * 36);
     double2* dst = reinterpret_cast<double2*>(m.Ssm + (int64_t)wr.y * 36);
     for (int t = threadIdx.x; t < wr.x * 18; t += kPcgThreads) dst[t] = __ldg(src + t);
@@ -870,7 +911,7 @@ __global__ void __launch_bounds__(kPcgMaxThreads, 1) k_pcg3(Pcg3Args a) {
     if (threadIdx.x < 6) {
       double s = 0.0;
       for (int i = 0; i < nrows; ++i) s += m.y[i * 6 + threadIdx.x];
-      for (int q = 0; q < a.R; ++q) a.v[q].rpart[blockIdx.x * 6 + threadIdx.x] = s;
+      for (int q = 0; q < a.R; ++q) a.v[q].rpart[cta * 6 + threadIdx.x] = s;
     }
   };
 
@@ -883,10 +924,10 @@ __global__ void __launch_bounds__(kPcgMaxThreads, 1) k_pcg3(Pcg3Args a) {
   if (a.warm) {
     for (int i = warp; i < nrows; i += kPcgWarps)
       if (lane < 6) push_z((row0 + i) * 6 + lane, V.x[(row0 + i) * 6 + lane]);
-    grid.sync();
+    gsync();
     fill_zc(0);
     __syncthreads();
-    spmv_segments(a, Sr, m.zc, m.lc, kc0, m.seg, m.Ssm, rpl);
+    spmv_segments(a, cta, Sr, m.zc, m.lc, kc0, m.seg, m.Ssm, rpl);
     __syncthreads();
     double xb = 0.0, xw = 0.0;
     for (int i = warp; i < nrows; i += kPcgWarps)
@@ -900,8 +941,8 @@ __global__ void __launch_bounds__(kPcgMaxThreads, 1) k_pcg3(Pcg3Args a) {
         xw += x0 * w;
       }
     const double2 t = block_sum2(xb, xw, red);
-    if (threadIdx.x == 0) { push_part(part_rz + blockIdx.x, t.x); push_part(part_rz + G + blockIdx.x, t.y); }
-    grid.sync();
+    if (threadIdx.x == 0) { push_part(part_rz + cta, t.x); push_part(part_rz + G + cta, t.y); }
+    gsync();
     gather_after_sync(a, V.rpart, V.part + part_rz, sums, 2, m.rc, false, true, nullptr, nullptr, m.cc0);
     const double g = sums[0] / sums[1];
     gamma = (sums[1] > 0.0 && isfinite(g)) ? g : 0.0;
@@ -928,8 +969,8 @@ __global__ void __launch_bounds__(kPcgMaxThreads, 1) k_pcg3(Pcg3Args a) {
   }
   if (two) write_rpart();
   double2 sb = block_sum2(bb_l, 0.0, red);
-  if (threadIdx.x == 0) push_part(part_bb + blockIdx.x, sb.x);
-  grid.sync();
+  if (threadIdx.x == 0) push_part(part_bb + cta, sb.x);
+  gsync();
   gather_after_sync(a, V.rpart, V.part + part_bb, sums, 1, m.rc, two, true, nullptr, nullptr, m.cc0);
   const double bnorm = sqrt(sums[0]);
   stag_rr = (a.stag_slack * a.rtol * bnorm) * (a.stag_slack * a.rtol * bnorm);
@@ -949,8 +990,8 @@ __global__ void __launch_bounds__(kPcgMaxThreads, 1) k_pcg3(Pcg3Args a) {
     }
   }
   double2 s1 = block_sum2(rz_l, 0.0, red);
-  if (threadIdx.x == 0) push_part(part_rz + blockIdx.x, s1.x);
-  grid.sync();
+  if (threadIdx.x == 0) push_part(part_rz + cta, s1.x);
+  gsync();
   sums_and_zc(V.part + part_rz, 1, 0);
   double rz_old = sums[0];
   int it = 0, fail = 0, stop = PCG_STOP_MAX_ITERS;
@@ -962,7 +1003,7 @@ __global__ void __launch_bounds__(kPcgMaxThreads, 1) k_pcg3(Pcg3Args a) {
     PH_INIT();
     for (it = 0; it < a.max_it;) {
       // ---- phase 1: w = S z; p = z + beta p; q = w + beta q; P^T q --------
-      spmv_segments(a, Sr, m.zc, m.lc, kc0, m.seg, m.Ssm, rpl);
+      spmv_segments(a, cta, Sr, m.zc, m.lc, kc0, m.seg, m.Ssm, rpl);
       __syncthreads();
       PH(0);
       double pq_l = 0.0;
@@ -992,18 +1033,18 @@ __global__ void __launch_bounds__(kPcgMaxThreads, 1) k_pcg3(Pcg3Args a) {
         if (threadIdx.x == 0) {
           double sx = 0.0;
           for (int w = 0; w < kPcgWarps; ++w) sx += red[w].x;
-          push_part(part_pq + blockIdx.x, sx);
+          push_part(part_pq + cta, sx);
         } else if (two && threadIdx.x >= 32 && threadIdx.x < 38) {
           const int c = threadIdx.x - 32;
           double sr = 0.0;
           for (int i = 0; i < nrows; ++i) sr += m.y[i * 6 + c];
-          for (int q = 0; q < a.R; ++q) a.v[q].rpart[blockIdx.x * 6 + c] = sr;
+          for (int q = 0; q < a.R; ++q) a.v[q].rpart[cta * 6 + c] = sr;
         }
       }
       PH(9);
       PH(10);
       PH(1);
-      grid.sync();
+      gsync();
       PH(2);
       // ---- phase 2: x += alpha p; r -= alpha q; rc -= alpha P^T q; z = M^-1 r
       gather_after_sync(a, V.rpart, V.part + part_pq, sums, 1, m.rc, two, false, &rz_old, &sums[0], m.cc0);
@@ -1033,9 +1074,9 @@ __global__ void __launch_bounds__(kPcgMaxThreads, 1) k_pcg3(Pcg3Args a) {
         }
       }
       const double2 t = block_sum2_free(rz_n, rr_n, red);  // red last read before the grid barrier
-      if (threadIdx.x == 0) { push_part(part_rz + blockIdx.x, t.x); push_part(part_rz + G + blockIdx.x, t.y); }
+      if (threadIdx.x == 0) { push_part(part_rz + cta, t.x); push_part(part_rz + G + cta, t.y); }
       PH(5);
-      grid.sync();
+      gsync();
       PH(6);
       sums_and_zc(V.part + part_rz, 2, it + 1);
       PH(7);
@@ -1051,7 +1092,8 @@ __global__ void __launch_bounds__(kPcgMaxThreads, 1) k_pcg3(Pcg3Args a) {
   }
   for (int i = warp; i < nrows; i += kPcgWarps)
     if (lane < 6) V.x[(row0 + i) * 6 + lane] = m.x[i * 6 + lane];
-  if ((int)blockIdx.x == a.rcta0[rk] && threadIdx.x == 0) {  // every rank's scalars
+  if (a.xbar && ld_acquire_sys(a.xbar + 1) != 0u) fail = 1;  // a cross-launch barrier gave up
+  if (cta == a.rcta0[rk] && threadIdx.x == 0) {  // every rank's scalars
     V.sc->pcg_iters = it;
     V.sc->pcg_fail = fail;
     V.sc->pcg_stop = fail ? PCG_STOP_FAILED : stop;
@@ -1477,11 +1519,38 @@ void TwoLevelPcg::solve(const PcgProblem& p, int max_it, double rtol, BAScalars*
   mine.S = p.S; mine.b = p.b; mine.x = p.x; mine.Minv = Minv_.get(); mine.Pm = Pm_.get();
   mine.Aci = coarse_on ? Aci_ : nullptr; mine.z = z_.get(); mine.part = part_.get(); mine.rpart = rpart_.get();
   mine.sc = sc;
+  mine.xbar = nullptr;
+  const bool separate = parted && coll->separate_launches();
+  if (separate && my == 0) {
+    xbar_.resize(2);
+    mine.xbar = xbar_.get();
+  }
   ProfScope ps(*prof, "pcg", 0.0, s);
-  auto launch = [&](const PcgRankView* views) {
+  auto fill = [&](const PcgRankView* views) {
     a.R = parted ? world_ : 1;
     for (int r = 0; r < a.R; ++r) a.v[r] = views[r];
     for (int r = 0; r <= a.R; ++r) a.rcta0[r] = parted ? rank_cta0_[r] : (r ? grid_ : 0);
+  };
+  if (separate) {
+    // one cooperative launch per rank over its CTAs, meeting at the
+    // cross-launch barrier (2 s spin budget per barrier, then a reported
+    // failure instead of a hang)
+    coll->launch_each(mine, s, [&]() { SFM_CUDA(cudaMemsetAsync(xbar_.get(), 0, 2 * sizeof(unsigned), s)); },
+                      [&](const PcgRankView* views) {
+                        fill(views);
+                        a.cta_base = rank_cta0_[my];
+                        a.xbar = views[0].xbar;
+                        a.xbar_limit = 4000000000ll;
+                        void* args[] = {&a};
+                        SFM_CUDA(cudaLaunchCooperativeKernel((void*)k_pcg3, rank_cta0_[my + 1] - rank_cta0_[my],
+                                                             nt_, args, smem_, s));
+                      });
+    return;
+  }
+  auto launch = [&](const PcgRankView* views) {
+    fill(views);
+    a.cta_base = 0;
+    a.xbar = nullptr;
     void* args[] = {&a};
     SFM_CUDA(cudaLaunchCooperativeKernel((void*)k_pcg3, grid_, nt_, args, smem_, s));
   };

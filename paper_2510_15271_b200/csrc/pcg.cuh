@@ -42,6 +42,7 @@ struct PcgRankView {       // one rank's buffers for one solve
   double* part;            // [4G]       replica of the per-CTA scalar partials
   double* rpart;           // [6G]       replica of the per-CTA restriction partials
   BAScalars* sc;           // the rank's scalars (iterations, stop reason, failure)
+  unsigned* xbar;          // rank 0: the cross-launch barrier counter | abort flag
 };
 
 // How a rank's TwoLevelPcg meets the others (implemented over Comm in ba.cu).
@@ -57,6 +58,15 @@ class PcgCollective {
   // rank's CTAs on the shared device)
   virtual void launch_all(const PcgRankView& mine, cudaStream_t s,
                           const std::function<void(const PcgRankView*)>& launch) = 0;
+  // true: every rank launches its own cooperative kernel over its CTAs and
+  // the launches meet at a cross-launch barrier (separate devices in one
+  // process with peer access, or -- pcg_partition 2 -- ranks sharing a device)
+  virtual bool separate_launches() const = 0;
+  // every rank hands in its view and gets all of them; rank 0 runs
+  // `root_prep` first (barrier reset); then every rank runs `launch` on its
+  // own stream and waits for it
+  virtual void launch_each(const PcgRankView& mine, cudaStream_t s, const std::function<void()>& root_prep,
+                           const std::function<void(const PcgRankView*)>& launch) = 0;
 };
 
 // Why a PCG solve stopped (BAScalars::pcg_stop).
@@ -112,6 +122,7 @@ class TwoLevelPcg {
   int npairs_ = 0;
   int world_ = 1, rank_ = 0;
   std::vector<int> rank_row0_, rank_blk0_, rank_cta0_, rank_pair0_;
+  DevBuf<unsigned> xbar_;                 // cross-launch barrier (rank 0)
   bool coarse_valid_ = false;
   double lam_build_ = 0.0, lam_max_ = 1e-2, drift_ = 4.0;
   double lam_floor_ = 1e-5;   // dampings below this count as equal (coarse rebuild rule)

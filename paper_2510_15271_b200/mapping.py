@@ -219,7 +219,7 @@ def _options(loss: RobustLoss, sopt: SolverOptions, dopt: DeviceOptions) -> nat.
                           int(dopt.pcg_max_iters), float(dopt.pcg_rtol), int(dopt.dense_max_dim),
                           int(dopt.coarse_cluster), int(dopt.coarse_refresh),
                           float(dopt.coarse_max_lambda), float(dopt.coarse_drift),
-                          1 if dopt.pcg_partition else 0, 0)
+                          int(dopt.pcg_partition), 0)
 
 
 def solve_arrays(arrays: BAArrays, loss: RobustLoss = TRIVIAL_LOSS,

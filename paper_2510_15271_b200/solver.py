@@ -61,9 +61,11 @@ class DeviceOptions:
     coarse_refresh: int = 8      # rebuild the coarse operator every N linearisations
     coarse_max_lambda: float = 1e-2  # above this damping: block-Jacobi only (S is diagonally dominant)
     coarse_drift: float = 4.0    # re-assemble A_c = P^T S(lambda) P when lambda moved by more than this
-    # point-sharded ranks sharing a device: row-partitioned PCG (False: the
-    # replicated PCG on the all-reduced S, which NCCL ranks always use)
-    pcg_partition: bool = True
+    # point-sharded ranks: 1 = row-partitioned PCG (one launch when the ranks
+    # share a device, one launch per device meeting at a cross-launch barrier
+    # in a multi-device context), 2 = per-rank launches on a shared device
+    # too, 0 = the replicated PCG on the all-reduced S (separate processes)
+    pcg_partition: int = 1
 
 
 DEFAULT_DEVICE_OPTIONS = DeviceOptions()

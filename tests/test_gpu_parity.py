@@ -262,16 +262,19 @@ def test_dropin_bundle_adjust_objects(golden):
     np.testing.assert_allclose(X, d["ref_points"], atol=1e-8)
 
 
-@pytest.mark.parametrize("partition", [True, False])
+@pytest.mark.parametrize("partition", [1, 0, 2])
 @pytest.mark.parametrize("n_shards", [2, 3, 4, 8])
 def test_point_sharded_solve_matches_single_rank(n_shards, partition):
     """SURVEY.md §8(e) on one B200: n logical ranks run the multi-GPU
     control flow (point shards balanced by observation count, partial Schur
     complements reduced -- reduce-scattered by block rows into the
-    row-partitioned PCG (partition=True: z and the dot products pushed
-    between the ranks inside the Krylov kernel, the solution allgathered) or
-    all-reduced into the replicated PCG -- reduced scalars); the result
-    equals the single-rank solve and the oracle's."""
+    row-partitioned PCG (partition 1: one launch over every rank's CTAs;
+    partition 2: one cooperative launch per rank meeting at the
+    cross-launch barrier, the multi-device mechanism; z and the dot products
+    pushed between the ranks inside the Krylov kernel, the solution
+    allgathered) or all-reduced into the replicated PCG (partition 0) --
+    reduced scalars); the result equals the single-rank solve and the
+    oracle's."""
     from oracle import ba as OB
     from paper_2510_15271_b200.mapping import solve_arrays, solve_sharded_emulated
     from paper_2510_15271_b200.scenes import make_scene, scene_arrays
