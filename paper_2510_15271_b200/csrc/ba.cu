@@ -1827,9 +1827,16 @@ void BASolver::setup(const sfm_ba_problem& pr, const sfm_ba_options& opt) {
     cudaStream_t ps = plan_stream_;
     cudaEvent_t pe = plan_ev_;
     // row-partitioned PCG: ranks sharing a device, or the devices of one
-    // process with peer access (NCCL ranks of separate processes: replicated)
+    // process with peer access (NCCL ranks of separate processes: replicated).
+    // Across devices each of the two barriers per iteration costs ~3.7 us
+    // more than a grid barrier (measured on one B200, tools/xbar_cost.py)
+    // plus the NVLink hop, so it only pays once S no longer fits in L2 and
+    // the SpMV it divides is HBM-bound; below that the replicated PCG on
+    // the reduced S is faster (scaling model).
+    const bool s_beyond_l2 = 288.0 * (double)n_full_ > 100e6;
     partitioned_ = comm_ && comm_->active() && opt_.pcg_partition != 0 &&
-                   (comm_->emu != nullptr || (comm_->host != nullptr && comm_->peer));
+                   (comm_->emu != nullptr ||
+                    (comm_->host != nullptr && comm_->peer && (s_beyond_l2 || opt_.pcg_partition == 2)));
     if (comm_) comm_->pcg_partition = opt_.pcg_partition;
     plan = std::async(std::launch::async, [this, dev, cl, refresh, ps, pe]() {
       SFM_CUDA(cudaSetDevice(dev));

@@ -748,11 +748,12 @@ __device__ __forceinline__ double2 block_sum2(double u, double v, double2* red) 
 #endif
 
 // Barrier across several cooperative launches (one per rank: per-device
-// launches of a multi-GPU context, or per-rank launches sharing a device):
-// the launch's own grid barrier, then one system-scope arrival per launch
-// on a shared counter and a spin until every launch has arrived, then the
-// grid barrier again.  A spin that outlives xbar_limit cycles sets the abort
-// flag, which releases every later barrier at once (the solve then reports a
+// launches of a multi-device context, or per-rank launches sharing a device):
+// every CTA of every launch arrives once on a shared counter in rank 0's
+// memory (system scope, after fencing its pushes system-wide) and spins until
+// all G CTAs of the epoch have arrived -- a one-level grid barrier spanning
+// the launches.  A spin that outlives xbar_limit cycles sets the abort flag,
+// which releases every later barrier at once (the solve then reports a
 // failure instead of hanging the device).
 __device__ __forceinline__ unsigned ld_acquire_sys(const unsigned* p) {
   unsigned v;
@@ -760,12 +761,12 @@ __device__ __forceinline__ unsigned ld_acquire_sys(const unsigned* p) {
   return v;
 }
 
-__device__ __forceinline__ void xlaunch_barrier(cg::grid_group& grid, const Pcg3Args& a, unsigned& epoch) {
-  __threadfence_system();  // this CTA's pushes into other ranks' replicas, system-wide
-  grid.sync();
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
+__device__ __forceinline__ void xlaunch_barrier(const Pcg3Args& a, unsigned& epoch) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();  // the CTA's pushes (ordered before by the CTA barrier), system-wide
     epoch += 1;
-    const unsigned target = epoch * (unsigned)a.R;
+    const unsigned target = epoch * (unsigned)a.G;
     atomicAdd_system(a.xbar, 1u);
     const long long t0 = clock64();
     while (ld_acquire_sys(a.xbar) < target) {
@@ -776,7 +777,7 @@ __device__ __forceinline__ void xlaunch_barrier(cg::grid_group& grid, const Pcg3
       }
     }
   }
-  grid.sync();
+  __syncthreads();
 }
 
 __global__ void __launch_bounds__(kPcgMaxThreads, 1) k_pcg3(Pcg3Args a) {
@@ -812,7 +813,7 @@ __global__ void __launch_bounds__(kPcgMaxThreads, 1) k_pcg3(Pcg3Args a) {
   const int cta = a.cta_base + (int)blockIdx.x;
   unsigned xepoch = 0;
   auto gsync = [&]() {
-    if (a.xbar) xlaunch_barrier(grid, a, xepoch);
+    if (a.xbar) xlaunch_barrier(a, xepoch);
     else grid.sync();
   };
   // this CTA's rank and its buffers; the pushes go to every rank's replica
