@@ -39,6 +39,11 @@ _, _, _, rep, raw = solve_arrays(a, huber, SolverOptions(max_iters=3), dev)
 print("pcg", rep.termination, rep.final_cost, raw.pcg_iterations)
 _, _, _, rep, raw = solve_arrays(a, huber, SolverOptions(max_iters=3, initial_lambda=1e3), dev)
 print("pcg high damping", rep.termination, rep.final_cost, raw.pcg_iterations)
+# point-sharded over 3 emulated ranks: reduce-scatter of S by block rows and
+# the row-partitioned PCG in one launch over every rank's CTAs
+from paper_2510_15271_b200.mapping import solve_sharded_emulated
+_, _, _, rep, raw = solve_sharded_emulated(a, huber, SolverOptions(max_iters=2), dev, 3)
+print("sharded", rep.termination, rep.final_cost, raw.pcg_iterations)
 # device-resident iterative_map: RANSAC, BA rounds, gating
 sc = make_scene(24, 1500, 7500, shape="curve", seed=3, outlier_frac=0.05, depth=(2.0, 40.0))
 models, n_models, fm = model_table([CameraModel(**sc.camera)] * sc.n_frames)
