@@ -119,6 +119,9 @@ class CommPcgCollective final : public PcgCollective {
 
 constexpr int kDenseMax = 210;    // packed lower triangle of 6*nf fits in smem
 constexpr int kBlock = 128;
+#ifndef SFM_PT_MINB
+#define SFM_PT_MINB 1    // A/B: min CTAs per SM of the point passes (caps of 6 / 8 spill and are slower)
+#endif
 
 // ---------------------------------------------------------------------------
 // small helpers
@@ -481,7 +484,7 @@ struct PointArgs {
 // delta_p = -e - V*^-1 sum_j Jp^T Jc dc_j (Jacobians at the linearization
 // state), X' = X + delta_p, then cost of (Rt_eval, X').
 template <bool TRIAL>
-__global__ void __launch_bounds__(kBlock) k_point_cost(PointArgs a) {
+__global__ void __launch_bounds__(kBlock, SFM_PT_MINB) k_point_cost(PointArgs a) {
   __shared__ double red[kBlock / 32];
   __shared__ sfm_camera_model smod[kSmemModels];
   const sfm_camera_model* models = stage_models(a.models, a.nmodels, smod);
@@ -656,7 +659,7 @@ __device__ __forceinline__ bool point_prep_one(const double* v, const double* g,
 }
 
 // V_i = sum Jp^T Jp, g_i = sum Jp^T r over ALL observations of the point.
-__global__ void __launch_bounds__(kBlock) k_point_lin(PointArgs a, double* __restrict__ V,
+__global__ void __launch_bounds__(kBlock, SFM_PT_MINB) k_point_lin(PointArgs a, double* __restrict__ V,
                                                       double* __restrict__ gp) {
   __shared__ sfm_camera_model smod[kSmemModels];
   const sfm_camera_model* models = stage_models(a.models, a.nmodels, smod);
@@ -2123,7 +2126,10 @@ void BASolver::linearize() {
       pa.sc_pre = sc_pre_.get();
       prep_lam_ = lam_;
     }
-    ProfScope ps(*prof_, "point_lin", 24.0 * N_ + 24.0 * P_ + 72.0 * P_ + 32.0 * N_ + (prep_ready_ ? 96.0 * P_ : 0.0), s);
+    // + the camera-major copy of the record (32 B) and its slot (4 B) per
+    // observation in a free camera, which this design writes here
+    ProfScope ps(*prof_, "point_lin", 24.0 * N_ + 24.0 * P_ + 72.0 * P_ + 32.0 * N_ + 36.0 * n_cm_ +
+                                          (prep_ready_ ? 96.0 * P_ : 0.0), s);
     k_point_lin<<<grid_for(P_, kBlock), kBlock, 0, s>>>(pa, V_.get(), gp_.get());
   }
   if (nfree_) {
