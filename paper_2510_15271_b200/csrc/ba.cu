@@ -119,9 +119,6 @@ class CommPcgCollective final : public PcgCollective {
 
 constexpr int kDenseMax = 210;    // packed lower triangle of 6*nf fits in smem
 constexpr int kBlock = 128;
-#ifndef SFM_PT_MINB
-#define SFM_PT_MINB 1    // A/B: min CTAs per SM of the point passes (caps of 6 / 8 spill and are slower)
-#endif
 
 // ---------------------------------------------------------------------------
 // small helpers
@@ -143,6 +140,21 @@ __device__ __forceinline__ void load_cam256(const double* __restrict__ Rt, int f
   R.m[0] = a.x; R.m[1] = a.y; R.m[2] = a.z; R.m[3] = a.w;
   R.m[4] = b.x; R.m[5] = b.y; R.m[6] = b.z; R.m[7] = b.w;
   R.m[8] = c.x; t = v3(c.y, c.z, c.w);
+}
+
+// Compact camera record q | t | 0 (64 B = two 256-bit loads) -> R, t.
+#ifndef SFM_PT_QCAM
+#define SFM_PT_QCAM 1   // point passes read the 64 B record (1) or the 96 B R | t (0)
+#endif
+__device__ __forceinline__ void load_cam_q(const double* __restrict__ Rt, const double* __restrict__ qt, int f,
+                                           Mat3& R, Vec3& t) {
+  if (SFM_PT_QCAM) {
+    const double4 a = ldg256(qt + (int64_t)f * 8), b = ldg256(qt + (int64_t)f * 8 + 4);
+    R = quat_to_matrix(Quat{a.x, a.y, a.z, a.w});
+    t = v3(b.x, b.y, b.z);
+  } else {
+    load_cam256(Rt, f, R, t);
+  }
 }
 
 // Camera models staged in shared memory when the table is small (the usual
@@ -243,8 +255,11 @@ __device__ __forceinline__ unsigned long long warp_max_u64(unsigned long long v)
 // setup kernels
 // ---------------------------------------------------------------------------
 
+// Camera records of a state: Rt = R (row-major) | t, 96 B, and the compact
+// qt = q | t | 0, 64 B (two 256-bit loads), from which the per-observation
+// point passes rebuild R (quat_to_matrix, the same arithmetic that made R).
 __global__ void k_frames_rt(int F, const double* __restrict__ q, const double* __restrict__ t,
-                            double* __restrict__ Rt) {
+                            double* __restrict__ Rt, double* __restrict__ qt) {
   int f = blockIdx.x * blockDim.x + threadIdx.x;
   if (f >= F) return;
   Mat3 R = quat_to_matrix(Quat{q[f * 4], q[f * 4 + 1], q[f * 4 + 2], q[f * 4 + 3]});
@@ -253,6 +268,13 @@ __global__ void k_frames_rt(int F, const double* __restrict__ q, const double* _
   Rt[f * 12 + 9] = t[f * 3];
   Rt[f * 12 + 10] = t[f * 3 + 1];
   Rt[f * 12 + 11] = t[f * 3 + 2];
+  if (qt) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) qt[f * 8 + i] = q[f * 4 + i];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) qt[f * 8 + 4 + i] = t[f * 3 + i];
+    qt[f * 8 + 7] = 0.0;
+  }
 }
 
 // Validates the layout contract: frames in range, points in range and
@@ -462,9 +484,11 @@ struct PointArgs {
   const sfm_camera_model* models;
   int nmodels;
   const int* free_idx;
-  const double* Rt;       // linearization state cameras
+  const double* Rt;       // linearization state cameras (R | t)
   const double* X;        // linearization state points
-  const double* Rt_eval;  // state whose cost is evaluated
+  const double* Rt_eval;  // state whose cost is evaluated (R | t)
+  const double* qt;       // linearization state cameras (q | t | 0), read by the point passes
+  const double* qt_eval;  // evaluated state (q | t | 0)
   double* X_out;          // trial points (TRIAL) or unused
   const double* pv;       // packed V*^-1 | e per point
   double lam;              // k_point_lin: also prepare pv for this lambda (the first trial's)
@@ -484,7 +508,7 @@ struct PointArgs {
 // delta_p = -e - V*^-1 sum_j Jp^T Jc dc_j (Jacobians at the linearization
 // state), X' = X + delta_p, then cost of (Rt_eval, X').
 template <bool TRIAL>
-__global__ void __launch_bounds__(kBlock, SFM_PT_MINB) k_point_cost(PointArgs a) {
+__global__ void __launch_bounds__(kBlock) k_point_cost(PointArgs a) {
   __shared__ double red[kBlock / 32];
   __shared__ sfm_camera_model smod[kSmemModels];
   const sfm_camera_model* models = stage_models(a.models, a.nmodels, smod);
@@ -502,7 +526,7 @@ __global__ void __launch_bounds__(kBlock, SFM_PT_MINB) k_point_cost(PointArgs a)
         const int j = a.free_idx[f];
         if (j < 0) continue;
         Mat3 R; Vec3 t;
-        load_cam256(a.Rt, f, R, t);
+        load_cam_q(a.Rt, a.qt, f, R, t);
         const sfm_camera_model& cm = models[a.frame_model[f]];
         double Jc[12], Jp[6];
         geo_jacobians(cm, R, ldg256(a.geo + o), Jc, Jp);
@@ -531,7 +555,7 @@ __global__ void __launch_bounds__(kBlock, SFM_PT_MINB) k_point_cost(PointArgs a)
       for (int64_t o = b0; o < b1; ++o) {
         const int f = a.of[o];
         Mat3 R; Vec3 t;
-        load_cam256(a.Rt_eval, f, R, t);
+        load_cam_q(a.Rt_eval, a.qt_eval, f, R, t);
         const sfm_camera_model& cm = models[a.frame_model[f]];
         Vec3 pc = add(mul(R, X), t);
         double u, v;
@@ -659,7 +683,7 @@ __device__ __forceinline__ bool point_prep_one(const double* v, const double* g,
 }
 
 // V_i = sum Jp^T Jp, g_i = sum Jp^T r over ALL observations of the point.
-__global__ void __launch_bounds__(kBlock, SFM_PT_MINB) k_point_lin(PointArgs a, double* __restrict__ V,
+__global__ void __launch_bounds__(kBlock) k_point_lin(PointArgs a, double* __restrict__ V,
                                                       double* __restrict__ gp) {
   __shared__ sfm_camera_model smod[kSmemModels];
   const sfm_camera_model* models = stage_models(a.models, a.nmodels, smod);
@@ -672,7 +696,7 @@ __global__ void __launch_bounds__(kBlock, SFM_PT_MINB) k_point_lin(PointArgs a, 
     for (int64_t o = a.ptr[p]; o < a.ptr[p + 1]; ++o) {
       const int f = a.of[o];
       Mat3 R; Vec3 t;
-      load_cam256(a.Rt, f, R, t);
+      load_cam_q(a.Rt, a.qt, f, R, t);
       const sfm_camera_model& cm = models[a.frame_model[f]];
       const double2 uv = reinterpret_cast<const double2*>(a.uv)[o];
       const Vec3 pc = add(mul(R, X), t);
@@ -1387,7 +1411,7 @@ __global__ void __launch_bounds__(1024) k_dense_solve(int nf, const int* __restr
 // ---------------------------------------------------------------------------
 __global__ void k_cam_trial(int nf, const int* __restrict__ free_frame, const double* __restrict__ dc,
                             const double* q, const double* t, const double* Rt, double* qo, double* to,
-                            double* Rto, double* __restrict__ part, BAScalars* sc) {
+                            double* Rto, double* qto, double* __restrict__ part, BAScalars* sc) {
   __shared__ double red[kBlock / 32];
   int j = blockIdx.x * blockDim.x + threadIdx.x;
   double s = 0.0;
@@ -1408,6 +1432,10 @@ __global__ void k_cam_trial(int nf, const int* __restrict__ free_frame, const do
     to[f * 3] = N.t.x; to[f * 3 + 1] = N.t.y; to[f * 3 + 2] = N.t.z;
     for (int i = 0; i < 9; ++i) Rto[f * 12 + i] = N.R.m[i];
     Rto[f * 12 + 9] = N.t.x; Rto[f * 12 + 10] = N.t.y; Rto[f * 12 + 11] = N.t.z;
+    if (qto) {
+      qto[f * 8] = N.q.w; qto[f * 8 + 1] = N.q.x; qto[f * 8 + 2] = N.q.y; qto[f * 8 + 3] = N.q.z;
+      qto[f * 8 + 4] = N.t.x; qto[f * 8 + 5] = N.t.y; qto[f * 8 + 6] = N.t.z; qto[f * 8 + 7] = 0.0;
+    }
   }
   double b = block_sum<kBlock>(s, red);
   if (threadIdx.x == 0) part[blockIdx.x] = b;
@@ -1562,7 +1590,8 @@ void BASolver::setup(const sfm_ba_problem& pr, const sfm_ba_options& opt) {
       }
     }
     Rt_[k].resize((size_t)F_ * 12);
-    if (F_) { k_frames_rt<<<grid_for(F_, 128), 128, 0, s>>>(F_, q_[k].get(), t_[k].get(), Rt_[k].get()); SFM_CHECK_LAUNCH(); }
+    qt_[k].resize((size_t)F_ * 8);
+    if (F_) { k_frames_rt<<<grid_for(F_, 128), 128, 0, s>>>(F_, q_[k].get(), t_[k].get(), Rt_[k].get(), qt_[k].get()); SFM_CHECK_LAUNCH(); }
   }
   cur_ = 0;
   // The points and pixels (~2/3 of the input bytes) are not read until the
@@ -2003,7 +2032,7 @@ void BASolver::restart() {
   if (F_) {
     SFM_CUDA(cudaMemcpyAsync(q_[0].get(), q0_.get(), q0_.bytes(), cudaMemcpyDeviceToDevice, s));
     SFM_CUDA(cudaMemcpyAsync(t_[0].get(), t0_.get(), t0_.bytes(), cudaMemcpyDeviceToDevice, s));
-    k_frames_rt<<<grid_for(F_, 128), 128, 0, s>>>(F_, q_[0].get(), t_[0].get(), Rt_[0].get());
+    k_frames_rt<<<grid_for(F_, 128), 128, 0, s>>>(F_, q_[0].get(), t_[0].get(), Rt_[0].get(), qt_[0].get());
     SFM_CHECK_LAUNCH();
   }
   if (P_) SFM_CUDA(cudaMemcpyAsync(X_[0].get(), X0_.get(), X0_.bytes(), cudaMemcpyDeviceToDevice, s));
@@ -2076,6 +2105,7 @@ double BASolver::eval_cost_current() {
   pa.frame_model = frame_model_.get(); pa.models = models_.get(); pa.nmodels = nmodels_;
   pa.free_idx = free_idx_.get();
   pa.Rt = Rt_[cur_].get(); pa.X = X_[cur_].get(); pa.Rt_eval = Rt_[cur_].get();
+  pa.qt = qt_[cur_].get(); pa.qt_eval = qt_[cur_].get();
   pa.obs_offset = obs_offset_; pa.part_cost = part_a_.get(); pa.part_dp2 = part_b_.get(); pa.sc = sc_.get();
   const unsigned gp = grid_for(std::max<int64_t>(P_, 1), kBlock);
   {
@@ -2113,6 +2143,7 @@ void BASolver::linearize() {
   pa.frame_model = frame_model_.get(); pa.models = models_.get(); pa.nmodels = nmodels_;
   pa.free_idx = free_idx_.get();
   pa.Rt = Rt_[cur_].get(); pa.X = X_[cur_].get(); pa.sc = sc_.get(); pa.geo = geo_.get();
+  pa.qt = qt_[cur_].get();
   pa.cm_pos = cm_pos_.get(); pa.geo_cm = geo_cm_.get();
   if (P_) {
     // compulsory: observation records in, points in, V/g_p and the 32-byte
@@ -2339,7 +2370,7 @@ bool BASolver::trial(double lam, double* new_cost, double* step_norm) {
   const unsigned gd = grid_for(std::max(nfree_, 1), kBlock);
   if (nfree_) {
     ProfScope ps(*prof_, "cam_trial", 0.0, s);
-    k_cam_trial<<<gd, kBlock, 0, s>>>(nfree_, free_frame_.get(), dc_.get(), q_[cur_].get(), t_[cur_].get(), Rt_[cur_].get(), q_[o].get(), t_[o].get(), Rt_[o].get(), part_d_.get(), sc_.get());
+    k_cam_trial<<<gd, kBlock, 0, s>>>(nfree_, free_frame_.get(), dc_.get(), q_[cur_].get(), t_[cur_].get(), Rt_[cur_].get(), q_[o].get(), t_[o].get(), Rt_[o].get(), qt_[o].get(), part_d_.get(), sc_.get());
   }
   PointArgs pa{};
   pa.P = P_; pa.lk = opt_.loss_kind; pa.lp = opt_.loss_param;
@@ -2347,6 +2378,7 @@ bool BASolver::trial(double lam, double* new_cost, double* step_norm) {
   pa.frame_model = frame_model_.get(); pa.models = models_.get(); pa.nmodels = nmodels_;
   pa.free_idx = free_idx_.get();
   pa.Rt = Rt_[cur_].get(); pa.X = X_[cur_].get(); pa.Rt_eval = Rt_[o].get(); pa.X_out = X_[o].get();
+  pa.qt = qt_[cur_].get(); pa.qt_eval = qt_[o].get();
   pa.pv = pv_.get(); pa.dc = dc_.get(); pa.geo = geo_.get();
   pa.obs_offset = obs_offset_; pa.part_cost = part_a_.get(); pa.part_dp2 = part_b_.get(); pa.sc = sc_.get();
   const unsigned gp = grid_for(std::max<int64_t>(P_, 1), kBlock);
@@ -2496,7 +2528,7 @@ void BASolver::eval(cudaStream_t s, Profiler* prof, const sfm_ba_problem& pr, in
   q.upload(pr.cam_q, (size_t)pr.n_frames * 4, s);
   t.upload(pr.cam_t, (size_t)pr.n_frames * 3, s);
   Rt.resize((size_t)pr.n_frames * 12);
-  if (pr.n_frames) { k_frames_rt<<<grid_for(pr.n_frames, 128), 128, 0, s>>>(pr.n_frames, q.get(), t.get(), Rt.get()); SFM_CHECK_LAUNCH(); }
+  if (pr.n_frames) { k_frames_rt<<<grid_for(pr.n_frames, 128), 128, 0, s>>>(pr.n_frames, q.get(), t.get(), Rt.get(), nullptr); SFM_CHECK_LAUNCH(); }
   X.upload(pr.points, (size_t)pr.n_points * 3, s);
   of.upload(pr.obs_frame, N, s);
   op.upload(pr.obs_point, N, s);

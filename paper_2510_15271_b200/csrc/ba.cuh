@@ -111,6 +111,7 @@ class BASolver {
   DevBuf<sfm_camera_model> models_;
   DevBuf<int> frame_model_, free_idx_, free_frame_;
   DevBuf<double> q_[2], t_[2], Rt_[2];  // [F*4], [F*3], [F*12]; index cur_
+  DevBuf<double> qt_[2];                // [F*8] q | t | 0 (the point passes' camera record)
   DevBuf<double> X_[2];                 // [P*3]
   DevBuf<double> q0_, t0_, X0_;         // entry state (save_entry / restart)
   int cur_ = 0;

@@ -661,7 +661,7 @@ void GBASolver::setup(const sfm_gba_problem& pr, const sfm_ba_options& opt) {
     q_[k].upload(pr.block_q, (size_t)nb_ * 4, s);
     t_[k].upload(pr.block_t, (size_t)nb_ * 3, s);
     Rt_[k].resize((size_t)nb_ * 12);
-    if (nb_) k_frames_rt<<<grid_for(nb_, 128), 128, 0, s>>>(nb_, q_[k].get(), t_[k].get(), Rt_[k].get());
+    if (nb_) k_frames_rt<<<grid_for(nb_, 128), 128, 0, s>>>(nb_, q_[k].get(), t_[k].get(), Rt_[k].get(), nullptr);
     X_[k].upload(pr.points, (size_t)P_ * 3, s);
   }
   cur_ = 0;
@@ -852,8 +852,8 @@ bool GBASolver::trial(double lam, double* new_cost, double* step_norm) {
   SFM_CUDA(cudaMemcpyAsync(Rt_[o].get(), Rt_[cur_].get(), sizeof(double) * 12 * nb_, cudaMemcpyDeviceToDevice, s));
   if (nf_)
     k_cam_trial<<<gd, kBlock, 0, s>>>(nf_, free_block_.get(), dc_.get(), q_[cur_].get(), t_[cur_].get(),
-                                      Rt_[cur_].get(), q_[o].get(), t_[o].get(), Rt_[o].get(), part_d_.get(),
-                                      sc_.get());
+                                      Rt_[cur_].get(), q_[o].get(), t_[o].get(), Rt_[o].get(), nullptr,
+                                      part_d_.get(), sc_.get());
   const unsigned gp = grid_for(std::max<int64_t>(P_, 1), kBlock);
   if (P_)
     k_gba_point_trial<<<gp, kBlock, 0, s>>>(P_, pptr_.get(), rkind_.get(), rslot_.get(), free_idx_.get(), rec_.get(),
