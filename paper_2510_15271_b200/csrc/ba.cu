@@ -2321,7 +2321,7 @@ bool BASolver::solve_implicit(double lam) {
         ProfScope ps(*prof_, "imp_point", 36.0 * N_ + 136.0 * P_, s);
         k_imp_point<<<grid_for(std::max<int64_t>(P_, 1), kBlock), kBlock, 0, s>>>(
             P_, pt_ptr_.get(), obs_frame_.get(), free_idx_.get(), frame_model_.get(), models_.get(), nmodels_,
-            Rt_[cur_].get(), geo_.get(), pv_.get(), imp_p_.get(), imp_s_.get(), imp_st_.get());
+            Rt_[cur_].get(), qt_[cur_].get(), geo_.get(), pv_.get(), imp_p_.get(), imp_s_.get(), imp_st_.get());
       }
       {
         ProfScope ps(*prof_, "imp_cam", 60.0 * n_cm_ + 96.0 * nfree_, s);

@@ -29,7 +29,8 @@ __global__ void __launch_bounds__(kBlock) k_imp_point(int64_t P, const int64_t* 
                                                       const int* __restrict__ of, const int* __restrict__ free_idx,
                                                       const int* __restrict__ frame_model,
                                                       const sfm_camera_model* __restrict__ models_g, int nmodels,
-                                                      const double* __restrict__ Rt, const double4* __restrict__ geo,
+                                                      const double* __restrict__ Rt, const double* __restrict__ qt,
+                                                      const double4* __restrict__ geo,
                                                       const double* __restrict__ pv, const double* __restrict__ pvec,
                                                       double* __restrict__ s, const ImpState* st) {
   __shared__ sfm_camera_model smod[kSmemModels];
@@ -43,7 +44,7 @@ __global__ void __launch_bounds__(kBlock) k_imp_point(int64_t P, const int64_t* 
     const int j = free_idx[f];
     if (j < 0) continue;
     Mat3 R; Vec3 t;
-    load_cam256(Rt, f, R, t);
+    load_cam_q(Rt, qt, f, R, t);
     double Jc[12], Jp[6];
     geo_jacobians(models[frame_model[f]], R, ldg256(geo + o), Jc, Jp);
     const double* d = pvec + (int64_t)j * 6;
