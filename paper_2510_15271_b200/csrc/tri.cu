@@ -121,23 +121,35 @@ __device__ __forceinline__ void givens_add(double Rm[10], double v[4]) {
 
 // Smallest right singular vector of the 4x4 upper-triangular R
 // (one-sided Jacobi on the columns).
-__device__ void smallest_right_sv(const double Rm[10], double out[4]) {
+__device__ __forceinline__ void smallest_right_sv(const double Rm[10], double out[4]) {
+  // every index below is a compile-time constant after unrolling, so A and
+  // V stay in registers (a runtime column index would put them in local
+  // memory for the whole sweep loop)
   double A[4][4];
   int base = 0;
+#pragma unroll
   for (int r = 0; r < 4; ++r)
+#pragma unroll
     for (int c = 0; c < 4; ++c) A[r][c] = 0.0;
+#pragma unroll
   for (int r = 0; r < 4; ++r) {
+#pragma unroll
     for (int c = r; c < 4; ++c) A[r][c] = Rm[base + (c - r)];
     base += 4 - r;
   }
   double V[4][4];
+#pragma unroll
   for (int r = 0; r < 4; ++r)
+#pragma unroll
     for (int c = 0; c < 4; ++c) V[r][c] = (r == c) ? 1.0 : 0.0;
   for (int sweep = 0; sweep < 40; ++sweep) {
     bool rotated = false;
+#pragma unroll
     for (int p = 0; p < 3; ++p)
+#pragma unroll
       for (int q = p + 1; q < 4; ++q) {
         double al = 0.0, be = 0.0, ga = 0.0;
+#pragma unroll
         for (int r = 0; r < 4; ++r) {
           al += A[r][p] * A[r][p];
           be += A[r][q] * A[r][q];
@@ -148,6 +160,7 @@ __device__ void smallest_right_sv(const double Rm[10], double out[4]) {
         double zeta = (be - al) / (2.0 * ga);
         double tt = copysign(1.0, zeta) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
         double cs = 1.0 / sqrt(1.0 + tt * tt), sn = cs * tt;
+#pragma unroll
         for (int r = 0; r < 4; ++r) {
           double a = A[r][p], b = A[r][q];
           A[r][p] = cs * a - sn * b;
@@ -159,17 +172,22 @@ __device__ void smallest_right_sv(const double Rm[10], double out[4]) {
       }
     if (!rotated) break;
   }
-  int best = 0;
-  double bn = 1e308;
+  // smallest column norm (first on ties), its V column selected by value
+  double bn = 1e308, v0 = 0.0, v1 = 0.0, v2 = 0.0, v3_ = 0.0;
+#pragma unroll
   for (int c = 0; c < 4; ++c) {
     double n = 0.0;
+#pragma unroll
     for (int r = 0; r < 4; ++r) n += A[r][c] * A[r][c];
-    if (n < bn) { bn = n; best = c; }
+    if (n < bn) { bn = n; v0 = V[0][c]; v1 = V[1][c]; v2 = V[2][c]; v3_ = V[3][c]; }
   }
   double nv = 0.0;
-  for (int r = 0; r < 4; ++r) nv += V[r][best] * V[r][best];
+  nv += v0 * v0;
+  nv += v1 * v1;
+  nv += v2 * v2;
+  nv += v3_ * v3_;
   nv = sqrt(nv);
-  for (int r = 0; r < 4; ++r) out[r] = V[r][best] / nv;
+  out[0] = v0 / nv; out[1] = v1 / nv; out[2] = v2 / nv; out[3] = v3_ / nv;
 }
 
 // Eigenvalues of a symmetric 3x3 (cyclic Jacobi) -> condition estimate.
@@ -596,22 +614,35 @@ __global__ void __launch_bounds__(kRansacWarps * 32) k_ransac(TrackArgs a) {
   const int npairs = k * (k - 1) / 2;
   int bcnt = -1, bidx = 0x7fffffff;
   double bneg = -INFINITY;
+  Vec3 bX = v3(0.0, 0.0, 0.0);  // this lane's best hypothesis (the winner is not re-solved)
   for (int pi = lane; pi < npairs; pi += 32) {
     int i, j;
     pair_of(k, pi, i, j);
     Vec3 X;
     if (tri_solve_sm(ob, (1u << i) | (1u << j), models, a.method, a.min_angle, true, X) != SFM_TRI_OK) continue;
-    // score_hyp: inlier count, then numpy's pairwise sum of their errors
+    // score_hyp: inlier count, then numpy's pairwise sum of their errors.
+    // Fewer than 8 inliers sum sequentially (NpSum's short path), so a
+    // track of k < 8 observations needs one pass over them, not two.
     int cnt = 0;
-    for (int o = 0; o < k; ++o) cnt += reproj_sm(ob[o], models, X) < a.thr;
-    NpSum acc(cnt);
-    for (int o = 0; o < k; ++o) {
-      const double e = reproj_sm(ob[o], models, X);
-      if (e < a.thr) acc.add(e);
+    double neg;
+    if (k < 8) {
+      double res = 0.0;
+      for (int o = 0; o < k; ++o) {
+        const double e = reproj_sm(ob[o], models, X);
+        if (e < a.thr) { ++cnt; res += e; }
+      }
+      neg = -res;
+    } else {
+      for (int o = 0; o < k; ++o) cnt += reproj_sm(ob[o], models, X) < a.thr;
+      NpSum acc(cnt);
+      for (int o = 0; o < k; ++o) {
+        const double e = reproj_sm(ob[o], models, X);
+        if (e < a.thr) acc.add(e);
+      }
+      neg = -acc.value();
     }
-    const double neg = -acc.value();
     if (cnt >= 2 && (cnt > bcnt || (cnt == bcnt && neg > bneg))) {
-      bcnt = cnt; bneg = neg; bidx = pi;
+      bcnt = cnt; bneg = neg; bidx = pi; bX = X;
     }
   }
   // warp arg-max: (count, -sum) lexicographic, lowest pair index on ties
@@ -629,14 +660,11 @@ __global__ void __launch_bounds__(kRansacWarps * 32) k_ransac(TrackArgs a) {
   Vec3 X = v3(NAN, NAN, NAN);
   unsigned inl = 0;
   if (bcnt >= 2) {
-    // the winning hypothesis again (lane 0), its inlier set across lanes
-    Vec3 Xb = v3(0.0, 0.0, 0.0);
-    if (lane == 0) {
-      int i, j;
-      pair_of(k, bidx, i, j);
-      tri_solve_sm(ob, (1u << i) | (1u << j), models, a.method, a.min_angle, true, Xb);
-    }
-    Xb = v3(__shfl_sync(0xffffffffu, Xb.x, 0), __shfl_sync(0xffffffffu, Xb.y, 0), __shfl_sync(0xffffffffu, Xb.z, 0));
+    // the winning hypothesis from the lane that scored it (pair bidx ran on
+    // lane bidx % 32), its inlier set across lanes
+    const int wl = bidx & 31;
+    const Vec3 Xb = v3(__shfl_sync(0xffffffffu, bX.x, wl), __shfl_sync(0xffffffffu, bX.y, wl),
+                       __shfl_sync(0xffffffffu, bX.z, wl));
     const unsigned sel = __ballot_sync(0xffffffffu, lane < k && reproj_sm(ob[lane < k ? lane : 0], models, Xb) < a.thr);
     // refinement on the inliers (midpoint has no parallax gate, :295)
     int st = SFM_TRI_FAILED;
