@@ -133,6 +133,14 @@ __device__ __forceinline__ double4 ldg256(const void* p) {
   return v;
 }
 
+// A camera's 6-vector (48 B, 16-byte aligned) as three 128-bit loads: a
+// gather across the warp costs one request per load instruction, not six.
+__device__ __forceinline__ void ldg_vec6(const double* p, double d[6]) {
+  const double2* q = reinterpret_cast<const double2*>(p);
+  const double2 a = __ldg(q), b = __ldg(q + 1), c = __ldg(q + 2);
+  d[0] = a.x; d[1] = a.y; d[2] = b.x; d[3] = b.y; d[4] = c.x; d[5] = c.y;
+}
+
 // Camera record R (row-major) | t: 96 bytes = three 256-bit loads.
 __device__ __forceinline__ void load_cam256(const double* __restrict__ Rt, int f, Mat3& R, Vec3& t) {
   const double* p = Rt + (int64_t)f * 12;
@@ -530,7 +538,8 @@ __global__ void __launch_bounds__(kBlock) k_point_cost(PointArgs a) {
         const sfm_camera_model& cm = models[a.frame_model[f]];
         double Jc[12], Jp[6];
         geo_jacobians(cm, R, ldg256(a.geo + o), Jc, Jp);
-        const double* d = a.dc + (int64_t)j * 6;
+        double d[6];
+        ldg_vec6(a.dc + (int64_t)j * 6, d);
         double y0 = 0.0, y1 = 0.0;
 #pragma unroll
         for (int k = 0; k < 6; ++k) { y0 += Jc[k] * d[k]; y1 += Jc[6 + k] * d[k]; }

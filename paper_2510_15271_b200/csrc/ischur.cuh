@@ -47,7 +47,8 @@ __global__ void __launch_bounds__(kBlock) k_imp_point(int64_t P, const int64_t* 
     load_cam_q(Rt, qt, f, R, t);
     double Jc[12], Jp[6];
     geo_jacobians(models[frame_model[f]], R, ldg256(geo + o), Jc, Jp);
-    const double* d = pvec + (int64_t)j * 6;
+    double d[6];
+    ldg_vec6(pvec + (int64_t)j * 6, d);
     double y0 = 0.0, y1 = 0.0;
 #pragma unroll
     for (int k = 0; k < 6; ++k) { y0 += Jc[k] * d[k]; y1 += Jc[6 + k] * d[k]; }
