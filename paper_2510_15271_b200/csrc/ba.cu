@@ -529,8 +529,10 @@ __global__ void __launch_bounds__(kBlock) k_point_cost(PointArgs a) {
     Vec3 X = load_X(a.X, p);
     if (TRIAL) {
       double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0;
+      int f_nx = b0 < b1 ? a.of[b0] : 0;  // the next observation's frame, one iteration ahead
       for (int64_t o = b0; o < b1; ++o) {
-        const int f = a.of[o];
+        const int f = f_nx;
+        if (o + 1 < b1) f_nx = a.of[o + 1];
         const int j = a.free_idx[f];
         if (j < 0) continue;
         Mat3 R; Vec3 t;
@@ -561,8 +563,10 @@ __global__ void __launch_bounds__(kBlock) k_point_cost(PointArgs a) {
       a.X_out[p * 3 + 2] = X.z;
     }
     if (!nonfinite) {
+      int f_nx = b0 < b1 ? a.of[b0] : 0;
       for (int64_t o = b0; o < b1; ++o) {
-        const int f = a.of[o];
+        const int f = f_nx;
+        if (o + 1 < b1) f_nx = a.of[o + 1];
         Mat3 R; Vec3 t;
         load_cam_q(a.Rt_eval, a.qt_eval, f, R, t);
         const sfm_camera_model& cm = models[a.frame_model[f]];

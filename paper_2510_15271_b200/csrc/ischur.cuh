@@ -39,8 +39,11 @@ __global__ void __launch_bounds__(kBlock) k_imp_point(int64_t P, const int64_t* 
   const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= P) return;
   double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0;
-  for (int64_t o = ptr[p]; o < ptr[p + 1]; ++o) {
-    const int f = of[o];
+  const int64_t b0 = ptr[p], b1 = ptr[p + 1];
+  int f_nx = b0 < b1 ? of[b0] : 0;  // the next observation's frame, one iteration ahead
+  for (int64_t o = b0; o < b1; ++o) {
+    const int f = f_nx;
+    if (o + 1 < b1) f_nx = of[o + 1];
     const int j = free_idx[f];
     if (j < 0) continue;
     Mat3 R; Vec3 t;
