@@ -356,8 +356,8 @@ def run_reference(args, rank, world):
 # --------------------------------------------------------------------------
 
 # profiler entry -> kernel symbol in the committed ncu capture (profiles/traffic.json)
-PROF_KERNEL = {"pcg": "k_pcg3", "schur_offdiag": "k_offdiag_blocks", "schur_diag": "k_cam_blocks<1>",
-               "cam_lin": "k_cam_blocks<0>", "point_lin": "k_point_lin", "point_trial": "k_point_cost<1>",
+PROF_KERNEL = {"pcg": "k_pcg3", "schur_offdiag": "k_offdiag_blocks", "schur_diag": "k_cam_fma<1>",
+               "cam_lin": "k_cam_fma<0>", "point_lin": "k_point_lin", "point_trial": "k_point_cost<1>",
                "point_prep": "k_point_prep", "imp_point": "k_imp_point", "imp_cam": "k_imp_cam"}
 HBM_KERNELS = ("point_lin", "point_trial", "cam_lin", "schur_diag", "schur_offdiag", "point_prep",
                "imp_point", "imp_cam")

@@ -98,6 +98,26 @@ def test_venice_1p4m_lm_iterations_match_oracle(venice_1p4m, rtol):
     scale = np.abs(Xo).max()
     np.testing.assert_allclose(X, Xo, atol=1e-8 * scale)
     np.testing.assert_allclose(t, to, atol=1e-8 * scale)
+
+
+def test_venice_1p4m_block_jacobi_only_matches_oracle(venice_1p4m):
+    """coarse_cluster < 0: the slow-converging block-Jacobi PCG (hundreds of
+    iterations per trial).  Neither the rounding-floor stagnation stop nor
+    the iteration cap may cut a trial short, and the steps still match the
+    oracle's exact solve."""
+    from paper_2510_15271_b200.mapping import solve_arrays
+    from paper_2510_15271_b200.solver import DeviceOptions, RobustLoss, SolverOptions
+    a, (qo, to, Xo, ro) = venice_1p4m
+    q, t, X, rep, raw = solve_arrays(a, RobustLoss("huber", 2.0), SolverOptions(max_iters=3),
+                                     DeviceOptions(linear_solver="pcg", pcg_rtol=1e-8, coarse_cluster=-1,
+                                                   pcg_max_iters=20000))
+    assert raw.pcg_stagnated == 0 and raw.pcg_max_hit == 0
+    assert raw.pcg_iterations > 3 * 100  # the regime the stagnation test must leave alone
+    assert rep.iterations == ro["iterations"] == 3
+    assert rep.final_cost == pytest.approx(ro["final_cost"], rel=1e-9)
+    scale = np.abs(Xo).max()
+    np.testing.assert_allclose(X, Xo, atol=1e-8 * scale)
+    np.testing.assert_allclose(t, to, atol=1e-8 * scale)
     np.testing.assert_allclose(q, qo, atol=1e-9)
 
 
