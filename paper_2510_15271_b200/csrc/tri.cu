@@ -570,12 +570,8 @@ __device__ int tri_solve_sm(const ObsSm* ob, unsigned sel, const sfm_camera_mode
   return SFM_TRI_OK;
 }
 
-// Warp per track: ransac_triangulate (mapping.py:255-305).
-__global__ void __launch_bounds__(kRansacWarps * 32) k_ransac(TrackArgs a) {
-  __shared__ ObsSm obs[kRansacWarps][kRansacMaxK];
-  const int64_t t = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (t >= a.T) return;
+// One track by the whole warp: ransac_triangulate (mapping.py:255-305).
+__device__ void ransac_track(const TrackArgs& a, int64_t t, int lane, ObsSm* ob) {
   const int64_t b0 = a.ptr[t], b1 = a.ptr[t + 1];
   const int k = (int)(b1 - b0);
   if (a.active && !a.active[t]) {
@@ -590,7 +586,7 @@ __global__ void __launch_bounds__(kRansacWarps * 32) k_ransac(TrackArgs a) {
     ransac_track_global(a, t, lane);
     return;
   }
-  ObsSm* ob = obs[warp];
+  __syncwarp();  // the previous track's readers of ob are done
   if (lane < k) {  // stage observation lane
     const int64_t o = b0 + lane;
     const int f = a.d.of[o];
@@ -685,6 +681,204 @@ __global__ void __launch_bounds__(kRansacWarps * 32) k_ransac(TrackArgs a) {
     a.status[t] = (int8_t)status;
     a.X[t * 3] = X.x; a.X[t * 3 + 1] = X.y; a.X[t * 3 + 2] = X.z;
   }
+}
+
+
+// Warp per track.
+__global__ void __launch_bounds__(kRansacWarps * 32) k_ransac(TrackArgs a) {
+  __shared__ ObsSm obs[kRansacWarps][kRansacMaxK];
+  const int64_t t = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (t >= a.T) return;
+  ransac_track(a, t, lane, obs[warp]);
+}
+
+// Short tracks share a warp.  Warp w takes tracks 3w .. 3w+2: when their
+// observations fit the warp's staging slots (sum k <= 32) and the active
+// tracks' pair hypotheses fit its lanes (sum k(k-1)/2 <= 32), all three run
+// in one pass -- each track's hypotheses on a contiguous lane range, a
+// segmented arg-max per range, the refinements on the ranges' first lanes in
+// parallel -- with each track's arithmetic exactly as in ransac_track, so the
+// statuses, masks and positions are the same bits.  Otherwise the warp runs
+// the three tracks one after another.  (configs[3]: k = 5, 10 hypotheses a
+// track, a third of the lanes busy one track per warp.)
+constexpr int kPack = 3;
+__global__ void __launch_bounds__(kRansacWarps * 32) k_ransac_packed(TrackArgs a) {
+  __shared__ ObsSm obs[kRansacWarps][kRansacMaxK];
+  const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t t0 = w * kPack;
+  if (t0 >= a.T) return;
+  const int nt = a.T - t0 < kPack ? (int)(a.T - t0) : kPack;
+  ObsSm* ob = obs[warp];
+  int kk[kPack], off[kPack + 1], hoff[kPack + 1];
+  bool act[kPack];
+  const int64_t base = a.ptr[t0];
+  off[0] = 0;
+  hoff[0] = 0;
+#pragma unroll
+  for (int q = 0; q < kPack; ++q) {
+    const bool in = q < nt;
+    kk[q] = in ? (int)(a.ptr[t0 + q + 1] - a.ptr[t0 + q]) : 0;
+    act[q] = in && (!a.active || a.active[t0 + q]);
+    off[q + 1] = off[q] + kk[q];
+    hoff[q + 1] = hoff[q] + (act[q] ? kk[q] * (kk[q] - 1) / 2 : 0);
+  }
+  if (off[kPack] > kRansacMaxK || hoff[kPack] > 32) {
+    for (int q = 0; q < nt; ++q) ransac_track(a, t0 + q, lane, ob);
+    return;
+  }
+  // stage the chunk's observations (one contiguous range), lane o <- observation o
+  const int ktot = off[kPack];
+  if (lane < ktot) {
+    const int64_t o = base + lane;
+    const int f = a.d.of[o];
+    ObsSm& m = ob[lane];
+    const double* p = a.d.Rt + (int64_t)f * 12;
+#pragma unroll
+    for (int i = 0; i < 9; ++i) m.R[i] = p[i];
+    m.t[0] = p[9]; m.t[1] = p[10]; m.t[2] = p[11];
+    m.ray[0] = a.d.ray[o * 3]; m.ray[1] = a.d.ray[o * 3 + 1]; m.ray[2] = a.d.ray[o * 3 + 2];
+    Mat3 R;
+#pragma unroll
+    for (int i = 0; i < 9; ++i) R.m[i] = m.R[i];
+    const Vec3 wd = mulT(R, v3(m.ray[0], m.ray[1], m.ray[2]));  // world_dir
+    m.w[0] = wd.x; m.w[1] = wd.y; m.w[2] = wd.z;
+    m.uv[0] = a.d.uv[o * 2]; m.uv[1] = a.d.uv[o * 2 + 1];
+    m.model = a.d.fm[f];
+    m.st = a.d.ray_st[o];
+  }
+  __syncwarp();
+  const sfm_camera_model* models = a.d.models;
+  // this lane's hypothesis: track hq, pair index pi within it
+  int hq = -1;
+#pragma unroll
+  for (int q = 0; q < kPack; ++q)
+    if (lane >= hoff[q] && lane < hoff[q + 1]) hq = q;
+  int qo = 0, qk = 0, hs = 0, he = 0;  // the lane's track: staging offset, k, lane range
+#pragma unroll
+  for (int q = 0; q < kPack; ++q)
+    if (q == hq) { qo = off[q]; qk = kk[q]; hs = hoff[q]; he = hoff[q + 1]; }
+  int bcnt = -1, bidx = 0x7fffffff;
+  double bneg = -INFINITY;
+  Vec3 bX = v3(0.0, 0.0, 0.0);
+  if (hq >= 0) {
+    const int pi = lane - hs;
+    const ObsSm* tob = ob + qo;
+    int i, j;
+    pair_of(qk, pi, i, j);
+    Vec3 X;
+    if (tri_solve_sm(tob, (1u << i) | (1u << j), models, a.method, a.min_angle, true, X) == SFM_TRI_OK) {
+      int cnt = 0;
+      double neg;
+      if (qk < 8) {
+        double res = 0.0;
+        for (int o = 0; o < qk; ++o) {
+          const double e = reproj_sm(tob[o], models, X);
+          if (e < a.thr) { ++cnt; res += e; }
+        }
+        neg = -res;
+      } else {
+        for (int o = 0; o < qk; ++o) cnt += reproj_sm(tob[o], models, X) < a.thr;
+        NpSum acc(cnt);
+        for (int o = 0; o < qk; ++o) {
+          const double e = reproj_sm(tob[o], models, X);
+          if (e < a.thr) acc.add(e);
+        }
+        neg = -acc.value();
+      }
+      if (cnt >= 2) { bcnt = cnt; bneg = neg; bidx = pi; bX = X; }
+    }
+  }
+  // segmented arg-max over each track's lane range: (count, -sum)
+  // lexicographic, lowest pair index on ties; the range's first lane ends
+  // with its track's winner
+#pragma unroll
+  for (int sh = 16; sh > 0; sh >>= 1) {
+    const int oc = __shfl_down_sync(0xffffffffu, bcnt, sh);
+    const double on = __shfl_down_sync(0xffffffffu, bneg, sh);
+    const int oi = __shfl_down_sync(0xffffffffu, bidx, sh);
+    const bool same = hq >= 0 && lane + sh < he;
+    const bool take = same && (oc > bcnt || (oc == bcnt && (on > bneg || (on == bneg && oi < bidx))));
+    if (take) { bcnt = oc; bneg = on; bidx = oi; }
+  }
+  // per observation lane: its track, that track's winner
+  int oq = -1;
+#pragma unroll
+  for (int q = 0; q < kPack; ++q)
+    if (lane >= off[q] && lane < off[q + 1]) oq = q;
+  int ohs = 0;
+  bool oact = false;
+#pragma unroll
+  for (int q = 0; q < kPack; ++q)
+    if (q == oq) { ohs = hoff[q]; oact = act[q]; }
+  const int wcnt = __shfl_sync(0xffffffffu, bcnt, ohs & 31);
+  const int widx = __shfl_sync(0xffffffffu, bidx, ohs & 31);
+  const int wl = (ohs + (wcnt >= 2 ? widx : 0)) & 31;
+  const Vec3 Xb = v3(__shfl_sync(0xffffffffu, bX.x, wl), __shfl_sync(0xffffffffu, bX.y, wl),
+                     __shfl_sync(0xffffffffu, bX.z, wl));
+  const bool obs_in = oq >= 0 && oact && wcnt >= 2;
+  const unsigned selall = __ballot_sync(0xffffffffu, obs_in && reproj_sm(ob[obs_in ? lane : 0], models, Xb) < a.thr);
+  // refinement on each track's inliers, on its range's first lane
+  int st = SFM_TRI_FAILED;
+  Vec3 X = v3(NAN, NAN, NAN);
+  const bool head = hq >= 0 && lane == hs;
+  if (head && bcnt >= 2) {
+    const unsigned sel = (selall >> qo) & ((qk >= 32) ? 0xffffffffu : ((1u << qk) - 1u));
+    st = tri_solve_sm(ob + qo, sel, models, a.method, a.min_angle, a.method == SFM_TRI_DLT, X);
+  }
+  // the track's refined position to its observation lanes
+  const int hl = ohs & 31;
+  const int rst = __shfl_sync(0xffffffffu, st, hl);
+  const Vec3 Xr = v3(__shfl_sync(0xffffffffu, X.x, hl), __shfl_sync(0xffffffffu, X.y, hl),
+                     __shfl_sync(0xffffffffu, X.z, hl));
+  const bool refined = obs_in && rst == SFM_TRI_OK;
+  const unsigned inlall = __ballot_sync(0xffffffffu, refined && reproj_sm(ob[refined ? lane : 0], models, Xr) < a.thr);
+  // per track: status from its inlier count, mask bits, position
+#pragma unroll
+  for (int q = 0; q < kPack; ++q) {
+    if (q >= nt) break;
+    const int64_t t = t0 + q;
+    const unsigned bits = (inlall >> off[q]) & ((kk[q] >= 32) ? 0xffffffffu : ((1u << kk[q]) - 1u));
+    if (!act[q]) {
+      if (lane < kk[q]) a.mask[base + off[q] + lane] = 0;
+      if (lane == 0) {
+        a.status[t] = SFM_TRI_SKIPPED;
+        a.X[t * 3] = a.X[t * 3 + 1] = a.X[t * 3 + 2] = NAN;
+      }
+      continue;
+    }
+    const int hl_q = hoff[q] & 31;
+    const int rq = __shfl_sync(0xffffffffu, st, hl_q);
+    const int cq = __shfl_sync(0xffffffffu, bcnt, hl_q);
+    const Vec3 Xq = v3(__shfl_sync(0xffffffffu, X.x, hl_q), __shfl_sync(0xffffffffu, X.y, hl_q),
+                       __shfl_sync(0xffffffffu, X.z, hl_q));
+    const bool ok = cq >= 2 && rq == SFM_TRI_OK && __popc(bits) >= 2;
+    const unsigned mk = ok ? bits : 0u;
+    if (lane < kk[q]) a.mask[base + off[q] + lane] = (mk >> lane) & 1u;
+    if (lane == 0) {
+      a.status[t] = (int8_t)(ok ? SFM_TRI_OK : SFM_TRI_FAILED);
+      a.X[t * 3] = ok ? Xq.x : NAN; a.X[t * 3 + 1] = ok ? Xq.y : NAN; a.X[t * 3 + 2] = ok ? Xq.z : NAN;
+    }
+  }
+}
+
+#ifndef SFM_RANSAC_PACK
+#define SFM_RANSAC_PACK 1
+#endif
+// Packed warps when the mean track is short enough that three tracks' pair
+// hypotheses usually fit 32 lanes (mean k <= 5.5); otherwise most packed
+// warps would fall back to three tracks in series, which measured slower
+// than one track per warp (configs[1], k ~ 9: 47.8 vs 38.8 ms; configs[3],
+// k ~ 5: 191 vs 395 ms packed).
+void launch_ransac(const TrackArgs& a, int64_t n_obs, cudaStream_t s) {
+  if (SFM_RANSAC_PACK && 2 * n_obs <= 11 * a.T) {
+    const int64_t warps = (a.T + kPack - 1) / kPack;
+    k_ransac_packed<<<grid_for(warps * 32, kRansacWarps * 32), kRansacWarps * 32, 0, s>>>(a);
+  } else {
+    k_ransac<<<grid_for(a.T * 32, kRansacWarps * 32), kRansacWarps * 32, 0, s>>>(a);
+  }
+  SFM_CHECK_LAUNCH();
 }
 
 __global__ void k_direct(TrackArgs a) {
@@ -790,7 +984,7 @@ void tri_ransac(cudaStream_t s, Profiler* prof, const sfm_tracks& tr, double thr
   a.thr = thr; a.min_angle = min_angle; a.method = method; a.X = X.get(); a.mask = mask.get(); a.status = st.get();
   if (tr.n_tracks) {
     ProfScope ps(*prof, "tri_ransac", 24.0 * tr.n_obs + 24.0 * tr.n_tracks + tr.n_obs, s);
-    k_ransac<<<grid_for(tr.n_tracks * 32, kRansacWarps * 32), kRansacWarps * 32, 0, s>>>(a);
+    launch_ransac(a, tr.n_obs, s);
   }
   X.download(out_X, (size_t)tr.n_tracks * 3, s);
   mask.download(out_mask, tr.n_obs, s);
@@ -873,7 +1067,7 @@ void tri_ransac_device(cudaStream_t s, Profiler* prof, const TriDeviceTracks& tr
   a.T = tr.n_tracks; a.ptr = tr.ptr; a.active = active; a.d = tri_data(tr);
   a.thr = thr; a.min_angle = min_angle; a.method = method; a.X = X; a.mask = mask; a.status = status;
   ProfScope ps(*prof, "tri_ransac", 24.0 * tr.n_obs + 24.0 * tr.n_tracks + tr.n_obs, s);
-  k_ransac<<<grid_for(tr.n_tracks * 32, kRansacWarps * 32), kRansacWarps * 32, 0, s>>>(a);
+  launch_ransac(a, tr.n_obs, s);
 }
 
 void tri_gate_device(cudaStream_t s, Profiler* prof, const TriDeviceTracks& tr, const double* P, double thr,
