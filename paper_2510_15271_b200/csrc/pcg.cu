@@ -19,7 +19,7 @@ namespace sfm {
 
 namespace {
 
-constexpr int kNB = 48;          // Gauss-Jordan tile (8 clusters x 6)
+constexpr int kNB = 48;          // Gauss-Jordan tile
 constexpr int kGJThreads = 256;
 #ifndef SFM_PCG_MAXT
 #define SFM_PCG_MAXT 512
@@ -41,7 +41,10 @@ __global__ void k_block_jacobi(int r0, int r1, const int* __restrict__ diag_pos,
   if (!ok) atomicOr(&sc->nonfinite, 1);
 }
 
-// P_j = Adj(T_j) (se3.py:204-211) of the free frame j's current pose.
+// P_j = [Adj(T_j) | (0, t_j)] of the free frame j's current pose: the
+// cluster's world-frame rigid motions (se3.py:204-211) as left
+// perturbations, and its scale (t_j -> (1+s) t_j: the translation part of the
+// perturbation, rotation-first ordering).  Row-major 6 x kCoarseDim.
 __global__ void k_coarse_basis(int nf, const int* __restrict__ free_frame, const double* q, const double* t,
                                const double* Rt, double* __restrict__ Pm) {
   int j = blockIdx.x * blockDim.x + threadIdx.x;
@@ -53,15 +56,20 @@ __global__ void k_coarse_basis(int nf, const int* __restrict__ free_frame, const
   for (int i = 0; i < 9; ++i) T.R.m[i] = Rt[f * 12 + i];
   double A[36];
   se3_adjoint(T, A);
-  for (int i = 0; i < 36; ++i) Pm[(int64_t)j * 36 + i] = A[i];
+  double* P = Pm + (int64_t)j * 6 * kCoarseDim;
+  for (int r = 0; r < 6; ++r) {
+    for (int c = 0; c < 6; ++c) P[r * kCoarseDim + c] = A[r * 6 + c];
+    P[r * kCoarseDim + 6] = r < 3 ? 0.0 : (r == 3 ? T.t.x : (r == 4 ? T.t.y : T.t.z));
+  }
 }
 
 // A_c = P^T S P, dense [npad x npad] row-major (zeroed beforehand).  Warp
 // per nonzero coarse block (c, d); its runs (row i of cluster c, the
 // contiguous blocks of row i whose columns fall in cluster d) are visited in
-// row order.  Inside a run the lanes take one S block each (T_k = S_k P_j),
-// the 36 products are summed over lanes in lane order through shared
-// memory, then acc += P_i^T T.
+// row order.  Inside a run the lanes take one S block each (T_k = S_k P_j,
+// 6 x kCoarseDim), the products are summed over lanes in lane order through
+// shared memory, then acc += P_i^T T (kCoarseDim x kCoarseDim).
+constexpr int kCD = kCoarseDim, kT = 6 * kCoarseDim, kA = kCoarseDim * kCoarseDim;
 __global__ void __launch_bounds__(128) k_coarse_assemble(int npairs, int npad, const int2* __restrict__ pair_cd,
                                                          const int* __restrict__ pair_run_ptr,
                                                          const int4* __restrict__ runs,
@@ -69,13 +77,15 @@ __global__ void __launch_bounds__(128) k_coarse_assemble(int npairs, int npad, c
                                                          const double* __restrict__ S,
                                                          const double* __restrict__ Pm,
                                                          double* __restrict__ Ac) {
-  __shared__ double Tsm[4][32][37];
-  __shared__ double Tsum[4][36];
+  __shared__ double Tsm[4][32][kT + 1];
+  __shared__ double Tsum[4][kT];
   const int pi = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (pi >= npairs) return;
+  // T entries this lane sums: lane, lane + 32 (< kT); A_c entries: lane, lane + 32 (< kA)
+  const int te1 = lane + 32;
   const int e0 = lane, e1 = lane + 32;
-  const int r0 = e0 / 6, cc0 = e0 % 6, r1 = e1 / 6, cc1 = e1 % 6;
+  const int r0 = e0 / kCD, cc0 = e0 % kCD, r1 = e1 / kCD, cc1 = e1 % kCD;
   double acc0 = 0.0, acc1 = 0.0;
   for (int q = pair_run_ptr[pi]; q < pair_run_ptr[pi + 1]; ++q) {
     const int4 run = runs[q];  // (row i, k0, k1, -)
@@ -85,48 +95,48 @@ __global__ void __launch_bounds__(128) k_coarse_assemble(int npairs, int npad, c
       const int nv = min(32, run.z - kb);
       if (k < run.z) {
         const double* Sb = S + (int64_t)k * 36;
-        const double* Pj = Pm + (int64_t)col[k] * 36;
-        double Pc[36];
+        const double* Pj = Pm + (int64_t)col[k] * kT;
+        double Pc[kT];
 #pragma unroll
-        for (int m = 0; m < 36; ++m) Pc[m] = __ldg(Pj + m);
+        for (int m = 0; m < kT; ++m) Pc[m] = __ldg(Pj + m);
 #pragma unroll
         for (int r = 0; r < 6; ++r) {
           double sr[6];
 #pragma unroll
           for (int m = 0; m < 6; ++m) sr[m] = __ldg(Sb + r * 6 + m);
 #pragma unroll
-          for (int c = 0; c < 6; ++c) {
+          for (int c = 0; c < kCD; ++c) {
             double v = 0.0;
 #pragma unroll
-            for (int m = 0; m < 6; ++m) v += sr[m] * Pc[m * 6 + c];
-            Tsm[warp][lane][r * 6 + c] = v;
+            for (int m = 0; m < 6; ++m) v += sr[m] * Pc[m * kCD + c];
+            Tsm[warp][lane][r * kCD + c] = v;
           }
         }
       }
       __syncwarp();
       for (int l = 0; l < nv; ++l) {
-        t0 += Tsm[warp][l][e0];
-        if (lane < 4) t1 += Tsm[warp][l][e1];
+        t0 += Tsm[warp][l][lane];
+        if (te1 < kT) t1 += Tsm[warp][l][te1];
       }
       __syncwarp();
     }
-    Tsum[warp][e0] = t0;
-    if (lane < 4) Tsum[warp][e1] = t1;
+    Tsum[warp][lane] = t0;
+    if (te1 < kT) Tsum[warp][te1] = t1;
     __syncwarp();
-    const double* Pi = Pm + (int64_t)run.x * 36;
+    const double* Pi = Pm + (int64_t)run.x * kT;
     double s0 = 0.0, s1 = 0.0;
 #pragma unroll
     for (int m = 0; m < 6; ++m) {
-      s0 += __ldg(Pi + m * 6 + r0) * Tsum[warp][m * 6 + cc0];
-      if (lane < 4) s1 += __ldg(Pi + m * 6 + r1) * Tsum[warp][m * 6 + cc1];
+      s0 += __ldg(Pi + m * kCD + r0) * Tsum[warp][m * kCD + cc0];
+      if (e1 < kA) s1 += __ldg(Pi + m * kCD + r1) * Tsum[warp][m * kCD + cc1];
     }
     acc0 += s0;
     acc1 += s1;
     __syncwarp();
   }
   const int2 cd = pair_cd[pi];
-  Ac[(int64_t)(6 * cd.x + r0) * npad + 6 * cd.y + cc0] = acc0;
-  if (lane < 4) Ac[(int64_t)(6 * cd.x + r1) * npad + 6 * cd.y + cc1] = acc1;
+  Ac[(int64_t)(kCD * cd.x + r0) * npad + kCD * cd.y + cc0] = acc0;
+  if (e1 < kA) Ac[(int64_t)(kCD * cd.x + r1) * npad + kCD * cd.y + cc1] = acc1;
 }
 
 __global__ void k_pad_identity(int first, int npad, double* Ac) {
@@ -549,16 +559,16 @@ __device__ __forceinline__ void spmv_segments(const Pcg3Args& a, int cta, const 
 // cluster's rows of A_c^-1) are staged once per solve.
 struct PcgSmem {
   double* seg;  // [maxsegs*6]
-  double* y;    // [maxrows*6]
-  double* rc;   // [6nc]
-  double* Ae;   // [6 x 6nc]
+  double* y;    // [maxrows*kCoarseDim] restriction per row
+  double* rc;   // [kCoarseDim*nc]
+  double* Ae;   // [kCoarseDim x kCoarseDim*nc]
   double* x;    // [maxrows*6] each
   double* r;
   double* p;
   double* q;
   double* z;
   double* Mi;   // [maxrows*36]
-  double* Pc;   // [maxrows*36]
+  double* Pc;   // [maxrows*6*kCoarseDim]
   double* Ssm;  // [resblocks*36] resident S blocks
   double* zc;   // [maxdist*6] z cache (distinct columns of the CTA's rows)
   int* lc;      // [maxblk] local column index of each of the CTA's blocks
@@ -580,15 +590,15 @@ __device__ __forceinline__ double precond_row(const PcgSmem& m, bool two, int i,
 #pragma unroll
     for (int j = 0; j < 6; ++j) zi = fma(M[j], rj[j], zi);
     if (two) {
-      const double* P = m.Pc + i * 36 + lane * 6;
+      const double* P = m.Pc + i * kT + lane * kCD;
 #pragma unroll
-      for (int j = 0; j < 6; ++j) zi = fma(P[j], e[j], zi);
+      for (int j = 0; j < kCD; ++j) zi = fma(P[j], e[j], zi);
     }
   }
   return zi;
 }
 
-// P_i^T v_i for lanes 0..5 (component lane)
+// P_i^T v_i for lanes 0..kCoarseDim-1 (coarse component lane)
 __device__ __forceinline__ double restrict_row(const PcgSmem& m, int i, double vi) {
   const unsigned full = 0xffffffffu;
   const int lane = threadIdx.x & 31;
@@ -596,10 +606,10 @@ __device__ __forceinline__ double restrict_row(const PcgSmem& m, int i, double v
 #pragma unroll
   for (int j = 0; j < 6; ++j) vj[j] = __shfl_sync(full, vi, j);
   double y = 0.0;
-  if (lane < 6) {
-    const double* P = m.Pc + i * 36;
+  if (lane < kCD) {
+    const double* P = m.Pc + i * kT;
 #pragma unroll
-    for (int k = 0; k < 6; ++k) y = fma(P[k * 6 + lane], vj[k], y);
+    for (int k = 0; k < 6; ++k) y = fma(P[k * kCD + lane], vj[k], y);
   }
   return y;
 }
@@ -645,8 +655,8 @@ __device__ __forceinline__ void gather_after_sync(const Pcg3Args& a, const doubl
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       const int t = t0 + j * tstride;
-      if (t < 6 * a.nc) {
-        qs[j] = __ldcg(rpart + cc0[t / 6] * 6 + t % 6);
+      if (t < kCD * a.nc) {
+        qs[j] = __ldcg(rpart + cc0[t / kCD] * kCD + t % kCD);
         nq = j + 1;
       }
     }
@@ -654,21 +664,21 @@ __device__ __forceinline__ void gather_after_sync(const Pcg3Args& a, const doubl
     for (int j = 0; j < 4; ++j) {
       const int t = t0 + j * tstride;
       if (j < nq)
-        for (int c = cc0[t / 6] + 1; c < cc0[t / 6 + 1]; ++c) qs[j] += __ldcg(rpart + c * 6 + t % 6);
+        for (int c = cc0[t / kCD] + 1; c < cc0[t / kCD + 1]; ++c) qs[j] += __ldcg(rpart + c * kCD + t % kCD);
     }
   }
   __syncthreads();
   if (two) {
     const double alpha = assign ? 0.0 : (*scale_num) / (*scale_den);
     int j = 0;
-    for (int t = threadIdx.x - 32 * nsum; t < 6 * a.nc && t >= 0 && j < nq; t += kPcgThreads - 32 * nsum, ++j)
+    for (int t = threadIdx.x - 32 * nsum; t < kCD * a.nc && t >= 0 && j < nq; t += kPcgThreads - 32 * nsum, ++j)
       rc[t] = assign ? qs[j] : rc[t] - alpha * qs[j];
     // threads that ran out of register slots finish the tail directly
-    for (int t = threadIdx.x - 32 * nsum + 4 * (kPcgThreads - 32 * nsum); t < 6 * a.nc && t >= 0;
+    for (int t = threadIdx.x - 32 * nsum + 4 * (kPcgThreads - 32 * nsum); t < kCD * a.nc && t >= 0;
          t += kPcgThreads - 32 * nsum) {
-      const int k = t / 6, mm = t % 6;
+      const int k = t / kCD, mm = t % kCD;
       double s = 0.0;
-      for (int c = cc0[k]; c < cc0[k + 1]; ++c) s += __ldcg(rpart + c * 6 + mm);
+      for (int c = cc0[k]; c < cc0[k + 1]; ++c) s += __ldcg(rpart + c * kCD + mm);
       rc[t] = assign ? s : rc[t] - alpha * s;
     }
   }
@@ -677,13 +687,14 @@ __device__ __forceinline__ void gather_after_sync(const Pcg3Args& a, const doubl
 
 // The two halves of e[0..5] = A_c^-1[6k.., :] . rc for this CTA's cluster k
 // (rows in smem) into tmp[12]; a reader forms e[j] = tmp[2j] + tmp[2j+1]
-// (coarse_e).  Warps 0..11: two warps per output row.
+// (coarse_e).  Warps 0..2*kCoarseDim-1: two warps per output row.
 __device__ __forceinline__ void coarse_apply(const Pcg3Args& a, const PcgSmem& m, double* tmp) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int n = 6 * a.nc;
-  if (warp < 12) {
+  const int n = kCD * a.nc, ldA = (n + 1) & ~1;
+  static_assert(2 * kCoarseDim <= 16, "two warps per coarse output row (512-thread CTAs have 16)");
+  if (warp < 2 * kCD) {
     const int o = warp >> 1, h = warp & 1;
-    const double* row = m.Ae + o * n;
+    const double* row = m.Ae + o * ldA;
     const int half = (n + 1) / 2;
     const int j0 = h * half, j1 = min(n, j0 + half);
     double s = 0.0;
@@ -694,9 +705,9 @@ __device__ __forceinline__ void coarse_apply(const Pcg3Args& a, const PcgSmem& m
   __syncthreads();
 }
 
-__device__ __forceinline__ void coarse_e(const double* tmp, double e[6]) {
+__device__ __forceinline__ void coarse_e(const double* tmp, double e[kCoarseDim]) {
 #pragma unroll
-  for (int j = 0; j < 6; ++j) e[j] = tmp[2 * j] + tmp[2 * j + 1];
+  for (int j = 0; j < kCD; ++j) e[j] = tmp[2 * j] + tmp[2 * j + 1];
 }
 
 // block_sum2 for a point where `red` is known to be free (right after a
@@ -783,20 +794,21 @@ __device__ __forceinline__ void xlaunch_barrier(const Pcg3Args& a, unsigned& epo
 __global__ void __launch_bounds__(kPcgMaxThreads, 1) k_pcg3(Pcg3Args a) {
   cg::grid_group grid = cg::this_grid();
   extern __shared__ double psm[];
-  const int MR = a.maxrows, n6 = 6 * a.nc;
+  const int MR = a.maxrows, nco = kCD * a.nc;
+  const int ldA = (nco + 1) & ~1;  // even strides keep every array 16-byte aligned
   PcgSmem m;
   m.seg = psm;
   m.y = m.seg + 6 * a.maxsegs;
-  m.rc = m.y + 6 * MR;
-  m.Ae = m.rc + n6;
-  m.x = m.Ae + 6 * n6;
+  m.rc = m.y + ((kCD * MR + 1) & ~1);
+  m.Ae = m.rc + ldA;
+  m.x = m.Ae + kCD * ldA;
   m.r = m.x + 6 * MR;
   m.p = m.r + 6 * MR;
   m.q = m.p + 6 * MR;
   m.z = m.q + 6 * MR;
   m.Mi = m.z + 6 * MR;
   m.Pc = m.Mi + 36 * MR;
-  m.Ssm = m.Pc + 36 * MR;
+  m.Ssm = m.Pc + kT * MR;
   m.zc = m.Ssm + 36 * a.resblocks;
   m.lc = reinterpret_cast<int*>(m.zc + 6 * a.maxdist);
   m.rs = reinterpret_cast<int2*>(m.lc + ((a.maxblk + 1) & ~1));
@@ -883,14 +895,12 @@ __global__ void __launch_bounds__(kPcgMaxThreads, 1) k_pcg3(Pcg3Args a) {
   const bool two = a.two != 0;
 
   // ---- stage the constant operators -----------------------------------------
-  for (int t = threadIdx.x; t < 36 * nrows; t += kPcgThreads) {
-    m.Mi[t] = V.Minv[(int64_t)row0 * 36 + t];
-    if (two) m.Pc[t] = V.Pm[(int64_t)row0 * 36 + t];
-  }
+  for (int t = threadIdx.x; t < 36 * nrows; t += kPcgThreads) m.Mi[t] = V.Minv[(int64_t)row0 * 36 + t];
   if (two) {
+    for (int t = threadIdx.x; t < kT * nrows; t += kPcgThreads) m.Pc[t] = V.Pm[(int64_t)row0 * kT + t];
     const int k = a.cta_cluster[cta];
-    for (int t = threadIdx.x; t < 6 * n6; t += kPcgThreads)
-      m.Ae[t] = V.Aci[(int64_t)(6 * k + t / n6) * a.npad + t % n6];
+    for (int t = threadIdx.x; t < kCD * nco; t += kPcgThreads)
+      m.Ae[(t / nco) * ldA + t % nco] = V.Aci[(int64_t)(kCD * k + t / nco) * a.npad + t % nco];
   }
   for (int t = threadIdx.x; t < nblk; t += kPcgThreads) m.lc[t] = __ldg(a.lcol + kc0 + t);
   for (int t = threadIdx.x; t < nrows; t += kPcgThreads) m.rs[t] = a.rowseg[row0 + t];
@@ -909,10 +919,10 @@ __global__ void __launch_bounds__(kPcgMaxThreads, 1) k_pcg3(Pcg3Args a) {
 
   auto write_rpart = [&]() {
     __syncthreads();
-    if (threadIdx.x < 6) {
+    if (threadIdx.x < kCD) {
       double s = 0.0;
-      for (int i = 0; i < nrows; ++i) s += m.y[i * 6 + threadIdx.x];
-      for (int q = 0; q < a.R; ++q) a.v[q].rpart[cta * 6 + threadIdx.x] = s;
+      for (int i = 0; i < nrows; ++i) s += m.y[i * kCD + threadIdx.x];
+      for (int q = 0; q < a.R; ++q) a.v[q].rpart[cta * kCD + threadIdx.x] = s;
     }
   };
 
@@ -965,7 +975,7 @@ __global__ void __launch_bounds__(kPcgMaxThreads, 1) k_pcg3(Pcg3Args a) {
     }
     if (two) {
       const double yv = restrict_row(m, i, ri);
-      if (lane < 6) m.y[i * 6 + lane] = yv;
+      if (lane < kCD) m.y[i * kCD + lane] = yv;
     }
   }
   if (two) write_rpart();
@@ -975,7 +985,9 @@ __global__ void __launch_bounds__(kPcgMaxThreads, 1) k_pcg3(Pcg3Args a) {
   gather_after_sync(a, V.rpart, V.part + part_bb, sums, 1, m.rc, two, true, nullptr, nullptr, m.cc0);
   const double bnorm = sqrt(sums[0]);
   stag_rr = (a.stag_slack * a.rtol * bnorm) * (a.stag_slack * a.rtol * bnorm);
-  double ev[6] = {0, 0, 0, 0, 0, 0};
+  double ev[kCoarseDim];
+#pragma unroll
+  for (int j = 0; j < kCD; ++j) ev[j] = 0.0;
   if (two) {
     coarse_apply(a, m, tmp);
     coarse_e(tmp, ev);
@@ -1022,7 +1034,7 @@ __global__ void __launch_bounds__(kPcgMaxThreads, 1) k_pcg3(Pcg3Args a) {
         }
         if (two) {
           const double yv = restrict_row(m, i, qv);
-          if (lane < 6) m.y[i * 6 + lane] = yv;
+          if (lane < kCD) m.y[i * kCD + lane] = yv;
         }
       }
       PH(8);
@@ -1035,11 +1047,11 @@ __global__ void __launch_bounds__(kPcgMaxThreads, 1) k_pcg3(Pcg3Args a) {
           double sx = 0.0;
           for (int w = 0; w < kPcgWarps; ++w) sx += red[w].x;
           push_part(part_pq + cta, sx);
-        } else if (two && threadIdx.x >= 32 && threadIdx.x < 38) {
+        } else if (two && threadIdx.x >= 32 && threadIdx.x < 32 + kCD) {
           const int c = threadIdx.x - 32;
           double sr = 0.0;
-          for (int i = 0; i < nrows; ++i) sr += m.y[i * 6 + c];
-          for (int q = 0; q < a.R; ++q) a.v[q].rpart[cta * 6 + c] = sr;
+          for (int i = 0; i < nrows; ++i) sr += m.y[i * kCD + c];
+          for (int q = 0; q < a.R; ++q) a.v[q].rpart[cta * kCD + c] = sr;
         }
       }
       PH(9);
@@ -1295,12 +1307,18 @@ void TwoLevelPcg::set_pattern(const int* row_ptr, const int* col, int nnzb, cuda
       cta_cluster[c] = k;
       for (int r = row0[c]; r < row0[c + 1]; ++r) frame_cluster[r] = k;
     }
-  ncp_ = ((nc_ + 7) / 8) * 8;
-  npad_ = 6 * ncp_;
+  // A_c is kCoarseDim*nc square, padded with identity rows to whole 48-row tiles
+  npad_ = ((kCoarseDim * nc_ + kNB - 1) / kNB) * kNB;
+  ncp_ = npad_ / kCoarseDim;
   grid_ = G;
   maxrows_ = maxrows;
   maxsegs_ = maxsegs;
-  smem_ = sizeof(double) * (size_t)(6 * maxsegs + 108 * maxrows + 42 * nc_);
+  {  // the kernel's carve-up (k_pcg3): seg | y | rc | Ae | x r p q z | Mi | Pc
+    const size_t ny = ((size_t)kCoarseDim * maxrows + 1) & ~(size_t)1;
+    const size_t ldA = ((size_t)kCoarseDim * nc_ + 1) & ~(size_t)1;
+    smem_ = sizeof(double) * (6 * (size_t)maxsegs + ny + ldA * (1 + kCoarseDim) +
+                              (30 + 36 + 6 * kCoarseDim) * (size_t)maxrows);
+  }
   SFM_REQUIRE(smem_ <= 200 * 1024, "PCG partition needs too much shared memory");
   // ---- S blocks kept resident in shared memory for the whole solve ---------
   // (the head of each warp's chunk, the same fraction in every warp)
@@ -1352,9 +1370,9 @@ void TwoLevelPcg::set_pattern(const int* row_ptr, const int* col, int nnzb, cuda
 
   mark("uploads");
   Minv_.resize((size_t)nf_ * 36);
-  Pm_.resize((size_t)nf_ * 36);
+  Pm_.resize((size_t)nf_ * 6 * kCoarseDim);
   r_.resize((size_t)nf_ * 6); z_.resize((size_t)nf_ * 6); p_.resize((size_t)nf_ * 6); q_.resize((size_t)nf_ * 6);
-  rpart_.resize((size_t)G * 6);
+  rpart_.resize((size_t)G * kCoarseDim);
   part_.resize(4 * (size_t)G);
   if (two) {
     Ac_[0].resize((size_t)npad_ * npad_);
@@ -1485,8 +1503,8 @@ void TwoLevelPcg::solve(const PcgProblem& p, int max_it, double rtol, BAScalars*
         k_coarse_assemble<<<grid_for((int64_t)(q1 - q0) * 32, 128), 128, 0, s>>>(
             q1 - q0, npad_, pair_cd_.get() + q0, pair_ptr_.get() + q0, runs_.get(), p.col, p.S, Pm_.get(),
             Ac_[0].get());
-      if (npad_ > 6 * nc_ && my == 0)
-        k_pad_identity<<<1, 256, 0, s>>>(6 * nc_, npad_, Ac_[0].get());
+      if (npad_ > kCoarseDim * nc_ && my == 0)
+        k_pad_identity<<<1, 256, 0, s>>>(kCoarseDim * nc_, npad_, Ac_[0].get());
       if (parted) coll->sum(Ac_[0].get(), (size_t)npad_ * npad_, s);  // disjoint rows: exact
     }
     double* A0 = Ac_[0].get();

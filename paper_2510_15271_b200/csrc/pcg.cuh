@@ -4,11 +4,13 @@
 // (solver.py:220-222, SuperLU on the un-reduced system) for large problems.
 // Preconditioner: additive two-level
 //     M^-1 r = D^-1 r + P A_c^-1 P^T r
-// with D the 6x6 block diagonal of S (block-Jacobi) and P the rigid-motion
+// with D the 6x6 block diagonal of S (block-Jacobi) and P the similarity
 // coarse space: cameras are aggregated into clusters of ~C consecutive free
-// frames (whole PCG CTA row ranges) and camera j's coarse basis is Adj(T_j) (a world-frame rigid motion
-// of the whole cluster, expressed as left perturbations).  A_c = P^T S P is
-// assembled on device and inverted by a cooperative blocked Gauss-Jordan.
+// frames (whole PCG CTA row ranges) and camera j's coarse basis is
+// [Adj(T_j) | (0, t_j)] -- a world-frame rigid motion and a world scaling of
+// the whole cluster, expressed as left perturbations (kCoarseDim = 7
+// columns).  A_c = P^T S P is assembled on device and inverted by a
+// cooperative blocked Gauss-Jordan.
 // The Krylov loop is one persistent cooperative kernel with two grid
 // barriers per iteration; every reduction has a fixed order.
 #pragma once
@@ -31,12 +33,19 @@ struct BAScalars;
 // after a barrier is rank-local.
 constexpr int kPcgMaxRanks = 16;
 
+// Coarse dimensions per cluster: the 6 rigid motions of the cluster plus its
+// scale (world scaling t_j -> (1+s) t_j, the similarity gauge's weak
+// direction that rigid motions do not span).  tools/precond_study.py, PCG
+// iterations to 1e-8 on S at the initial state: configs[2] 77 -> 26,
+// configs[1] 146 -> 25.
+constexpr int kCoarseDim = 7;
+
 struct PcgRankView {       // one rank's buffers for one solve
   const double* S;         // [nnzb*36]  valid in the rank's rows
   const double* b;         // [nf*6]     valid in the rank's rows
   double* x;               // [nf*6]     written in the rank's rows (warm start read there)
   const double* Minv;      // [nf*36]    block-Jacobi inverses of the rank's rows
-  const double* Pm;        // [nf*36]    coarse basis (all rows)
+  const double* Pm;        // [nf*6*kCoarseDim] coarse basis (all rows), row-major 6 x kCoarseDim
   const double* Aci;       // [npad^2]   coarse inverse (replicated), null = one level
   double* z;               // [nf*6]     replica of z (every CTA pushes its rows here)
   double* part;            // [4G]       replica of the per-CTA scalar partials

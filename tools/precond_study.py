@@ -276,16 +276,43 @@ if os.environ.get("NS") and S_hist:
 # the rigid-motion columns Adj(T_j) do not span ------------------------------
 if os.environ.get("SCALE"):
     for Cx in [int(v) for v in os.environ.get("SCALE_C", str(C)).split(",")]:
-        ncx = (nf + Cx - 1) // Cx
-        clx = np.arange(nf) // Cx
+        # balanced clusters of ~Cx frames (no one-frame tail: 7 columns need 2+ frames)
+        ncx = max(1, nf // Cx)
+        clx = (np.arange(nf) * ncx) // nf
         Pd = np.zeros((nf, 6, 7))
         for i, f in enumerate(free):
             qq, tt = G.pose(q[f], t[f])
             Pd[i, :, :6] = G.adjoint((qq, tt))
             Pd[i, 3:, 6] = tt
         Px = sp.bsr_matrix((Pd, clx, np.arange(nf + 1)), shape=(6 * nf, 7 * ncx)).tocsr()
-        Acix = np.linalg.inv((Px.T @ (S @ Px)).toarray())
+        Ax = (Px.T @ (S @ Px)).toarray()
+        ev = np.linalg.eigvalsh(Ax)
+        print(f"rigid+scale C={Cx}: A_c eigenvalues {ev[0]:.3e} .. {ev[-1]:.3e}", flush=True)
+        Acix = np.linalg.inv(Ax)
         pcg(lambda r: jac(r) + Px @ (Acix @ (Px.T @ r)), zero, f"additive rigid+scale C={Cx}")
+        # the same space with each cluster's 7 columns orthonormalised first
+        # (QR of the cluster's stacked 6n x 7 block): same span, A_c well scaled
+        Pq = np.zeros_like(Pd)
+        for c in range(ncx):
+            rows = np.flatnonzero(clx == c)
+            Bc = Pd[rows].reshape(-1, 7)
+            Q, _ = np.linalg.qr(Bc)
+            Pq[rows] = Q.reshape(len(rows), 6, 7)
+        Pxq = sp.bsr_matrix((Pq, clx, np.arange(nf + 1)), shape=(6 * nf, 7 * ncx)).tocsr()
+        Aq = (Pxq.T @ (S @ Pxq)).toarray()
+        evq = np.linalg.eigvalsh(Aq)
+        print(f"rigid+scale C={Cx} orthonormal: A_c eigenvalues {evq[0]:.3e} .. {evq[-1]:.3e}", flush=True)
+        Aciq = np.linalg.inv(Aq)
+        pcg(lambda r: jac(r) + Pxq @ (Aciq @ (Pxq.T @ r)), zero, f"additive rigid+scale C={Cx} orthonormal")
+        # rigid only, orthonormalised (the same span as the kernel's)
+        Pr = np.zeros((nf, 6, 6))
+        for c in range(ncx):
+            rows = np.flatnonzero(clx == c)
+            Q, _ = np.linalg.qr(Pd[rows, :, :6].reshape(-1, 6))
+            Pr[rows] = Q.reshape(len(rows), 6, 6)
+        Pxr = sp.bsr_matrix((Pr, clx, np.arange(nf + 1)), shape=(6 * nf, 6 * ncx)).tocsr()
+        Acir = np.linalg.inv((Pxr.T @ (S @ Pxr)).toarray())
+        pcg(lambda r: jac(r) + Pxr @ (Acir @ (Pxr.T @ r)), zero, f"additive rigid C={Cx} orthonormal")
         # global similarity (7 columns over all frames) on top of the rigid clusters
     Pg = np.zeros((nf, 6, 7))
     for i, f in enumerate(free):
