@@ -20,6 +20,9 @@ namespace sfm {
 namespace {
 
 constexpr int kNB = 48;          // Gauss-Jordan tile
+#ifndef SFM_GJ_SYM
+#define SFM_GJ_SYM 1  // upper-tile Gauss-Jordan on the symmetric coarse operator
+#endif
 constexpr int kGJThreads = 256;
 #ifndef SFM_PCG_MAXT
 #define SFM_PCG_MAXT 512
@@ -165,6 +168,20 @@ __device__ __forceinline__ void tile_mm(const double* __restrict__ A, const doub
   }
 }
 
+// acc += A^T B over 48x48 tiles (A read column-wise: a warp's lanes share
+// its rows, so the reads broadcast)
+__device__ __forceinline__ void tile_mm_at(const double* __restrict__ A, const double* __restrict__ B, int ty,
+                                           int tx, double acc[3][3]) {
+#pragma unroll 4
+  for (int m = 0; m < kNB; ++m) {
+    double a0 = A[m * kNB + ty * 3 + 0], a1 = A[m * kNB + ty * 3 + 1], a2 = A[m * kNB + ty * 3 + 2];
+    double b0 = B[m * kNB + tx * 3 + 0], b1 = B[m * kNB + tx * 3 + 1], b2 = B[m * kNB + tx * 3 + 2];
+    acc[0][0] += a0 * b0; acc[0][1] += a0 * b1; acc[0][2] += a0 * b2;
+    acc[1][0] += a1 * b0; acc[1][1] += a1 * b1; acc[1][2] += a1 * b2;
+    acc[2][0] += a2 * b0; acc[2][1] += a2 * b1; acc[2][2] += a2 * b2;
+  }
+}
+
 // In-register Gauss-Jordan inverse of the CTA's 48x48 tile P (thread
 // (ty, tx) holds rows 3ty.., columns 3tx..); one barrier per column, the
 // pivot row / column double-buffered in smem.  Writes the inverse to g.
@@ -270,6 +287,147 @@ __global__ void __launch_bounds__(kGJThreads) k_gj_inverse(double* A0, double* A
 #else
 #define GJP(k) do {} while (0)
 #endif
+#if SFM_GJ_SYM
+  // A_c is symmetric, and so is every Gauss-Jordan iterate up to sign: with
+  // the swept pivots S = {0..K-1} and the rest U, M_SS = A_SS^-1 and
+  // M_UU = A_UU - A_US A_SS^-1 A_SU are symmetric and M_US = -M_SU^T.  So
+  // only the upper tiles (I <= J) are updated -- half the tile products --
+  // and a lower tile a step needs is read as its transposed upper partner:
+  // M(K,J) = -M(J,K)^T for J < K, M(I,K) = M(K,I)^T for I > K.  The last
+  // step's upper triangle is mirrored at the end.
+  auto upper_of = [&](int u, int& I, int& J) {
+    I = 0;
+    while (u >= T - I) { u -= T - I; ++I; }
+    J = I + u;
+  };
+  auto upper_idx = [&](int I, int J) { return I * T - (I * (I - 1)) / 2 + (J - I); };
+  for (int K = 0; K < T; ++K) {
+    const double* src = (K & 1) ? A1 : A0;
+    double* dst = (K & 1) ? A0 : A1;
+    const double* pg = pivg + (K & 1) * kNB * kNB;
+    double* pg_next = pivg + ((K + 1) & 1) * kNB * kNB;
+    load_tile(pg, kNB, piv);
+    __syncthreads();
+    GJP(0);
+    const int nt = T * (T + 1) / 2;
+    const int next_diag = K + 1 < T ? upper_idx(K + 1, K + 1) : -1;
+    const int owner = next_diag >= 0 ? next_diag % (int)gridDim.x : -1;
+    const int G = (int)gridDim.x, bx = (int)blockIdx.x;
+    for (int it = bx - (owner == bx ? G : 0); it < nt; it += G) {
+      const bool first = it < 0;
+      const int tile = first ? next_diag : it;
+      if (!first && tile == next_diag) continue;  // done first
+      int I, J;
+      upper_of(tile, I, J);
+      double* out = dst;
+      double acc[3][3];
+      auto zero = [&]() {
+#pragma unroll
+        for (int a = 0; a < 3; ++a)
+#pragma unroll
+          for (int b = 0; b < 3; ++b) acc[a][b] = 0.0;
+      };
+      auto store = [&](int ti, int tj, double sgn) {
+#pragma unroll
+        for (int a = 0; a < 3; ++a)
+#pragma unroll
+          for (int b = 0; b < 3; ++b)
+            out[(int64_t)(ti * kNB + ty * 3 + a) * n + tj * kNB + tx * 3 + b] = sgn * acc[a][b];
+      };
+      if (I == K && J == K) {
+#pragma unroll
+        for (int a = 0; a < 3; ++a)
+#pragma unroll
+          for (int b = 0; b < 3; ++b) acc[a][b] = piv[(ty * 3 + a) * kNB + tx * 3 + b];
+        store(K, K, 1.0);
+        continue;
+      }
+      if (I == K) {  // row K (J > K): piv M(K,J)
+        load_tile(src + (int64_t)(K * kNB) * n + J * kNB, n, tKJ);
+        __syncthreads();
+        zero();
+        tile_mm(piv, tKJ, ty, tx, acc);
+        store(K, J, 1.0);
+        __syncthreads();
+        continue;
+      }
+      if (J == K) {  // column K (I < K): -M(I,K) piv
+        load_tile(src + (int64_t)(I * kNB) * n + K * kNB, n, tIK);
+        __syncthreads();
+        zero();
+        tile_mm(tIK, piv, ty, tx, acc);
+        store(I, K, -1.0);
+        __syncthreads();
+        continue;
+      }
+      // tM = piv M(K,J)
+      if (J > K) {
+        load_tile(src + (int64_t)(K * kNB) * n + J * kNB, n, tKJ);
+        __syncthreads();
+        zero();
+        tile_mm(piv, tKJ, ty, tx, acc);
+#pragma unroll
+        for (int a = 0; a < 3; ++a)
+#pragma unroll
+          for (int b = 0; b < 3; ++b) tM[(ty * 3 + a) * kNB + tx * 3 + b] = acc[a][b];
+      } else {  // M(K,J) = -M(J,K)^T: tM = -(M(J,K) piv)^T (piv symmetric)
+        load_tile(src + (int64_t)(J * kNB) * n + K * kNB, n, tKJ);
+        __syncthreads();
+        zero();
+        tile_mm(tKJ, piv, ty, tx, acc);
+#pragma unroll
+        for (int a = 0; a < 3; ++a)
+#pragma unroll
+          for (int b = 0; b < 3; ++b) tM[(tx * 3 + b) * kNB + ty * 3 + a] = -acc[a][b];
+      }
+      double old_ij[3][3];
+#pragma unroll
+      for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int b = 0; b < 3; ++b)
+          old_ij[a][b] = __ldcg(src + (int64_t)(I * kNB + ty * 3 + a) * n + J * kNB + tx * 3 + b);
+      // M(I,K): stored for I < K, M(K,I)^T for I > K
+      const bool iT = I > K;
+      load_tile(iT ? src + (int64_t)(K * kNB) * n + I * kNB : src + (int64_t)(I * kNB) * n + K * kNB, n, tIK);
+      __syncthreads();
+      zero();
+      if (iT) tile_mm_at(tIK, tM, ty, tx, acc);
+      else tile_mm(tIK, tM, ty, tx, acc);
+#pragma unroll
+      for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int b = 0; b < 3; ++b) acc[a][b] = old_ij[a][b] - acc[a][b];
+      store(I, J, 1.0);
+      GJP(1);
+      if (first) {  // the next step's pivot tile: invert it now
+        __syncthreads();
+        gj_invert_tile(acc, cbuf, rbuf, &bad, pg_next);
+        GJP(2);
+      }
+      __syncthreads();
+    }
+    GJP(3);
+    grid.sync();
+    GJP(4);
+  }
+  {  // mirror the inverse's upper tiles into the lower ones
+    double* res = (T & 1) ? A1 : A0;
+    const int G = (int)gridDim.x, bx = (int)blockIdx.x;
+    for (int tile = bx; tile < T * (T + 1) / 2; tile += G) {
+      int I, J;
+      upper_of(tile, I, J);
+      if (I == J) continue;
+      load_tile(res + (int64_t)(I * kNB) * n + J * kNB, n, tKJ);
+      __syncthreads();
+#pragma unroll
+      for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int b = 0; b < 3; ++b)
+          res[(int64_t)(J * kNB + ty * 3 + a) * n + I * kNB + tx * 3 + b] = tKJ[(tx * 3 + b) * kNB + ty * 3 + a];
+      __syncthreads();
+    }
+  }
+#else
   for (int K = 0; K < T; ++K) {
     const double* src = (K & 1) ? A1 : A0;
     double* dst = (K & 1) ? A0 : A1;
@@ -364,6 +522,7 @@ __global__ void __launch_bounds__(kGJThreads) k_gj_inverse(double* A0, double* A
     grid.sync();
     GJP(4);
   }
+#endif
 #ifdef SFM_GJ_PHASES
   if (tid == 0 && (blockIdx.x < 2 || blockIdx.x == 100))
     printf("GJ cta %d T=%d piv=%lld tiles=%lld inv=%lld tail=%lld sync=%lld\n", blockIdx.x, T, gt[0] / T, gt[1] / T,
