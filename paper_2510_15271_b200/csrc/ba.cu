@@ -773,14 +773,7 @@ __device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, dou
 // edge block is added on rank 0 and both BSR triangles written.
 constexpr int kOffWarps = 4;
 constexpr int kOffLd = 13;  // padded row of the staged factors (bank spread)
-#ifndef SFM_OFF_V
-#define SFM_OFF_V 0
-#endif
-#if SFM_OFF_V == 1
-constexpr int kOffRows = 64;
-#else
 constexpr int kOffRows = 32;
-#endif
 constexpr size_t kOffSmem = sizeof(double) * kOffWarps * 2 * kOffRows * kOffLd;
 
 // One packed header per off-diagonal work item (structure build): the
@@ -842,88 +835,6 @@ __global__ void __launch_bounds__(kOffWarps * 32, SFM_OFF_MINB) k_offdiag_blocks
     const Mat3& Rb = Rsm[warp][1];
     const sfm_camera_model& ca = Csm[warp][0];
     const sfm_camera_model& cb = Csm[warp][1];
-#if SFM_OFF_V == 1
-    // 64 pairs per round (lanes take pairs kb + lane and kb + 32 + lane):
-    // both halves' gathers are issued together, and the next round's pair
-    // records are loaded before this round's factors are computed, so a
-    // round waits for one L2 round trip instead of two
-    const int64_t k0 = kr.x, k1 = kr.y;
-    unsigned long long prA = 0, prB = 0;
-    int ptA = 0, ptB = 0;
-    if (k0 + lane < k1) { prA = __ldg(a.pairs + k0 + lane); ptA = __ldg(a.pair_pt + k0 + lane); }
-    if (k0 + 32 + lane < k1) { prB = __ldg(a.pairs + k0 + 32 + lane); ptB = __ldg(a.pair_pt + k0 + 32 + lane); }
-    auto stage = [&](double4 ga, double4 gb, double4 pva, double2 pvb, bool has, int row) {
-      double* As = &Aw[row * kOffLd];
-      double* Bs = &Bw[row * kOffLd];
-      if (!has) {
-#pragma unroll
-        for (int i = 0; i < 12; ++i) { As[i] = 0.0; Bs[i] = 0.0; }
-        return;
-      }
-      const double v0 = pva.x, v1 = pva.y, v2 = pva.z, v3_ = pva.w, v4 = pvb.x, v5 = pvb.y;
-      double Jca[12], Jpa[6];
-      geo_jacobians(ca, Ra, ga, Jca, Jpa);
-#pragma unroll
-      for (int i = 0; i < 12; ++i) As[i] = Jca[i];
-      double Jcb[12], Jpb[6];
-      geo_jacobians(cb, Rb, gb, Jcb, Jpb);
-      const double P00 = v0 * Jpb[0] + v1 * Jpb[1] + v2 * Jpb[2];
-      const double P01 = v1 * Jpb[0] + v3_ * Jpb[1] + v4 * Jpb[2];
-      const double P02 = v2 * Jpb[0] + v4 * Jpb[1] + v5 * Jpb[2];
-      const double P10 = v0 * Jpb[3] + v1 * Jpb[4] + v2 * Jpb[5];
-      const double P11 = v1 * Jpb[3] + v3_ * Jpb[4] + v4 * Jpb[5];
-      const double P12 = v2 * Jpb[3] + v4 * Jpb[4] + v5 * Jpb[5];
-      const double m00 = Jpa[0] * P00 + Jpa[1] * P01 + Jpa[2] * P02;
-      const double m01 = Jpa[0] * P10 + Jpa[1] * P11 + Jpa[2] * P12;
-      const double m10 = Jpa[3] * P00 + Jpa[4] * P01 + Jpa[5] * P02;
-      const double m11 = Jpa[3] * P10 + Jpa[4] * P11 + Jpa[5] * P12;
-#pragma unroll
-      for (int c = 0; c < 6; ++c) {
-        Bs[c] = -(m00 * Jcb[c] + m01 * Jcb[6 + c]);
-        Bs[6 + c] = -(m10 * Jcb[c] + m11 * Jcb[6 + c]);
-      }
-    };
-    for (int64_t kb = k0; kb < k1; kb += 64) {
-      const bool hasA = kb + lane < k1, hasB = kb + 32 + lane < k1;
-      double4 gaA = make_double4(0, 0, 0, 0), gbA = gaA, pvA = gaA, gaB = gaA, gbB = gaA, pvB = gaA;
-      double2 pwA = make_double2(0, 0), pwB = pwA;
-      if (hasA) {
-        gaA = ldg256(a.geo + (int64_t)(prA >> 32));
-        gbA = ldg256(a.geo + (int64_t)(uint32_t)prA);
-        pvA = ldg256(a.pv + (int64_t)ptA * 12);
-        pwA = __ldg(reinterpret_cast<const double2*>(a.pv + (int64_t)ptA * 12 + 4));
-      }
-      if (hasB) {
-        gaB = ldg256(a.geo + (int64_t)(prB >> 32));
-        gbB = ldg256(a.geo + (int64_t)(uint32_t)prB);
-        pvB = ldg256(a.pv + (int64_t)ptB * 12);
-        pwB = __ldg(reinterpret_cast<const double2*>(a.pv + (int64_t)ptB * 12 + 4));
-      }
-      {  // next round's pair records
-        const int64_t nA = kb + 64 + lane, nB = kb + 96 + lane;
-        if (nA < k1) { prA = __ldg(a.pairs + nA); ptA = __ldg(a.pair_pt + nA); }
-        if (nB < k1) { prB = __ldg(a.pairs + nB); ptB = __ldg(a.pair_pt + nB); }
-      }
-      stage(gaA, gbA, pvA, pwA, hasA, lane);
-      stage(gaB, gbB, pvB, pwB, hasB, 32 + lane);
-      __syncwarp();
-      const int nch = (int)((min((int64_t)64, k1 - kb) + 1) >> 1);
-      const int slot = (fk & 1) * 6 + fr;
-      for (int ch = 0; ch < nch; ch += 2) {
-        const int p0 = 2 * ch + (fk >> 1);
-        const double a0 = fr < 6 ? Aw[p0 * kOffLd + slot] : 0.0;
-        const double b0 = fr < 6 ? Bw[p0 * kOffLd + slot] : 0.0;
-        dmma_8x8x4(d0, d1, a0, b0);
-        if (ch + 1 < nch) {
-          const int p1 = p0 + 2;
-          const double a1 = fr < 6 ? Aw[p1 * kOffLd + slot] : 0.0;
-          const double b1 = fr < 6 ? Bw[p1 * kOffLd + slot] : 0.0;
-          dmma_8x8x4(e0, e1, a1, b1);
-        }
-      }
-      __syncwarp();
-    }
-#else
     const int64_t k0 = kr.x, k1 = kr.y;
     double* As = &Aw[lane * kOffLd];
     double* Bs = &Bw[lane * kOffLd];
@@ -978,7 +889,6 @@ __global__ void __launch_bounds__(kOffWarps * 32, SFM_OFF_MINB) k_offdiag_blocks
       }
       __syncwarp();
     }
-#endif
   }
   d0 += e0;
   d1 += e1;
