@@ -44,11 +44,38 @@ __global__ void k_block_jacobi(int r0, int r1, const int* __restrict__ diag_pos,
   if (!ok) atomicOr(&sc->nonfinite, 1);
 }
 
-// P_j = [Adj(T_j) | (0, t_j)] of the free frame j's current pose: the
-// cluster's world-frame rigid motions (se3.py:204-211) as left
-// perturbations, and its scale (t_j -> (1+s) t_j: the translation part of the
-// perturbation, rotation-first ordering).  Row-major 6 x kCoarseDim.
-__global__ void k_coarse_basis(int nf, const int* __restrict__ free_frame, const double* q, const double* t,
+// Centroid of cluster k's camera centres C_j = -R_j^T t_j (frames
+// [cluster_row0[k], cluster_row0[k+1])), in frame order.
+__global__ void k_cluster_centroid(int nc, const int* __restrict__ cluster_row0, const int* __restrict__ free_frame,
+                                   const double* __restrict__ t, const double* __restrict__ Rt, double* __restrict__ cen) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= nc) return;
+  double sx = 0.0, sy = 0.0, sz = 0.0;
+  const int j0 = cluster_row0[k], j1 = cluster_row0[k + 1];
+  for (int j = j0; j < j1; ++j) {
+    const int f = free_frame[j];
+    const double* R = Rt + (int64_t)f * 12;
+    const double tx = t[f * 3], ty = t[f * 3 + 1], tz = t[f * 3 + 2];
+    sx -= R[0] * tx + R[3] * ty + R[6] * tz;
+    sy -= R[1] * tx + R[4] * ty + R[7] * tz;
+    sz -= R[2] * tx + R[5] * ty + R[8] * tz;
+  }
+  const double inv = j1 > j0 ? 1.0 / (j1 - j0) : 0.0;
+  cen[k * 3] = sx * inv;
+  cen[k * 3 + 1] = sy * inv;
+  cen[k * 3 + 2] = sz * inv;
+}
+
+// Camera j's coarse basis, row-major 6 x kCoarseDim: its cluster's world
+// rigid motions about the cluster centroid c, as left perturbations
+// (Adj(T_j) [[I, 0], [hat(c), I]], se3.py:204-211), and the cluster's
+// scaling about c (t_j -> t_j + s (t_j + R_j c): the translation part of the
+// perturbation, rotation-first ordering).  About the centroid rather than the
+// world origin: the same span, but a cluster far from the origin would
+// otherwise see its rotations and its scale as near-translations and A_c
+// would lose the precision its Gauss-Jordan inverse needs.
+__global__ void k_coarse_basis(int nf, const int* __restrict__ free_frame, const int* __restrict__ frame_cluster,
+                               const double* __restrict__ cen, const double* q, const double* t,
                                const double* Rt, double* __restrict__ Pm) {
   int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= nf) return;
@@ -59,10 +86,22 @@ __global__ void k_coarse_basis(int nf, const int* __restrict__ free_frame, const
   for (int i = 0; i < 9; ++i) T.R.m[i] = Rt[f * 12 + i];
   double A[36];
   se3_adjoint(T, A);
+  const int k = frame_cluster[j];
+  const double c[3] = {cen[k * 3], cen[k * 3 + 1], cen[k * 3 + 2]};
+  const double hc[9] = {0.0, -c[2], c[1], c[2], 0.0, -c[0], -c[1], c[0], 0.0};  // hat(c)
   double* P = Pm + (int64_t)j * 6 * kCoarseDim;
   for (int r = 0; r < 6; ++r) {
-    for (int c = 0; c < 6; ++c) P[r * kCoarseDim + c] = A[r * 6 + c];
-    P[r * kCoarseDim + 6] = r < 3 ? 0.0 : (r == 3 ? T.t.x : (r == 4 ? T.t.y : T.t.z));
+    for (int i = 0; i < 3; ++i) {
+      double v = A[r * 6 + i];
+      for (int m = 0; m < 3; ++m) v += A[r * 6 + 3 + m] * hc[m * 3 + i];
+      P[r * kCoarseDim + i] = v;
+      P[r * kCoarseDim + 3 + i] = A[r * 6 + 3 + i];
+    }
+  }
+  if (kCoarseDim > 6) {
+    const Vec3 Rc = mul(T.R, v3(c[0], c[1], c[2]));
+    const double sc[6] = {0.0, 0.0, 0.0, T.t.x + Rc.x, T.t.y + Rc.y, T.t.z + Rc.z};
+    for (int r = 0; r < 6; ++r) P[r * kCoarseDim + 6] = sc[r];
   }
 }
 
@@ -1526,6 +1565,13 @@ void TwoLevelPcg::set_pattern(const int* row_ptr, const int* col, int nnzb, cuda
   rowseg_.upload(rowseg.data(), rowseg.size(), s);
   cta_cluster_.upload(cta_cluster.data(), cta_cluster.size(), s);
   cluster_cta0_.upload(cluster_cta0.data(), cluster_cta0.size(), s);
+  {  // frames of each cluster (the coarse basis is taken about their centroid)
+    std::vector<int> cluster_row0(nc_ + 1);
+    for (int k = 0; k <= nc_; ++k) cluster_row0[k] = row0[cluster_cta0[k]];
+    cluster_row0_.upload(cluster_row0.data(), cluster_row0.size(), s);
+    frame_cluster_.upload(frame_cluster.data(), frame_cluster.size(), s);
+    cen_.resize((size_t)3 * nc_);
+  }
 
   mark("uploads");
   Minv_.resize((size_t)nf_ * 36);
@@ -1608,7 +1654,9 @@ void TwoLevelPcg::set_basis(const int* free_frame, const double* q, const double
   if (lin_count_++ % refresh_ != 0) return;
   coarse_valid_ = false;
   ProfScope ps(*prof, "coarse_basis", 0.0, s);
-  k_coarse_basis<<<grid_for(nf_, 128), 128, 0, s>>>(nf_, free_frame, q, t, Rt, Pm_.get());
+  k_cluster_centroid<<<grid_for(nc_, 128), 128, 0, s>>>(nc_, cluster_row0_.get(), free_frame, t, Rt, cen_.get());
+  k_coarse_basis<<<grid_for(nf_, 128), 128, 0, s>>>(nf_, free_frame, frame_cluster_.get(), cen_.get(), q, t, Rt,
+                                                     Pm_.get());
 }
 
 void TwoLevelPcg::solve(const PcgProblem& p, int max_it, double rtol, BAScalars* sc, cudaStream_t s,

@@ -140,6 +140,8 @@ class TwoLevelPcg {
   DevBuf<double> Minv_, Pm_, Ac_[2], gjpiv_, r_, z_, p_, q_, rpart_, part_;
   DevBuf<int2> pair_cd_, rowseg_, wres_;
   DevBuf<int> pair_ptr_, cta_row0_, cta_cluster_, cluster_cta0_, zl_ptr_, zl_, lcol_;
+  DevBuf<int> cluster_row0_, frame_cluster_;  // frames of each coarse cluster, cluster of each frame
+  DevBuf<double> cen_;                        // [nc*3] cluster centroids (coarse basis origin)
   DevBuf<int4> runs_, wchunk_;
 };
 
