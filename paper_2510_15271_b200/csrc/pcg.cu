@@ -1484,7 +1484,7 @@ void TwoLevelPcg::set_pattern(const int* row_ptr, const int* col, int nnzb, cuda
   }
   mark("z cache");
   // ---- coarse clusters = groups of consecutive CTAs -------------------------
-  const bool two = cluster_ > 0;
+  bool two = cluster_ > 0;
   nc_ = two ? std::min(G, std::max(1, (nf_ + cluster_ - 1) / cluster_)) : 1;
   // clusters never straddle a rank: each rank gets its share of them
   std::vector<int> rank_nc0(1, 0);
@@ -1500,6 +1500,34 @@ void TwoLevelPcg::set_pattern(const int* row_ptr, const int* col, int nnzb, cuda
     for (int k = 0; k < nr; ++k) cluster_cta0[k0 + k] = ca + (int)((int64_t)gr * k / nr);
   }
   cluster_cta0[nc_] = G;
+  if (two && kCoarseDim > 6) {
+    // one frame spans only 6 of a cluster's kCoarseDim columns (A_c would be
+    // singular): a cluster of fewer than 2 frames joins the next one of its
+    // rank (the last one of a rank joins the previous); a rank of one frame
+    // leaves the solve on block-Jacobi
+    std::vector<int> cta0, rnc(1, 0);
+    for (int r = 0; r < R; ++r) {
+      const int kb = rank_nc0[r], ke = rank_nc0[r + 1], rend = cluster_cta0[ke];
+      const size_t first = cta0.size();
+      int start = cluster_cta0[kb];
+      for (int k = kb; k < ke; ++k) {
+        const int end = cluster_cta0[k + 1];
+        if (row0[end] - row0[start] >= 2) {
+          cta0.push_back(start);
+          start = end;
+        }
+      }
+      if (start != rend && cta0.size() == first) cta0.push_back(start);  // else: the previous cluster absorbs it
+      if (row0[rend] - row0[cluster_cta0[kb]] < 2) two = false;
+      rnc.push_back((int)cta0.size());
+    }
+    cta0.push_back(G);
+    nc_ = (int)cta0.size() - 1;
+    cluster_cta0 = cta0;
+    rank_nc0 = rnc;
+    cta_cluster.assign(G, 0);
+    frame_cluster.assign(nf_, 0);
+  }
   for (int k = 0; k < nc_; ++k)
     for (int c = cluster_cta0[k]; c < cluster_cta0[k + 1]; ++c) {
       cta_cluster[c] = k;

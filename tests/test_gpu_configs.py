@@ -415,3 +415,22 @@ def test_config3_sharded_matches_single_rank(n_shards):
     scale = np.abs(X1).max()
     np.testing.assert_allclose(Xs, X1, atol=1e-9 * scale)
     np.testing.assert_allclose(qs, q1, atol=1e-10)
+
+
+@pytest.mark.parametrize("cluster", [1, 2])
+def test_tiny_coarse_clusters_match_oracle(cluster):
+    """coarse_cluster 1 / 2: clusters of one frame cannot carry the 7 coarse
+    columns (rigid motions + scale); the plan folds them into neighbours and
+    the solve still matches the oracle's exact steps."""
+    from paper_2510_15271_b200.mapping import solve_arrays
+    from paper_2510_15271_b200.scenes import make_scene, scene_arrays
+    from paper_2510_15271_b200.solver import DeviceOptions, RobustLoss, SolverOptions
+    a = scene_arrays(make_scene(120, 20000, 100000, shape="venice", seed=3))
+    qo, to, Xo, ro = oracle_problem(a).solve(1, 2.0, 3)
+    q, t, X, rep, raw = solve_arrays(a, RobustLoss("huber", 2.0), SolverOptions(max_iters=3),
+                                     DeviceOptions(linear_solver="pcg", pcg_rtol=1e-10, coarse_cluster=cluster))
+    assert raw.pcg_max_hit == 0
+    assert rep.iterations == ro["iterations"] == 3
+    assert rep.final_cost == pytest.approx(ro["final_cost"], rel=1e-9)
+    scale = np.abs(Xo).max()
+    np.testing.assert_allclose(X, Xo, atol=1e-7 * scale)
