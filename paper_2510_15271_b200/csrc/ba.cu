@@ -2436,8 +2436,13 @@ bool BASolver::solve_implicit(double lam) {
   }
   constexpr int kChunk = 4, kMaxIt = 12;
   ImpState h{};
-  for (int done_it = 0; done_it < kMaxIt; done_it += kChunk) {
-    for (int k = 0; k < kChunk; ++k) {
+  // iterations are enqueued in chunks with one host check each (a converged
+  // solve turns the rest of its chunk into early-exit launches); the first
+  // chunk is as long as the previous trial needed (<= 3: why this path was
+  // taken), so a tail trial of 1-2 iterations launches 1-2 rounds, not 4
+  int chunk = std::max(1, std::min(kChunk, last_pcg_));
+  for (int done_it = 0; done_it < kMaxIt; done_it += chunk, chunk = kChunk) {
+    for (int k = 0; k < chunk && done_it + k < kMaxIt; ++k) {
       {
         ProfScope ps(*prof_, "imp_point", 36.0 * N_ + 136.0 * P_, s);
         k_imp_point<<<grid_for(std::max<int64_t>(P_, 1), kBlock), kBlock, 0, s>>>(
