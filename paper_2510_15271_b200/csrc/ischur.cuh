@@ -108,8 +108,12 @@ __global__ void __launch_bounds__(kImpWarps * 32) k_imp_cam(ImpCamArgs a) {
   const sfm_camera_model cm = a.models[a.frame_model[f]];
   const int64_t k0 = a.cm_ptr[j], k1 = a.cm_ptr[j + 1];
   double acc[6] = {0, 0, 0, 0, 0, 0};
-  for (int64_t k = k0 + threadIdx.x; k < k1; k += kImpWarps * 32) {
-    const int pt = __ldg(a.cm_pt + k);
+  constexpr int kStride = kImpWarps * 32;
+  int64_t k = k0 + threadIdx.x;
+  int pt_nx = k < k1 ? __ldg(a.cm_pt + k) : 0;  // the next observation's point, one iteration ahead
+  for (; k < k1; k += kStride) {
+    const int pt = pt_nx;
+    if (k + kStride < k1) pt_nx = __ldg(a.cm_pt + k + kStride);
     const double* vi = a.v + (int64_t)pt * a.vstride + a.voff;
     const double v0 = __ldg(vi), v1 = __ldg(vi + 1), v2 = __ldg(vi + 2);
     double Jc[12], Jp[6];
