@@ -771,7 +771,13 @@ __device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, dou
 // the warp contracts them on the fp64 tensor cores (two pairs per
 // DMMA.8x8x4, fixed order, so the sum is bit-reproducible).  The lambda_c
 // edge block is added on rank 0 and both BSR triangles written.
-constexpr int kOffWarps = 4;
+// One-warp CTAs, 20 per SM: measured 0.483 ms vs 0.496 with four-warp CTAs
+// (5 per SM) and 0.590 with eight (same bits; a finer grain lets a finished
+// block's slot refill without waiting for its CTA's other warps).
+#ifndef SFM_OFF_WARPS
+#define SFM_OFF_WARPS 1
+#endif
+constexpr int kOffWarps = SFM_OFF_WARPS;
 constexpr int kOffLd = 13;  // padded row of the staged factors (bank spread)
 constexpr int kOffRows = 32;
 constexpr size_t kOffSmem = sizeof(double) * kOffWarps * 2 * kOffRows * kOffLd;
@@ -798,7 +804,7 @@ __global__ void k_off_records(int n, const int* __restrict__ work, const unsigne
 }
 
 #ifndef SFM_OFF_MINB
-#define SFM_OFF_MINB 5
+#define SFM_OFF_MINB 20
 #endif
 #ifndef SFM_CAM_MINB
 #define SFM_CAM_MINB 5
