@@ -17,6 +17,7 @@
 // the pair hypotheses, a warp arg-max with a lowest-index tie-break
 // reproduces the reference's sequential "first best" rule.
 #include <cmath>
+#include <cstdlib>
 
 #include "sfm_math.cuh"
 #include "tri.cuh"
@@ -872,7 +873,9 @@ __global__ void __launch_bounds__(kRansacWarps * 32) k_ransac_packed(TrackArgs a
 // than one track per warp (configs[1], k ~ 9: 47.8 vs 38.8 ms; configs[3],
 // k ~ 5: 191 vs 395 ms packed).
 void launch_ransac(const TrackArgs& a, int64_t n_obs, cudaStream_t s) {
-  if (SFM_RANSAC_PACK && 2 * n_obs <= 11 * a.T) {
+  bool packed = SFM_RANSAC_PACK && 2 * n_obs <= 11 * a.T;
+  if (const char* e = std::getenv("SFM_RANSAC_PACKED")) packed = std::atoi(e) != 0;  // tests: force either kernel
+  if (packed) {
     const int64_t warps = (a.T + kPack - 1) / kPack;
     k_ransac_packed<<<grid_for(warps * 32, kRansacWarps * 32), kRansacWarps * 32, 0, s>>>(a);
   } else {

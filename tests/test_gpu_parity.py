@@ -145,9 +145,13 @@ def tracks_struct(d):
     return s, keep
 
 
+@pytest.mark.parametrize("packed", ["0", "1"])
 @pytest.mark.parametrize("case", ["dlt", "midpoint", "kinds_dlt", "kinds_midpoint"])
-def test_ransac_matches_reference(golden, case):
+def test_ransac_matches_reference(golden, case, packed, monkeypatch):
+    """Both RANSAC kernels (one track per warp; three short tracks per warp,
+    with the in-series fallback for chunks that do not fit) against sfmkit."""
     from paper_2510_15271_b200 import _native as nat
+    monkeypatch.setenv("SFM_RANSAC_PACKED", packed)
     method = case.split("_")[-1]
     d = golden("tri_" + case)
     s, keep = tracks_struct(d)
