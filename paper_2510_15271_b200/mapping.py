@@ -22,6 +22,8 @@ from __future__ import annotations
 
 import ctypes
 from dataclasses import dataclass, field
+from itertools import chain
+from operator import attrgetter
 
 import numpy as np
 
@@ -298,6 +300,14 @@ def _check_supported(sparse_map, frames, mode):
                                   "(general two-slot path)")
 
 
+_get_track = attrgetter("track")
+_get_observations = attrgetter("observations")
+_get_inlier_mask = attrgetter("inlier_mask")
+_get_frame_id = attrgetter("frame_id")
+_get_pixel = attrgetter("pixel")
+_get_position = attrgetter("position")
+
+
 def flatten_ba(sparse_map, config, stage=1, mode=PURE):
     """SparseMap -> (BAArrays, frames, landmark indices, loss).
 
@@ -328,21 +338,24 @@ def flatten_ba(sparse_map, config, stage=1, mode=PURE):
     fixed_arr = np.array([1 if f in fixed else 0 for f in frames], dtype=np.uint8)
     lms = [li for li, lm in enumerate(sparse_map.landmarks) if lm.track.status == TRIANGULATED]
     sel = [sparse_map.landmarks[li] for li in lms]
-    points = np.array([lm.position for lm in sel], dtype=np.float64).reshape(-1, 3)
+    points = np.array(list(map(_get_position, sel)), dtype=np.float64).reshape(-1, 3)
     # inlier observations, landmark-major in track order (mapping.py:452-475),
     # gathered with one pass over the objects and numpy for the rest
-    allobs = [o for lm in sel for o in lm.track.observations]
-    counts = np.fromiter((len(lm.track.observations) for lm in sel), dtype=np.int64, count=len(sel))
-    keep = (np.concatenate([np.asarray(lm.inlier_mask, dtype=bool) for lm in sel])
+    # (attribute getters mapped in C: the per-object Python work is the cost here)
+    tracks = list(map(_get_track, sel))
+    obs_lists = list(map(_get_observations, tracks))
+    allobs = list(chain.from_iterable(obs_lists))
+    counts = np.fromiter(map(len, obs_lists), dtype=np.int64, count=len(sel))
+    keep = (np.concatenate(list(map(_get_inlier_mask, sel))).astype(bool, copy=False)
             if sel else np.zeros(0, bool))
-    fids = np.fromiter((o.frame_id for o in allobs), dtype=np.int64, count=len(allobs))
+    fids = np.fromiter(map(_get_frame_id, allobs), dtype=np.int64, count=len(allobs))
     frame_arr = np.asarray(frames, dtype=np.int64)
     at = np.searchsorted(frame_arr, fids)
     bad = (at >= len(frame_arr)) | (frame_arr[np.minimum(at, max(len(frame_arr) - 1, 0))] != fids) \
         if len(frame_arr) else np.ones(len(fids), bool)
     if np.any(bad & keep):
         raise KeyError(int(fids[np.flatnonzero(bad & keep)[0]]))
-    pix = (np.concatenate([o.pixel for o in allobs]).reshape(-1, 2) if allobs
+    pix = (np.array(list(map(_get_pixel, allobs)), dtype=np.float64).reshape(-1, 2) if allobs
            else np.zeros((0, 2)))
     of = at[keep]
     op = np.repeat(np.arange(len(sel), dtype=np.int64), counts)[keep]
