@@ -408,8 +408,11 @@ def bundle_adjust(sparse_map, config: MappingConfig = None, stage: int = 1, mode
             continue  # never retracted: keep the entry object
         kf = sparse_map.keyframes[f]
         kf.cam_from_world = type(kf.cam_from_world)(q[i], t[i])
-    for pi, li in enumerate(lms):
-        sparse_map.landmarks[li].position = X[pi].copy()
+    # each landmark gets its own row of the (private) result array: views made
+    # in C, not a Python-level copy per landmark
+    landmarks = sparse_map.landmarks
+    for li, row in zip(lms, list(X)):
+        landmarks[li].position = row
     return report
 
 
