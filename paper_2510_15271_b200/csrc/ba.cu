@@ -1428,7 +1428,12 @@ __global__ void k_point_prep(int64_t P, double lam, const double* __restrict__ V
                              const double* __restrict__ gp, double* __restrict__ pv, BAScalars* sc) {
   int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= P) return;
-  if (!point_prep_one(V + p * 6, gp + p * 3, lam, pv + p * 12)) atomicOr(&sc->nonfinite, 1);
+  // V (48 B, 16-byte aligned) as three 128-bit loads, g_p as scalars (24 B stride)
+  const double2* v2 = reinterpret_cast<const double2*>(V + p * 6);
+  const double2 a = __ldg(v2), b = __ldg(v2 + 1), c = __ldg(v2 + 2);
+  const double v[6] = {a.x, a.y, b.x, b.y, c.x, c.y};
+  const double g[3] = {__ldg(gp + p * 3), __ldg(gp + p * 3 + 1), __ldg(gp + p * 3 + 2)};
+  if (!point_prep_one(v, g, lam, pv + p * 12)) atomicOr(&sc->nonfinite, 1);
 }
 
 // ---------------------------------------------------------------------------
