@@ -1704,7 +1704,7 @@ void TwoLevelPcg::solve(const PcgProblem& p, int max_it, double rtol, BAScalars*
   // The coarse operator A_c = P^T S(lam) P depends on the damping: S(lam)
   // has lam*D_c on its diagonal and (V + lam D_p)^-1 in its point term.  An
   // A_c assembled at lam_b and applied at lam >> lam_b over-weights the
-  // coarse correction P A_c^-1 P^T by up to lam/lam_b on the rigid-motion
+  // coarse correction P A_c^-1 P^T by up to lam/lam_b on the coarse
   // directions (and under-weights it for lam << lam_b), which wrecks the
   // conditioning of the preconditioned system -- the rejected-trial tail of
   // an LM solve climbs lam by 10x per trial up to 1e32.  So:
@@ -1715,7 +1715,7 @@ void TwoLevelPcg::solve(const PcgProblem& p, int max_it, double rtol, BAScalars*
   //     by more than drift_ (either way) from the lam it was built at, or the
   //     basis was refreshed (set_basis).
   //   Below lam_floor_ (1e-5) the damping is negligible next to the coarse
-  //   operator's own (rigid-motion) spectrum, so dampings under the floor
+  //   operator's own (coarse-space) spectrum, so dampings under the floor
   //   count as equal.  Config 3, LM iterations 1-14 (bench.py --max-iters 14,
   //   tools/ab_env.sh): floor 1e-6 / 1e-5 / 1e-4 -> 1504 / 1508 / 1548 PCG
   //   iterations and 2.42 / 1.82 / 1.21 ms of coarse inverses, 317 / 323 /

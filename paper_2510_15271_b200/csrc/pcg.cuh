@@ -7,9 +7,9 @@
 // with D the 6x6 block diagonal of S (block-Jacobi) and P the similarity
 // coarse space: cameras are aggregated into clusters of ~C consecutive free
 // frames (whole PCG CTA row ranges) and camera j's coarse basis is
-// [Adj(T_j) | (0, t_j)] -- a world-frame rigid motion and a world scaling of
-// the whole cluster, expressed as left perturbations (kCoarseDim = 7
-// columns).  A_c = P^T S P is assembled on device and inverted by a
+// [Adj(T_j) K_c | (0, t_j + R_j c)] -- a world-frame rigid motion of the
+// whole cluster about its camera centroid c and its scaling about c,
+// expressed as left perturbations (kCoarseDim = 7 columns).  A_c = P^T S P is assembled on device and inverted by a
 // cooperative blocked Gauss-Jordan.
 // The Krylov loop is one persistent cooperative kernel with two grid
 // barriers per iteration; every reduction has a fixed order.
@@ -111,7 +111,8 @@ class TwoLevelPcg {
   const std::vector<int>& rank_blocks() const { return rank_blk0_; }  // [world+1]
   // Coarse assembly runs from the (fixed) BSR pattern of S.
   void set_pattern(const int* row_ptr, const int* col, int nnzb, cudaStream_t s);
-  // Coarse basis P_j = Adj(T_j) from the linearisation-point poses.
+  // Coarse basis P_j (rigid motions + scale about the cluster centroid) from
+  // the linearisation-point poses.
   void set_basis(const int* free_frame, const double* q, const double* t, const double* Rt,
                  cudaStream_t s, Profiler* prof);
   // Coarse level only while lam <= lam_max; rebuilt when lam has drifted by
