@@ -9,8 +9,8 @@
 // frames (whole PCG CTA row ranges) and camera j's coarse basis is
 // [Adj(T_j) K_c | (0, t_j + R_j c)] -- a world-frame rigid motion of the
 // whole cluster about its camera centroid c and its scaling about c,
-// expressed as left perturbations (kCoarseDim = 7 columns).  A_c = P^T S P is assembled on device and inverted by a
-// cooperative blocked Gauss-Jordan.
+// expressed as left perturbations (kCoarseDim = 7 columns).  A_c = P^T S P
+// is assembled on device and inverted by a cooperative blocked Gauss-Jordan.
 // The Krylov loop is one persistent cooperative kernel with two grid
 // barriers per iteration; every reduction has a fixed order.
 #pragma once
